@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""bench.py -- FP64 SEM Ax+gs and Jacobi-PCG throughput on 1..8 B200 (one process per GPU).
+
+Metric (BASELINE.json): "FP64 Ax+gs GDOF/s and PCG iter/s at N=7, 1/2/4/8 B200,
+% of HBM roofline".  A STEP is one nek_pcg_solve of 100 fixed Jacobi-PCG
+iterations (every row of SURVEY 8(a) on the path: Ax, local gather-scatter, the
+halo exchange when N>1, the mask, the fused CG updates and dot-product
+reductions).  `value` is the BP5-style throughput of the whole job:
+    value = sum over ranks of n_dof * iterations / max-over-ranks device time,
+n_dof = E * N^3, in GDOF/s; pcg_iter_per_s = value / n_dof_total.
+Ax+gs GDOF/s (nek_ax alone) is reported in `ax_gs`.
+
+Workload at N=1: BASELINE configs[1] = 16^3 elements, N=7, bubble-deformed unit
+box, Dirichlet on all faces, Poisson (h1,h2) = (1,0), b = seeded smooth field.
+N>1: weak scaling, each rank owns one 16^3 z-slab of a 16 x 16 x 16N box.
+Inputs are resident in HBM when the timed region starts; L2 (126 MiB) is
+flushed between timed steps by writing a 256 MiB buffer (outside the events).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+       (N>1 via: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 Ax+gs GDOF/s and PCG iter/s at N=7, 1/2/4/8 B200, % of HBM roofline"
+ITERS = 100
+EX = EY = EZ_PER_RANK = 16
+NORD = 7
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters", type=int, default=ITERS)
+    ap.add_argument("--ez", type=int, default=EZ_PER_RANK, help="element layers per rank")
+    ap.add_argument("--order", type=int, default=NORD)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="time with the CUDA-graph PCG loop instead of "
+                    "eager launches + per-kernel events (no roofline then)")
+    return ap.parse_args()
+
+
+def rank_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def make_mesh(rank, world, ez, N):
+    from workloads import meshgen as mg
+    return mg.box_mesh(EX, EY, ez * world, N, deform="bubble", eps=0.05, dirichlet="all",
+                       zlayers=(rank * ez, (rank + 1) * ez))
+
+
+def workload_name(args, world):
+    return (f"SEM Poisson Jacobi-PCG, {args.iters} iters/step; {EX}x{EY}x{args.ez} elements per GPU "
+            f"(box {EX}x{EY}x{args.ez * world}, z-slabs), N={args.order}, bubble-deformed, Dirichlet all faces")
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(mesh, iters):
+    """The oracle as it stands, single-threaded C, on a bounded sample."""
+    import oracle
+    from workloads import meshgen as mg
+    O = oracle.Oracle.from_mesh(mesh)
+    b = mg.smooth_field(mesh, seed=1)
+    d = O.dinv(1.0, 0.0)
+    t0 = time.perf_counter()
+    O.pcg(1.0, 0.0, b, 0.0, iters, dinv=d)
+    dt = time.perf_counter() - t0
+    return {"value": mesh.n_dof * iters / dt / 1e9, "unit": "GDOF/s", "cores": 1, "kind": "oracle",
+            "sample": f"{iters} Jacobi-PCG iterations (incl. init) on the N=1 workload mesh, plain C oracle, 1 thread"}
+
+
+def run_reference(args):
+    rank, world, _ = rank_env()
+    if rank != 0:
+        return 0
+    mesh = make_mesh(0, 1, args.ez, args.order)
+    import oracle
+    from workloads import meshgen as mg
+    O = oracle.Oracle.from_mesh(mesh)
+    b = mg.smooth_field(mesh, seed=1)
+    d = O.dinv(1.0, 0.0)
+    it_per_step = 10
+    for _ in range(args.warmup):
+        O.pcg(1.0, 0.0, b, 0.0, it_per_step, dinv=d)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.pcg(1.0, 0.0, b, 0.0, it_per_step, dinv=d)
+    dt = time.perf_counter() - t0
+    val = mesh.n_dof * it_per_step * args.steps / dt / 1e9
+    sample = f"{it_per_step} Jacobi-PCG iterations per step on the N=1 workload mesh, plain C oracle, 1 thread"
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": val, "unit": "GDOF/s", "n_gpus": 1,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                      "data": "synthetic", "config": {"workload": workload_name(args, 1), "E": mesh.E,
+                                                      "N": mesh.N, "n_dof": mesh.n_dof},
+                      "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": 1, "kind": "oracle", "sample": sample},
+                      "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    rank, world, local = rank_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torch.distributed.run")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2409_19119_b200 import nek
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(nek.comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        comm = (rank, world, bytes(idt.cpu().numpy().tobytes()))
+    else:
+        dist = None
+        comm = None
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    mesh = make_mesh(rank, world, args.ez, args.order)
+    ctx = nek.setup(mesh.E, mesh.N, mesh.xyz, mesh.gid, mesh.mask, comm=comm, device=local)
+    info = nek.get_info(ctx)
+    from workloads import meshgen as mg
+    b = torch.from_numpy(mg.smooth_field(mesh, seed=1)).to(dev)
+    x = torch.zeros_like(b)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    timing = not args.graph
+    nek.set_timing(ctx, timing)
+
+    # warm-up (also builds the Jacobi diagonal and, with --graph, the CUDA graph)
+    for _ in range(args.warmup):
+        nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, args.iters)
+    torch.cuda.synchronize()
+    nek.get_stats(ctx, reset=True)
+
+    # ---- timed region: K PCG solves, each bracketed by events; L2 flushed between
+    clk = ClockSampler(local)
+    clk.start()
+    barrier(); torch.cuda.synchronize()
+    evs = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st, it, rr, _ = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, args.iters)
+        e1.record(stream)
+        evs.append((e0, e1))
+        assert it == args.iters, (st, it)
+    torch.cuda.synchronize(); barrier()
+    clocks = clk.stop()
+    t_ms = sum(a.elapsed_time(c) for a, c in evs)
+    stats = nek.get_stats(ctx, reset=True)
+
+    # ---- Ax+gs alone (nek_ax), same flush discipline
+    u = torch.from_numpy(mg.smooth_field(mesh, seed=2)).to(dev)
+    w = torch.empty_like(u)
+    for _ in range(3):
+        nek.ax(ctx, 1.0, 0.0, u, w)
+    reps = 20
+    barrier(); torch.cuda.synchronize()
+    ax_ms = 0.0
+    for _ in range(reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nek.ax(ctx, 1.0, 0.0, u, w)
+        e1.record(stream)
+        e1.synchronize()
+        ax_ms += e0.elapsed_time(e1)
+    barrier()
+    axstats = nek.get_stats(ctx, reset=True)
+
+    # ---- end to end through the public API with pinned host buffers
+    bh = torch.empty(mesh.n_local, dtype=torch.float64, pin_memory=True)
+    bh.copy_(b.cpu())
+    xh = torch.empty(mesh.n_local, dtype=torch.float64, pin_memory=True)
+    nek.set_timing(ctx, False)
+    nek.pcg_solve(ctx, 1.0, 0.0, bh, xh, 0.0, args.iters)
+    e2e_steps = max(1, min(args.steps, 5))
+    barrier(); torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        nek.pcg_solve(ctx, 1.0, 0.0, bh, xh, 0.0, args.iters)
+    torch.cuda.synchronize(); barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+
+    # ---- max over ranks
+    vals = torch.tensor([t_ms, ax_ms, e2e_s], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    t_ms, ax_ms, e2e_s = [float(v) for v in vals.cpu()]
+    n_dof_total = mesh.n_dof * world
+    value = n_dof_total * args.iters * args.steps / (t_ms * 1e-3) / 1e9
+    ax_gdofs = n_dof_total * reps / (ax_ms * 1e-3) / 1e9
+
+    if rank == 0:
+        P3 = (args.order + 1) ** 3
+        ax_bytes_per_elem = P3 * (8 + 48 + 8)     # u, 6 metric factors, w (Poisson: h2 = 0)
+        roofline = None
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        peak = peaks.get("hbm_gbs", 6650.0)
+        peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        if timing and stats["ax_launches"] > 0 and stats["ax_ms"] > 0:
+            per_launch_ms = stats["ax_ms"] / stats["ax_launches"]
+            per_launch_bytes = ax_bytes_per_elem * stats["ax_elements"] / stats["ax_launches"]
+            achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+            traffic = None
+            try:
+                tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+                traffic = tr.get(f"ax_N{args.order}_E{mesh.E}")
+            except Exception:
+                pass
+            roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "traffic": traffic, "kernel": "ax (SEM Helmholtz apply)", "peak_source": peak_src,
+                        "algorithmic_bytes_per_launch": per_launch_bytes, "avg_launch_ms": per_launch_ms,
+                        "share_of_step": stats["ax_ms"] / t_ms}
+        out = {
+            "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args, world), "E_per_gpu": mesh.E, "N": mesh.N,
+                       "n_dof_per_gpu": mesh.n_dof, "n_local_per_gpu": mesh.n_local,
+                       "pcg_iters_per_step": args.iters, "h1": 1.0, "h2": 0.0,
+                       "l2": "flushed between steps (256 MiB write outside the timed events)",
+                       "parallelism": f"dp{world} (element z-slabs, NCCL halo + allgather reductions)",
+                       "timing": "eager launches + per-kernel CUDA events" if timing else "CUDA graph"},
+            "pcg_iter_per_s": args.iters * args.steps / (t_ms * 1e-3),
+            "ax_gs": {"gdof_per_s": ax_gdofs, "ms_per_apply": ax_ms / reps,
+                      "algorithmic_GBps": (ax_bytes_per_elem * mesh.E * world / P3 * P3 + 0) * reps / (ax_ms * 1e-3) / 1e9},
+            "kernel_ms_per_step": {k: stats[k] / args.steps for k in ("ax_ms", "gs_ms", "halo_ms", "vec_ms")},
+            "gpu_launches": int(stats["launches"]),
+            "e2e": {"value": n_dof_total * args.iters / e2e_s / 1e9, "unit": "GDOF/s",
+                    "h2d_bytes_per_step": mesh.n_local * 8, "d2h_bytes_per_step": mesh.n_local * 8},
+            "roofline": roofline, "clocks": clocks,
+            "halo": {"doubles_per_gs": info["halo_doubles"], "neighbors": info["n_neighbors"]},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(mesh, 50)
+        print(json.dumps(out))
+    nek.free(ctx)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,243 @@
+/*
+ * nek.h -- C ABI of the B200-native SEM hot path (arXiv 2409.19119, NekRS).
+ *
+ * What it computes (PAPER.md = P:n, SPEC.md = S:n, readings = R#):
+ *   - the matrix-free spectral-element Helmholtz operator on hexahedra of order
+ *     N with GLL points,  w_e = h1 * D^T G_e D u_e + h2 * (wJ)_e u_e
+ *     (Eq. 3 and "fast tensor contractions ... O(N^4) work and
+ *     O(N^3) memory references"; P:148-151 the pressure Poisson system);
+ *   - the gather-scatter QQ^T (direct stiffness summation; "C0
+ *     continuity implies ... unit-depth stencils"), on one GPU and across GPUs
+ *     as an NCCL halo exchange overlapped with interior-element work
+ *     (P:391-398);
+ *   - Jacobi-preconditioned conjugate gradients with device-side
+ *     scalars and one reduction exchange per dot-product group.
+ * All arithmetic is FP64.
+ *
+ * Conventions common to every call:
+ *   E-vector: a field stored per element, length n_local = E*(N+1)^3, local
+ *   index l = e*(N+1)^3 + i + (N+1)*j + (N+1)^2*k, i (the r direction) fastest
+ *   ("local i-j-k indexing").
+ *   Field pointers (u, w, v, b, x) may be DEVICE pointers on the context's
+ *   device (used in stream order on `stream`, no host synchronisation) or HOST
+ *   pointers (pageable or pinned; the call then stages them through internal
+ *   device buffers and returns after the result is back in host memory).
+ *   `stream` is a cudaStream_t (NULL = the legacy default stream).
+ *   Multi-GPU (comm->nranks > 1): one process per GPU; every call below that
+ *   takes a context is COLLECTIVE -- all ranks make the same calls in the same
+ *   order.  Each rank passes only its own elements; a
+ *   node shared between ranks carries the same gid on every rank.
+ *   Ownership: the caller owns every array it passes; setup inputs are copied
+ *   (they may be freed after nek_setup returns); the library owns all internal
+ *   device memory until nek_free.  A context is not thread-safe.
+ *   Errors: every call returns a status code (never throws, never exits);
+ *   the message of the last failure is available from nek_errmsg(ctx), or from
+ *   nek_last_error() when no context exists.
+ */
+#ifndef NEK_H
+#define NEK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NEK_ABI_VERSION 1
+
+typedef struct nek_ctx nek_ctx;
+
+/* Status codes (SURVEY 8(b) error table). */
+enum {
+    NEK_OK = 0,        /* success                                                        */
+    NEK_MAXIT = 1,     /* PCG reached maxit; x holds the last iterate -- not an error */
+    NEK_EINVAL = -1,   /* bad argument (null pointer, E < 0, bad rank/size, ...)         */
+    NEK_EORDER = -2,   /* N outside [1, 15]                                      */
+    NEK_EGEOM = -3,    /* Jacobian J <= 0 at some node; message names element and node */
+    NEK_ETOPO = -4,    /* copies of one gid with different coordinates (> 1e-9 * diameter)
+                          or different Dirichlet flags             */
+    NEK_ENOTSPD = -5,  /* PCG found <p, A p> <= 0                                */
+    NEK_ENOMEM = -6,   /* device or host allocation failed                               */
+    NEK_ECUDA = -7,    /* CUDA runtime error (message has the CUDA error string)          */
+    NEK_ENCCL = -8,    /* NCCL error                                                     */
+    NEK_ENODEV = -9    /* no CUDA device / the library was built without this arch      */
+};
+
+/* Communicator for multi-GPU runs.  nranks == 1 (or a NULL comm) = single GPU,
+ * no NCCL.  nccl_id: the 128-byte ncclUniqueId produced on rank 0 by
+ * nek_comm_unique_id and broadcast to every rank by the caller (the Python
+ * binding uses torch.distributed). */
+typedef struct {
+    int rank;
+    int nranks;
+    unsigned char nccl_id[128];
+} nek_comm;
+
+int nek_version(void);                 /* returns NEK_ABI_VERSION */
+const char *nek_last_error(void);      /* message of the last failure without a context (thread-local) */
+
+/* Fill id[128] with a fresh NCCL unique id (call on rank 0 only).
+ * Returns NEK_OK or NEK_ENCCL. */
+int nek_comm_unique_id(unsigned char id[128]);
+
+/*
+ * nek_setup -- build a context for E local elements of order N.
+ *   xyz       HOST, [3][E*(N+1)^3] FP64: x, y, z of every GLL node of every
+ *             element (BASELINE north_star "vertex coordinates", read as all
+ *             GLL nodes -- R1; isoparametric map P:175-178).
+ *   gid       HOST, [E*(N+1)^3] int64 >= 0: global node id, equal on all copies
+ *             of a node (on all ranks).
+ *   dirichlet HOST, [E*(N+1)^3] uint8 or NULL: 1 = homogeneous Dirichlet node;
+ *             must agree on all copies (R6).
+ *   comm      NULL or nranks == 1 for one GPU; else see nek_comm.
+ *   device    CUDA device ordinal for this rank.
+ *   stream    stream for the setup kernels.
+ * Setup computes, on the device: the GLL rule and derivative matrix,
+ * the 6 symmetric geometric factors plus the Jacobian weight per point
+ * (G_ab = w_q J grad r_a . grad r_b, wJ = w_q J, R4), the canonical
+ * gather-scatter maps (R7) and, for nranks > 1, the halo plan (one setup
+ * collective: an allgather of element-surface gids).
+ * On success *out holds the context; on failure *out is NULL and the status is
+ * one of EINVAL, EORDER, EGEOM, ETOPO, ENOMEM, ECUDA, ENCCL, ENODEV.
+ */
+int nek_setup(nek_ctx **out, int64_t E, int N, const double *xyz, const int64_t *gid,
+              const uint8_t *dirichlet, const nek_comm *comm, int device, void *stream);
+
+/*
+ * nek_ax -- w = M QQ^T (h1 K_L + h2 B_L) M u  (R5, R6): the local stiffness
+ * apply sum_ab D_a^T G_ab D_b u_e plus h2 wJ u, the gather-scatter
+ * (local runs and, for nranks > 1, the halo exchange overlapped with the Ax of
+ * interior elements) and the Dirichlet mask on both sides.
+ * u and w: E-vectors (device or host), must not alias.
+ */
+int nek_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, void *stream);
+
+/*
+ * nek_gs -- v <- QQ^T v in place (global over all ranks).
+ * Copies of a node are summed left to right in ascending local index, and
+ * across ranks in ascending rank order (R7), so every copy on every rank gets
+ * identical bits; at nranks == 1 the result is bit-identical to the oracle.
+ */
+int nek_gs(nek_ctx *ctx, double *v, void *stream);
+
+/*
+ * nek_pcg_solve -- Jacobi-preconditioned CG for (h1 K + h2 B) x = b on the
+ * masked subspace, Hestenes-Stiefel form:
+ *   x0 = 0, r0 = M b, z = Dinv r, p = z, rho = <r,z>
+ *   repeat: stop if ||r|| <= tol ||M b||; w = A p; sigma = <p,w>; alpha = rho/sigma;
+ *           x += alpha p; r -= alpha w; rho' = <r, Dinv r>; beta = rho'/rho; p = Dinv r + beta p
+ * Dinv = M / diag(QQ^T (h1 K_L + h2 B_L)) uses the exact assembled diagonal (R10).
+ * <.,.> is the owner-copy inner product over unique global nodes (R8).
+ *   b, x      E-vectors (device or host); x is overwritten (x0 = 0, R11).
+ *   tol       relative residual tolerance (R9); tol = 0 runs exactly maxit iterations.
+ *   maxit     iteration cap (>= 0).
+ *   iters     out (host, nullable): iterations performed.
+ *   relres    out (host, nullable): ||r_k|| / ||M b|| at exit.
+ *   hist      out (host, nullable): maxit+1 entries, hist[k] = ||r_k||/||M b|| for k <= iters.
+ * Returns NEK_OK (converged; also b = 0 -> x = 0, iters = 0), NEK_MAXIT,
+ * NEK_ENOTSPD (x holds the last iterate), or an error.  The call synchronises
+ * `stream` (convergence is polled from the device every few iterations).
+ */
+int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x, double tol,
+                  int maxit, int *iters, double *relres, double *hist, void *stream);
+
+/* Release every resource of the context (collective for nranks > 1). NULL is a no-op. */
+int nek_free(nek_ctx *ctx);
+
+/* Message of the context's last failure ("" if none).  Valid until the next call. */
+const char *nek_errmsg(const nek_ctx *ctx);
+
+/* ----------------------------------------------------------- introspection */
+typedef struct {
+    int64_t E;                 /* local elements                                   */
+    int32_t N;                 /* polynomial order                                 */
+    int32_t rank, nranks;
+    int64_t n_local;           /* E*(N+1)^3                                        */
+    int64_t n_dof;             /* E*N^3, the paper's resolution count     */
+    int64_t n_masked;          /* local Dirichlet nodes                            */
+    int64_t n_runs;            /* local shared runs (local-only runs at nranks > 1) */
+    int64_t n_perm;            /* local copies in those runs                       */
+    int64_t n_ifc_runs;        /* runs whose gid is also on another rank           */
+    int64_t n_ifc_perm;        /* local copies in interface runs                   */
+    int64_t n_neighbors;       /* ranks sharing at least one gid with this rank    */
+    int64_t halo_doubles;      /* FP64 values sent (= received) per gather-scatter */
+    int64_t n_boundary_elems;  /* elements holding at least one interface node     */
+    int64_t device_bytes;      /* device memory held by the context                */
+    double  geom_min_jac;      /* min J over local nodes                           */
+} nek_info_t;
+
+int nek_get_info(const nek_ctx *ctx, nek_info_t *info);
+
+/* Copy the canonical local gather-scatter map to host arrays (R7):
+ * perm[n_perm] (int32 local indices, runs back to back), offs[n_runs+1]. */
+int nek_get_gs_map(const nek_ctx *ctx, int32_t *perm, int64_t *offs);
+
+/* Copy the geometric factors to host: G[E][6][(N+1)^3] (rr, rs, rt, ss, st, tt),
+ * wJ[E*(N+1)^3]. Either pointer may be NULL. */
+int nek_get_geom(const nek_ctx *ctx, double *G, double *wJ);
+
+/* Jacobi inverse diagonal Dinv = M / diag(QQ^T (h1 K_L + h2 B_L)) into an
+ * E-vector (device or host). */
+int nek_get_dinv(nek_ctx *ctx, double h1, double h2, double *dinv, void *stream);
+
+/* Per-kernel device timing (CUDA events on the library's stream).  When on,
+ * every kernel class launched by nek_ax / nek_gs / nek_pcg_solve is bracketed
+ * by events and its duration accumulated; nek_get_stats reads (and optionally
+ * resets) the totals.  Launch counts are always accumulated. */
+typedef struct {
+    double  ax_ms, gs_ms, halo_ms, vec_ms;    /* summed device time per kernel class */
+    int64_t ax_launches, gs_launches, halo_launches, vec_launches;
+    int64_t launches;                          /* all kernels launched by the library */
+    int64_t ax_elements;                       /* elements processed by Ax launches  */
+} nek_stats_t;
+
+int nek_set_timing(nek_ctx *ctx, int on);
+int nek_get_stats(nek_ctx *ctx, nek_stats_t *stats, int reset);
+
+/* Ax kernel variant selection (0 = default).  For experiments and tests. */
+int nek_set_variant(nek_ctx *ctx, int ax_variant);
+
+/* --------------------------------------------- host-only planning (no GPU) */
+/*
+ * The gather-scatter / halo plan is built by host code that needs no device;
+ * these calls expose it so multi-rank logic can be tested on CPU.
+ *
+ * nek_plan_create: local maps for E elements of order N (same inputs as
+ *   nek_setup; xyz may be NULL to skip the coordinate check).
+ * nek_plan_surface_gids: sorted unique gids on element surfaces; returns the
+ *   count, fills out[] when non-NULL.  These are what nek_setup allgathers.
+ * nek_plan_set_ranks: give rank/nranks and every rank's surface-gid list
+ *   (counts[nranks], lists[nranks] -> sorted int64 arrays); builds the halo plan.
+ * nek_plan_size / nek_plan_get: size (in elements) and contents of plan arrays:
+ */
+typedef struct nek_plan nek_plan;
+enum {
+    NEK_PLAN_PERM = 0,        /* int32  local-only run copies (canonical order)           */
+    NEK_PLAN_OFFS = 1,        /* int64  local-only run offsets (n_runs+1)                 */
+    NEK_PLAN_IFC_PERM = 2,    /* int32  interface run copies                              */
+    NEK_PLAN_IFC_OFFS = 3,    /* int64  interface run offsets (n_ifc_runs+1)              */
+    NEK_PLAN_IFC_GID = 4,     /* int64  gid of each interface run                         */
+    NEK_PLAN_NEIGHBORS = 5,   /* int32  neighbour ranks, ascending                        */
+    NEK_PLAN_SEND_OFFS = 6,   /* int64  per-neighbour offsets into the send/recv slots    */
+    NEK_PLAN_SEND_RUN = 7,    /* int32  interface run packed into each send slot          */
+    NEK_PLAN_CONTRIB_OFFS = 8,/* int64  per interface run offsets into CONTRIB            */
+    NEK_PLAN_CONTRIB = 9,     /* int32  summands in ascending rank order: -1 = own partial,
+                                         s >= 0 = received slot s                         */
+    NEK_PLAN_OWNER = 10,      /* uint8  1 on the owner copy of every local node (R8)      */
+    NEK_PLAN_ELEM_ORDER = 11  /* int32  elements, boundary ones first                     */
+};
+int nek_plan_create(nek_plan **out, int64_t E, int N, const int64_t *gid, const uint8_t *dirichlet,
+                    const double *xyz);
+int64_t nek_plan_surface_gids(const nek_plan *plan, int64_t *out);
+int nek_plan_set_ranks(nek_plan *plan, int rank, int nranks, const int64_t *counts,
+                       const int64_t *const *lists);
+int64_t nek_plan_size(const nek_plan *plan, int what);
+int nek_plan_get(const nek_plan *plan, int what, void *out);
+const char *nek_plan_errmsg(const nek_plan *plan);
+void nek_plan_free(nek_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEK_H */

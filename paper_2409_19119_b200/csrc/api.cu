@@ -1,0 +1,701 @@
+// api.cu -- the C ABI (include/nek.h): setup, operator, gather-scatter, PCG.
+//
+// Orchestration only: every step of the path runs in the kernels of
+// kernels.cu (and NCCL for the cross-GPU exchange).  One internal stream
+// s_main carries the work of a call (forked from / joined to the caller's
+// stream with events); a second stream s_comm carries the NCCL halo so it
+// overlaps the Ax of interior elements.  PCG iterations are
+// captured once into a CUDA graph and replayed (no host synchronisation
+// inside the loop except the periodic convergence poll).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nek.h"
+#include "nek_ctx.h"
+
+using namespace nekb200;
+
+static thread_local std::string g_last_error;
+
+static int fail(nek_ctx *ctx, int code, const std::string &msg)
+{
+    if (ctx) ctx->err = msg;
+    g_last_error = msg;
+    return code;
+}
+
+#define CK(call)                                                                                        \
+    do {                                                                                                \
+        cudaError_t _e = (call);                                                                        \
+        if (_e != cudaSuccess)                                                                          \
+            return fail(ctx, _e == cudaErrorMemoryAllocation ? NEK_ENOMEM : NEK_ECUDA,                  \
+                        std::string(#call) + ": " + cudaGetErrorString(_e));                            \
+    } while (0)
+#define NK(call)                                                                                        \
+    do {                                                                                                \
+        ncclResult_t _r = (call);                                                                       \
+        if (_r != ncclSuccess) return fail(ctx, NEK_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+template <class T>
+static cudaError_t dalloc(nek_ctx *ctx, T **p, int64_t count)
+{
+    *p = nullptr;
+    if (count <= 0) count = 1;
+    cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+    if (e == cudaSuccess) ctx->device_bytes += sizeof(T) * count;
+    return e;
+}
+
+template <class T>
+static cudaError_t upload(nek_ctx *ctx, T **p, const std::vector<T> &v)
+{
+    cudaError_t e = dalloc(ctx, p, (int64_t)v.size());
+    if (e != cudaSuccess || v.empty()) return e;
+    return cudaMemcpy(*p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+}
+
+static bool is_device_ptr(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static std::vector<uint32_t> pack_bits(const std::vector<uint8_t> &v)
+{
+    std::vector<uint32_t> b((v.size() + 31) / 32 + 1, 0u);
+    for (size_t l = 0; l < v.size(); ++l)
+        if (v[l]) b[l >> 5] |= 1u << (l & 31);
+    return b;
+}
+
+// ------------------------------------------------------------ timing pool
+namespace {
+struct TimedLaunch { int cls; cudaEvent_t a, b; };
+struct TimerPool {
+    std::vector<cudaEvent_t> free_ev;
+    std::vector<TimedLaunch> pending;
+};
+}  // namespace
+static TimerPool &pool_of(nek_ctx *ctx)
+{
+    static thread_local std::vector<std::pair<nek_ctx *, TimerPool>> pools;
+    for (auto &p : pools) if (p.first == ctx) return p.second;
+    pools.push_back({ctx, TimerPool()});
+    return pools.back().second;
+}
+static cudaEvent_t take_event(nek_ctx *ctx)
+{
+    TimerPool &P = pool_of(ctx);
+    if (!P.free_ev.empty()) { cudaEvent_t e = P.free_ev.back(); P.free_ev.pop_back(); return e; }
+    cudaEvent_t e; cudaEventCreate(&e); return e;
+}
+enum { CLS_AX = 0, CLS_GS = 1, CLS_HALO = 2, CLS_VEC = 3 };
+struct Scope {
+    nek_ctx *ctx; int cls; cudaEvent_t a = nullptr;
+    Scope(nek_ctx *c, int k) : ctx(c), cls(k) {
+        if (ctx->timing) { a = take_event(ctx); cudaEventRecord(a, ctx->s_main); }
+    }
+    ~Scope() {
+        if (ctx->timing) {
+            cudaEvent_t b = take_event(ctx);
+            cudaEventRecord(b, ctx->s_main);
+            pool_of(ctx).pending.push_back({cls, a, b});
+        }
+    }
+};
+static void harvest_timers(nek_ctx *ctx)
+{
+    TimerPool &P = pool_of(ctx);
+    for (auto &t : P.pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(t.b);
+        if (cudaEventElapsedTime(&ms, t.a, t.b) != cudaSuccess) { cudaGetLastError(); ms = 0.f; }
+        double *dst = t.cls == CLS_AX ? &ctx->stats.ax_ms : t.cls == CLS_GS ? &ctx->stats.gs_ms
+                    : t.cls == CLS_HALO ? &ctx->stats.halo_ms : &ctx->stats.vec_ms;
+        *dst += ms;
+        P.free_ev.push_back(t.a); P.free_ev.push_back(t.b);
+    }
+    P.pending.clear();
+}
+
+// ------------------------------------------------------------ building blocks
+static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, double *part, const int *done,
+                 int64_t nelem, int64_t eoff, const int32_t *elist)
+{
+    Scope sc(ctx, CLS_AX);
+    int nl = 0;
+    CK(launch_ax(ctx->variant, ctx->N, nelem, eoff, elist, u, ctx->G, ctx->wJ, ctx->mbits, h1, h2, w, part, done,
+                 ctx->s_main, &nl));
+    ctx->stats.ax_launches += nl;
+    ctx->stats.launches += nl;
+    ctx->stats.ax_elements += nelem;
+    return NEK_OK;
+}
+
+static int halo_start(nek_ctx *ctx, const double *v, const int *done)
+{
+    {
+        Scope sc(ctx, CLS_HALO);
+        CK(launch_gs_ifc_pack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots,
+                              ctx->send_run, ctx->sendbuf, done, ctx->s_main));
+        ctx->stats.launches += (ctx->nifc > 0) + (ctx->nslots > 0);
+        ctx->stats.halo_launches += 1;
+    }
+    CK(cudaEventRecord(ctx->ev_fork, ctx->s_main));
+    CK(cudaStreamWaitEvent(ctx->s_comm, ctx->ev_fork, 0));
+    NK(ncclGroupStart());
+    for (size_t k = 0; k < ctx->neighbors.size(); ++k) {
+        size_t cnt = (size_t)(ctx->send_offs[k + 1] - ctx->send_offs[k]);
+        NK(ncclSend(ctx->sendbuf + ctx->send_offs[k], cnt, ncclDouble, ctx->neighbors[k], ctx->nccl, ctx->s_comm));
+        NK(ncclRecv(ctx->recvbuf + ctx->send_offs[k], cnt, ncclDouble, ctx->neighbors[k], ctx->nccl, ctx->s_comm));
+    }
+    NK(ncclGroupEnd());
+    CK(cudaEventRecord(ctx->ev_join, ctx->s_comm));
+    return NEK_OK;
+}
+
+static int halo_finish(nek_ctx *ctx, double *v, const int *done)
+{
+    CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_join, 0));
+    Scope sc(ctx, CLS_HALO);
+    CK(launch_gs_ifc_unpack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, ctx->coffs, ctx->contrib, ctx->ifc_partial,
+                            ctx->recvbuf, v, done, ctx->s_main));
+    ctx->stats.launches += (ctx->nifc > 0);
+    return NEK_OK;
+}
+
+static int do_gs_local(nek_ctx *ctx, double *v, const int *done)
+{
+    Scope sc(ctx, CLS_GS);
+    CK(launch_gs_local(ctx->nruns, ctx->perm, ctx->offs, v, done, ctx->s_main));
+    ctx->stats.gs_launches += 1;
+    ctx->stats.launches += (ctx->nruns > 0);
+    return NEK_OK;
+}
+
+// v <- QQ^T v (global)
+static int gs_full(nek_ctx *ctx, double *v, const int *done)
+{
+    int st;
+    if (ctx->nranks > 1 && (st = halo_start(ctx, v, done)) != NEK_OK) return st;
+    if ((st = do_gs_local(ctx, v, done)) != NEK_OK) return st;
+    if (ctx->nranks > 1 && (st = halo_finish(ctx, v, done)) != NEK_OK) return st;
+    return NEK_OK;
+}
+
+// w = M QQ^T (h1 K_L + h2 B_L) M u; block partials of <M u, A_L M u> into part (nullable).
+static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, double *part, const int *done)
+{
+    int st;
+    if (ctx->nranks == 1) {
+        if ((st = do_ax(ctx, h1, h2, u, w, part, done, ctx->E, 0, nullptr)) != NEK_OK) return st;
+        return do_gs_local(ctx, w, done);
+    }
+    if ((st = do_ax(ctx, h1, h2, u, w, part, done, ctx->n_boundary, 0, ctx->elist)) != NEK_OK) return st;
+    if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
+    if ((st = do_ax(ctx, h1, h2, u, w, part, done, ctx->E - ctx->n_boundary, ctx->n_boundary, ctx->elist)) != NEK_OK)
+        return st;
+    if ((st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
+    return halo_finish(ctx, w, done);
+}
+
+static int reduce_slots(nek_ctx *ctx, const double *part, int64_t count, int nd, int slot, const int *done)
+{
+    {
+        Scope sc(ctx, CLS_VEC);
+        CK(launch_reduce(part, count, nd, ctx->red_loc + slot, done, ctx->s_main));
+        ctx->stats.launches += 1;
+        ctx->stats.vec_launches += 1;
+    }
+    if (ctx->nranks > 1) NK(ncclAllGather(ctx->red_loc, ctx->red_all, RED_N, ncclDouble, ctx->nccl, ctx->s_main));
+    return NEK_OK;
+}
+
+static void enter(nek_ctx *ctx, void *stream)
+{
+    cudaEventRecord(ctx->ev_in, (cudaStream_t)stream);
+    cudaStreamWaitEvent(ctx->s_main, ctx->ev_in, 0);
+}
+static void leave(nek_ctx *ctx, void *stream)
+{
+    cudaEventRecord(ctx->ev_out, ctx->s_main);
+    cudaStreamWaitEvent((cudaStream_t)stream, ctx->ev_out, 0);
+}
+
+static int ensure_stage(nek_ctx *ctx)
+{
+    if (!ctx->stage_in) CK(dalloc(ctx, &ctx->stage_in, ctx->n));
+    if (!ctx->stage_out) CK(dalloc(ctx, &ctx->stage_out, ctx->n));
+    return NEK_OK;
+}
+
+static int ensure_dinv(nek_ctx *ctx, double h1, double h2)
+{
+    if (ctx->dinv_valid && ctx->dinv_h1 == h1 && ctx->dinv_h2 == h2) return NEK_OK;
+    CK(launch_diag(ctx->N, ctx->E, ctx->G, ctx->wJ, h1, h2, ctx->vtmp, ctx->s_main));
+    int st = gs_full(ctx, ctx->vtmp, nullptr);
+    if (st != NEK_OK) return st;
+    CK(launch_dinv(ctx->n, ctx->mbits, ctx->vtmp, ctx->vdinv, ctx->s_main));
+    ctx->stats.launches += 2;
+    ctx->dinv_valid = true; ctx->dinv_h1 = h1; ctx->dinv_h2 = h2;
+    if (ctx->graph && (ctx->graph_h1 != h1 || ctx->graph_h2 != h2)) {
+        cudaGraphExecDestroy(ctx->graph);
+        ctx->graph = nullptr;
+    }
+    return NEK_OK;
+}
+
+// ------------------------------------------------------------------- ABI
+extern "C" {
+
+int nek_version(void) { return NEK_ABI_VERSION; }
+const char *nek_last_error(void) { return g_last_error.c_str(); }
+const char *nek_errmsg(const nek_ctx *ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int nek_comm_unique_id(unsigned char id[128])
+{
+    nek_ctx *ctx = nullptr;
+    if (!id) return fail(ctx, NEK_EINVAL, "null id");
+    ncclUniqueId u;
+    NK(ncclGetUniqueId(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    std::memcpy(id, &u, 128);
+    return NEK_OK;
+}
+
+static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const int64_t *gid,
+                      const uint8_t *dirichlet, const nek_comm *comm, void *stream)
+{
+    if (N < 1 || N > 15) return fail(ctx, NEK_EORDER, "order N=" + std::to_string(N) + " outside [1,15]");
+    if (E < 0 || (E > 0 && (!xyz || !gid))) return fail(ctx, NEK_EINVAL, "E < 0 or null xyz/gid");
+    if (comm && comm->nranks > 1 && (comm->rank < 0 || comm->rank >= comm->nranks))
+        return fail(ctx, NEK_EINVAL, "bad rank");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { cudaGetLastError(); return fail(ctx, NEK_ENODEV, "no CUDA device"); }
+    if (ctx->device < 0 || ctx->device >= ndev) return fail(ctx, NEK_EINVAL, "bad device ordinal");
+    CK(cudaSetDevice(ctx->device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, ctx->device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(ctx, NEK_ENODEV, std::string("library built for sm_100a only; device is ") + prop.name);
+
+    ctx->E = E; ctx->N = N; ctx->Nq = N + 1; ctx->P3 = ctx->Nq * ctx->Nq * ctx->Nq; ctx->n = E * ctx->P3;
+    ctx->rank = comm && comm->nranks > 1 ? comm->rank : 0;
+    ctx->nranks = comm && comm->nranks > 1 ? comm->nranks : 1;
+
+    // host planning (local maps + validation)
+    nek_plan *p = nullptr;
+    int st = nek_plan_create(&p, E, N, gid, dirichlet, xyz);
+    ctx->plan = p;
+    if (st != NEK_OK) return fail(ctx, st, p ? p->err : "plan allocation failed");
+
+    CK(cudaStreamCreateWithFlags(&ctx->s_main, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->s_comm, cudaStreamNonBlocking));
+    for (cudaEvent_t *e : {&ctx->ev_in, &ctx->ev_out, &ctx->ev_fork, &ctx->ev_join})
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    enter(ctx, stream);
+
+    if (ctx->nranks > 1) {
+        ncclUniqueId uid;
+        std::memcpy(&uid, comm->nccl_id, 128);
+        NK(ncclCommInitRank(&ctx->nccl, ctx->nranks, uid, ctx->rank));
+        // setup collective: allgather of element-surface gids (sorted) of every rank
+        int64_t ns = nek_plan_surface_gids(p, nullptr);
+        std::vector<int64_t> mine(ns);
+        nek_plan_surface_gids(p, mine.data());
+        int64_t *dcnt = nullptr, *dall = nullptr, *dmine = nullptr;
+        CK(cudaMalloc(&dcnt, sizeof(int64_t) * (ctx->nranks + 1)));
+        CK(cudaMemcpy(dcnt + ctx->nranks, &ns, sizeof(int64_t), cudaMemcpyHostToDevice));
+        NK(ncclAllGather(dcnt + ctx->nranks, dcnt, 1, ncclInt64, ctx->nccl, ctx->s_main));
+        std::vector<int64_t> counts(ctx->nranks);
+        CK(cudaMemcpyAsync(counts.data(), dcnt, sizeof(int64_t) * ctx->nranks, cudaMemcpyDeviceToHost, ctx->s_main));
+        CK(cudaStreamSynchronize(ctx->s_main));
+        int64_t mx = 1;
+        for (auto c : counts) mx = std::max(mx, c);
+        CK(cudaMalloc(&dmine, sizeof(int64_t) * mx));
+        CK(cudaMalloc(&dall, sizeof(int64_t) * mx * ctx->nranks));
+        if (ns) CK(cudaMemcpy(dmine, mine.data(), sizeof(int64_t) * ns, cudaMemcpyHostToDevice));
+        NK(ncclAllGather(dmine, dall, (size_t)mx, ncclInt64, ctx->nccl, ctx->s_main));
+        std::vector<int64_t> all((size_t)mx * ctx->nranks);
+        CK(cudaMemcpyAsync(all.data(), dall, sizeof(int64_t) * all.size(), cudaMemcpyDeviceToHost, ctx->s_main));
+        CK(cudaStreamSynchronize(ctx->s_main));
+        cudaFree(dcnt); cudaFree(dall); cudaFree(dmine);
+        std::vector<const int64_t *> lists(ctx->nranks);
+        for (int q = 0; q < ctx->nranks; ++q) lists[q] = all.data() + (size_t)q * mx;
+        st = nek_plan_set_ranks(p, ctx->rank, ctx->nranks, counts.data(), lists.data());
+        if (st != NEK_OK) return fail(ctx, st, p->err);
+    }
+
+    // reference element
+    std::vector<double> x(N + 1), w(N + 1), D((N + 1) * (N + 1));
+    gll_rule(N, x.data(), w.data());
+    deriv_matrix(N, x.data(), D.data());
+    CK(upload_D(N, D.data()));
+
+    // maps -> device (int32 offsets: n_local < 2^31 is enforced by the plan)
+    auto to32 = [](const std::vector<int64_t> &v) { return std::vector<int32_t>(v.begin(), v.end()); };
+    ctx->nruns = (int64_t)p->offs.size() - 1; ctx->nperm = (int64_t)p->perm.size();
+    CK(upload(ctx, &ctx->perm, p->perm));
+    CK(upload(ctx, &ctx->offs, to32(p->offs)));
+    ctx->nifc = (int64_t)p->ifc_offs.size() - 1; ctx->nifc_perm = (int64_t)p->ifc_perm.size();
+    CK(upload(ctx, &ctx->ifc_perm, p->ifc_perm));
+    CK(upload(ctx, &ctx->ifc_offs, to32(p->ifc_offs)));
+    CK(upload(ctx, &ctx->send_run, p->send_run));
+    CK(upload(ctx, &ctx->coffs, to32(p->contrib_offs)));
+    CK(upload(ctx, &ctx->contrib, p->contrib));
+    ctx->nslots = (int64_t)p->send_run.size();
+    ctx->neighbors = p->neighbors;
+    ctx->send_offs = p->send_offs;
+    CK(dalloc(ctx, &ctx->ifc_partial, ctx->nifc));
+    CK(dalloc(ctx, &ctx->sendbuf, ctx->nslots));
+    CK(dalloc(ctx, &ctx->recvbuf, ctx->nslots));
+    CK(upload(ctx, &ctx->elist, p->elem_order));
+    ctx->n_boundary = p->n_boundary;
+    CK(upload(ctx, &ctx->mbits, pack_bits(p->mask)));
+    CK(upload(ctx, &ctx->obits, pack_bits(p->owner)));
+    ctx->n_masked = 0;
+    for (auto m : p->mask) ctx->n_masked += m;
+
+    // geometry
+    const int64_t n = ctx->n;
+    CK(dalloc(ctx, &ctx->G, 6 * n));
+    CK(dalloc(ctx, &ctx->wJ, n));
+    {
+        double *dxyz = nullptr, *dwq = nullptr;
+        unsigned long long *dbad = nullptr, hbad = ~0ull;
+        CK(cudaMalloc(&dxyz, sizeof(double) * 3 * std::max<int64_t>(n, 1)));
+        CK(cudaMalloc(&dwq, sizeof(double) * (N + 1)));
+        CK(cudaMalloc(&dbad, sizeof(unsigned long long)));
+        if (n) CK(cudaMemcpy(dxyz, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dwq, w.data(), sizeof(double) * (N + 1), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dbad, &hbad, sizeof(hbad), cudaMemcpyHostToDevice));
+        CK(launch_geom(N, E, dxyz, ctx->G, ctx->wJ, dwq, dbad, ctx->s_main));
+        CK(cudaMemcpyAsync(&hbad, dbad, sizeof(hbad), cudaMemcpyDeviceToHost, ctx->s_main));
+        CK(cudaStreamSynchronize(ctx->s_main));
+        cudaFree(dxyz); cudaFree(dwq); cudaFree(dbad);
+        if (hbad != ~0ull) {
+            int64_t l = (int64_t)hbad;
+            return fail(ctx, NEK_EGEOM, "non-positive Jacobian at element " + std::to_string(l / ctx->P3) +
+                                           ", node " + std::to_string(l % ctx->P3));
+        }
+    }
+    // work vectors, reductions, scalars
+    for (double **v : {&ctx->vr, &ctx->vp, &ctx->vw, &ctx->vx, &ctx->vdinv, &ctx->vtmp}) CK(dalloc(ctx, v, n));
+    ctx->npart = std::max<int64_t>(ax_partials_needed(ctx->variant, N, E), 2 * vec_blocks());
+    CK(dalloc(ctx, &ctx->part, ctx->npart));
+    CK(dalloc(ctx, &ctx->red_loc, RED_N));
+    if (ctx->nranks > 1) CK(dalloc(ctx, &ctx->red_all, RED_N * ctx->nranks));
+    else ctx->red_all = ctx->red_loc;
+    CK(dalloc(ctx, &ctx->sc, 1));
+    CK(cudaMallocHost(&ctx->sc_host, sizeof(PcgScalars)));
+    CK(dalloc(ctx, &ctx->counter, 1));
+    CK(cudaMemset(ctx->counter, 0, sizeof(unsigned int)));
+    CK(cudaMemset(ctx->red_loc, 0, sizeof(double) * RED_N));
+    CK(cudaStreamSynchronize(ctx->s_main));
+    leave(ctx, stream);
+    return NEK_OK;
+}
+
+int nek_setup(nek_ctx **out, int64_t E, int N, const double *xyz, const int64_t *gid, const uint8_t *dirichlet,
+              const nek_comm *comm, int device, void *stream)
+{
+    if (!out) return fail(nullptr, NEK_EINVAL, "null out");
+    *out = nullptr;
+    nek_ctx *ctx = new (std::nothrow) nek_ctx();
+    if (!ctx) return fail(nullptr, NEK_ENOMEM, "host allocation failed");
+    ctx->device = device;
+    int st;
+    try {
+        st = setup_impl(ctx, E, N, xyz, gid, dirichlet, comm, stream);
+    } catch (const std::bad_alloc &) {
+        st = fail(ctx, NEK_ENOMEM, "host allocation failed");
+    }
+    if (st != NEK_OK) {
+        g_last_error = ctx->err;
+        nek_free(ctx);
+        return st;
+    }
+    *out = ctx;
+    return NEK_OK;
+}
+
+int nek_free(nek_ctx *ctx)
+{
+    if (!ctx) return NEK_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->s_main) cudaStreamSynchronize(ctx->s_main);
+    if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+    for (void *p : {(void *)ctx->G, (void *)ctx->wJ, (void *)ctx->perm, (void *)ctx->offs, (void *)ctx->ifc_perm,
+                    (void *)ctx->ifc_offs, (void *)ctx->send_run, (void *)ctx->coffs, (void *)ctx->contrib,
+                    (void *)ctx->ifc_partial, (void *)ctx->sendbuf, (void *)ctx->recvbuf, (void *)ctx->elist,
+                    (void *)ctx->mbits, (void *)ctx->obits, (void *)ctx->vr, (void *)ctx->vp, (void *)ctx->vw,
+                    (void *)ctx->vx, (void *)ctx->vdinv, (void *)ctx->vtmp, (void *)ctx->stage_in,
+                    (void *)ctx->stage_out, (void *)ctx->part, (void *)ctx->red_loc, (void *)ctx->sc,
+                    (void *)ctx->counter, (void *)ctx->hist})
+        if (p) cudaFree(p);
+    if (ctx->red_all && ctx->red_all != ctx->red_loc) cudaFree(ctx->red_all);
+    if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
+    TimerPool &P = pool_of(ctx);
+    for (auto &t : P.pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+    for (auto e : P.free_ev) cudaEventDestroy(e);
+    P.pending.clear(); P.free_ev.clear();
+    for (cudaEvent_t e : {ctx->ev_in, ctx->ev_out, ctx->ev_fork, ctx->ev_join}) if (e) cudaEventDestroy(e);
+    if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+    if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
+    if (ctx->s_comm) cudaStreamDestroy(ctx->s_comm);
+    nek_plan_free(ctx->plan);
+    delete ctx;
+    return NEK_OK;
+}
+
+int nek_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, void *stream)
+{
+    if (!ctx) return fail(nullptr, NEK_EINVAL, "null ctx");
+    if (!u || !w || (const void *)u == (void *)w) return fail(ctx, NEK_EINVAL, "null or aliasing u/w");
+    CK(cudaSetDevice(ctx->device));
+    const bool du = is_device_ptr(u), dw = is_device_ptr(w);
+    int st;
+    enter(ctx, stream);
+    const double *ud = u;
+    double *wd = w;
+    if (!du || !dw) { if ((st = ensure_stage(ctx)) != NEK_OK) return st; }
+    if (!du) { CK(cudaMemcpyAsync(ctx->stage_in, u, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->s_main)); ud = ctx->stage_in; }
+    if (!dw) wd = ctx->stage_out;
+    if ((st = apply_op(ctx, h1, h2, ud, wd, nullptr, nullptr)) != NEK_OK) return st;
+    if (!dw) {
+        CK(cudaMemcpyAsync(w, wd, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
+        CK(cudaStreamSynchronize(ctx->s_main));
+    }
+    leave(ctx, stream);
+    return NEK_OK;
+}
+
+int nek_gs(nek_ctx *ctx, double *v, void *stream)
+{
+    if (!ctx) return fail(nullptr, NEK_EINVAL, "null ctx");
+    if (!v) return fail(ctx, NEK_EINVAL, "null v");
+    CK(cudaSetDevice(ctx->device));
+    const bool dv = is_device_ptr(v);
+    int st;
+    enter(ctx, stream);
+    double *vd = v;
+    if (!dv) {
+        if ((st = ensure_stage(ctx)) != NEK_OK) return st;
+        CK(cudaMemcpyAsync(ctx->stage_in, v, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->s_main));
+        vd = ctx->stage_in;
+    }
+    if ((st = gs_full(ctx, vd, nullptr)) != NEK_OK) return st;
+    if (!dv) {
+        CK(cudaMemcpyAsync(v, vd, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
+        CK(cudaStreamSynchronize(ctx->s_main));
+    }
+    leave(ctx, stream);
+    return NEK_OK;
+}
+
+// one PCG iteration (device-resident, skipped once sc->done is set)
+static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
+{
+    int st;
+    const int *done = &ctx->sc->done;
+    const int nb = vec_blocks();
+    if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, ctx->part, done)) != NEK_OK) return st;
+    if ((st = reduce_slots(ctx, ctx->part, ax_partials_needed(ctx->variant, ctx->N, ctx->E), 1, RED_SIGMA, done)) != NEK_OK)
+        return st;
+    {
+        Scope sc(ctx, CLS_VEC);
+        CK(launch_pcg_update(ctx->n, ctx->obits, ctx->vdinv, ctx->vp, ctx->vw, ctx->vx, ctx->vr, ctx->red_all,
+                             ctx->nranks, ctx->sc, ctx->part, nb, ctx->s_main));
+        ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
+    }
+    if ((st = reduce_slots(ctx, ctx->part, nb, 2, RED_RHO, done)) != NEK_OK) return st;
+    {
+        Scope sc(ctx, CLS_VEC);
+        CK(launch_pcg_pupdate(ctx->n, ctx->vdinv, ctx->vr, ctx->vp, ctx->red_all, ctx->nranks, ctx->sc, ctx->hist,
+                              ctx->counter, nb, ctx->s_main));
+        ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
+    }
+    return NEK_OK;
+}
+
+int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x, double tol, int maxit, int *iters,
+                  double *relres, double *hist, void *stream)
+{
+    if (!ctx) return fail(nullptr, NEK_EINVAL, "null ctx");
+    if (!b || !x || maxit < 0 || !(tol >= 0.0)) return fail(ctx, NEK_EINVAL, "bad b/x/maxit/tol");
+    CK(cudaSetDevice(ctx->device));
+    int st;
+    enter(ctx, stream);
+    if ((st = ensure_dinv(ctx, h1, h2)) != NEK_OK) return st;
+    if (ctx->hist_cap < maxit + 1) {
+        if (ctx->hist) cudaFree(ctx->hist);
+        ctx->hist = nullptr;
+        CK(dalloc(ctx, &ctx->hist, maxit + 1));
+        ctx->hist_cap = maxit + 1;
+        if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+    }
+    const bool db = is_device_ptr(b), dx = is_device_ptr(x);
+    const double *bd = b;
+    if (!db) {
+        if ((st = ensure_stage(ctx)) != NEK_OK) return st;
+        CK(cudaMemcpyAsync(ctx->stage_in, b, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->s_main));
+        bd = ctx->stage_in;
+    }
+    PcgScalars *H = ctx->sc_host;
+    std::memset(H, 0, sizeof(*H));
+    H->tol = tol; H->maxit = maxit;
+    CK(cudaMemcpyAsync(ctx->sc, H, sizeof(PcgScalars), cudaMemcpyHostToDevice, ctx->s_main));
+    const int nb = vec_blocks();
+    {
+        Scope sc(ctx, CLS_VEC);
+        CK(launch_pcg_init(ctx->n, ctx->mbits, ctx->obits, bd, ctx->vdinv, ctx->vr, ctx->vp, ctx->vx, ctx->part, nb,
+                           ctx->s_main));
+        ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
+    }
+    if ((st = reduce_slots(ctx, ctx->part, nb, 2, RED_RHO, nullptr)) != NEK_OK) return st;
+    CK(launch_pcg_init_fin(ctx->sc, ctx->red_all, ctx->nranks, ctx->hist, ctx->s_main));
+    ctx->stats.launches += 1;
+
+    const int C = std::max(1, std::min(maxit, 10));
+    const bool use_graph = !ctx->timing;
+    if (use_graph && (!ctx->graph || ctx->graph_iters != C || ctx->graph_h1 != h1 || ctx->graph_h2 != h2)) {
+        if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+        cudaGraph_t g;
+        nek_stats_t saved = ctx->stats;
+        CK(cudaStreamBeginCapture(ctx->s_main, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < C; ++k) {
+            if ((st = pcg_iteration(ctx, h1, h2)) != NEK_OK) {
+                cudaStreamEndCapture(ctx->s_main, &g);
+                return st;
+            }
+        }
+        CK(cudaStreamEndCapture(ctx->s_main, &g));
+        // launches recorded in one replay of the graph
+        ctx->graph_stats = ctx->stats;
+        ctx->graph_stats.launches -= saved.launches;
+        ctx->graph_stats.ax_launches -= saved.ax_launches;
+        ctx->graph_stats.ax_elements -= saved.ax_elements;
+        ctx->graph_stats.gs_launches -= saved.gs_launches;
+        ctx->graph_stats.halo_launches -= saved.halo_launches;
+        ctx->graph_stats.vec_launches -= saved.vec_launches;
+        ctx->stats = saved;
+        CK(cudaGraphInstantiate(&ctx->graph, g, 0));
+        cudaGraphDestroy(g);
+        ctx->graph_iters = C; ctx->graph_h1 = h1; ctx->graph_h2 = h2;
+    }
+    int launched = 0;
+    while (launched < maxit) {
+        if (use_graph) {
+            CK(cudaGraphLaunch(ctx->graph, ctx->s_main));
+            const nek_stats_t &g = ctx->graph_stats;
+            ctx->stats.launches += g.launches; ctx->stats.ax_launches += g.ax_launches;
+            ctx->stats.ax_elements += g.ax_elements; ctx->stats.gs_launches += g.gs_launches;
+            ctx->stats.halo_launches += g.halo_launches; ctx->stats.vec_launches += g.vec_launches;
+            launched += C;
+        } else {
+            if ((st = pcg_iteration(ctx, h1, h2)) != NEK_OK) return st;
+            launched += 1;
+        }
+        if (tol > 0.0 && (launched % (use_graph ? C : 10)) == 0) {
+            CK(cudaMemcpyAsync(H, ctx->sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, ctx->s_main));
+            CK(cudaStreamSynchronize(ctx->s_main));
+            if (H->done) break;
+        }
+    }
+    CK(cudaMemcpyAsync(H, ctx->sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, ctx->s_main));
+    if (dx) CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->s_main));
+    else CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
+    CK(cudaStreamSynchronize(ctx->s_main));
+    if (hist && H->iter >= 0)
+        CK(cudaMemcpy(hist, ctx->hist, sizeof(double) * (H->iter + 1), cudaMemcpyDeviceToHost));
+    if (ctx->timing) harvest_timers(ctx);
+    if (iters) *iters = H->iter;
+    if (relres) *relres = H->bb > 0 ? std::sqrt(H->rr) / H->bb : 0.0;
+    leave(ctx, stream);
+    if (H->status == NEK_ENOTSPD) return fail(ctx, NEK_ENOTSPD, "PCG breakdown: <p, A p> <= 0 at iteration " + std::to_string(H->iter));
+    return H->status;
+}
+
+int nek_get_info(const nek_ctx *ctx, nek_info_t *info)
+{
+    if (!ctx || !info) return NEK_EINVAL;
+    std::memset(info, 0, sizeof(*info));
+    info->E = ctx->E; info->N = ctx->N; info->rank = ctx->rank; info->nranks = ctx->nranks;
+    info->n_local = ctx->n; info->n_dof = ctx->E * ctx->N * ctx->N * ctx->N; info->n_masked = ctx->n_masked;
+    info->n_runs = ctx->nruns; info->n_perm = ctx->nperm; info->n_ifc_runs = ctx->nifc; info->n_ifc_perm = ctx->nifc_perm;
+    info->n_neighbors = (int64_t)ctx->neighbors.size(); info->halo_doubles = ctx->nslots;
+    info->n_boundary_elems = ctx->n_boundary; info->device_bytes = ctx->device_bytes; info->geom_min_jac = ctx->min_jac;
+    return NEK_OK;
+}
+
+int nek_get_gs_map(const nek_ctx *ctx, int32_t *perm, int64_t *offs)
+{
+    if (!ctx || !ctx->plan) return NEK_EINVAL;
+    if (perm) nek_plan_get(ctx->plan, NEK_PLAN_PERM, perm);
+    if (offs) nek_plan_get(ctx->plan, NEK_PLAN_OFFS, offs);
+    return NEK_OK;
+}
+
+int nek_get_geom(const nek_ctx *ctx_c, double *G, double *wJ)
+{
+    nek_ctx *ctx = const_cast<nek_ctx *>(ctx_c);
+    if (!ctx) return NEK_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->s_main));
+    if (G) CK(cudaMemcpy(G, ctx->G, sizeof(double) * 6 * ctx->n, cudaMemcpyDeviceToHost));
+    if (wJ) CK(cudaMemcpy(wJ, ctx->wJ, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost));
+    return NEK_OK;
+}
+
+int nek_get_dinv(nek_ctx *ctx, double h1, double h2, double *dinv, void *stream)
+{
+    if (!ctx || !dinv) return fail(ctx, NEK_EINVAL, "null");
+    CK(cudaSetDevice(ctx->device));
+    enter(ctx, stream);
+    int st = ensure_dinv(ctx, h1, h2);
+    if (st != NEK_OK) return st;
+    if (is_device_ptr(dinv)) {
+        CK(cudaMemcpyAsync(dinv, ctx->vdinv, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->s_main));
+    } else {
+        CK(cudaMemcpyAsync(dinv, ctx->vdinv, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
+        CK(cudaStreamSynchronize(ctx->s_main));
+    }
+    leave(ctx, stream);
+    return NEK_OK;
+}
+
+int nek_set_timing(nek_ctx *ctx, int on)
+{
+    if (!ctx) return NEK_EINVAL;
+    ctx->timing = on != 0;
+    return NEK_OK;
+}
+
+int nek_get_stats(nek_ctx *ctx, nek_stats_t *stats, int reset)
+{
+    if (!ctx || !stats) return NEK_EINVAL;
+    cudaSetDevice(ctx->device);
+    harvest_timers(ctx);
+    *stats = ctx->stats;
+    if (reset) std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+    return NEK_OK;
+}
+
+int nek_set_variant(nek_ctx *ctx, int v)
+{
+    if (!ctx || v < 0) return NEK_EINVAL;
+    ctx->variant = v;
+    if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+    return NEK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+// nek_ctx.h -- internal state of a context (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "nek.h"
+#include "nek_plan_impl.h"
+
+namespace nekb200 {
+
+// Device-side scalars of one PCG solve (one struct, device memory).
+struct PcgScalars {
+    double rho;        // <r, z> of the current iterate
+    double bb;         // ||M b||
+    double tol;        // relative tolerance
+    double rr;         // ||r||^2 of the current iterate
+    int iter;          // iterations completed
+    int maxit;
+    int done;          // 1 once converged / maxit / breakdown
+    int status;        // NEK_OK, NEK_MAXIT, NEK_ENOTSPD
+};
+
+// Reduction slots (device): red_loc = this rank's partial sums, red_all = the
+// nranks partials gathered in rank order (equal to red_loc at nranks == 1).
+enum { RED_SIGMA = 0, RED_RHO = 1, RED_RR = 2, RED_N = 3 };
+
+struct KernelArgsCommon {
+    int64_t n;            // local points
+    const uint32_t *mbits;  // Dirichlet bit per local point
+    const uint32_t *obits;  // owner bit per local point
+};
+
+// GLL rule (ascending nodes, weights) and D[i][j] = h_j'(x_i), host.
+void gll_rule(int N, double *x, double *w);
+void deriv_matrix(int N, const double *x, double *D);
+
+// kernels.cu entry points (all launched on `s`)
+cudaError_t upload_D(int N, const double *D);
+cudaError_t launch_geom(int N, int64_t E, const double *xyz, double *G, double *wJ, const double *wq,
+                        unsigned long long *bad, cudaStream_t s);
+cudaError_t launch_ax(int variant, int N, int64_t nelem, int64_t eoff, const int32_t *elist, const double *u,
+                      const double *G, const double *wJ, const uint32_t *mbits, double h1, double h2, double *w,
+                      double *part, const int *done, cudaStream_t s, int *nlaunch);
+int ax_partials_needed(int variant, int N, int64_t E);
+cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst, const int *done, cudaStream_t s);
+cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *offs, double *v, const int *done,
+                            cudaStream_t s);
+cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t *offs, const double *v,
+                               double *partial, int64_t nslots, const int32_t *send_run, double *sendbuf,
+                               const int *done, cudaStream_t s);
+cudaError_t launch_gs_ifc_unpack(int64_t nifc, const int32_t *perm, const int32_t *offs, const int32_t *coffs,
+                                 const int32_t *contrib, const double *partial, const double *recvbuf, double *v,
+                                 const int *done, cudaStream_t s);
+cudaError_t launch_diag(int N, int64_t E, const double *G, const double *wJ, double h1, double h2, double *d,
+                        cudaStream_t s);
+cudaError_t launch_dinv(int64_t n, const uint32_t *mbits, const double *d, double *dinv, cudaStream_t s);
+cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const double *src, double *dst, cudaStream_t s);
+cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *obits, const double *b,
+                            const double *dinv, double *r, double *p, double *x, double *part, int nblk,
+                            cudaStream_t s);
+cudaError_t launch_pcg_init_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
+cudaError_t launch_pcg_update(int64_t n, const uint32_t *obits, const double *dinv, const double *p,
+                              const double *w, double *x, double *r, const double *red_all, int nranks,
+                              PcgScalars *sc, double *part, int nblk, cudaStream_t s);
+cudaError_t launch_pcg_pupdate(int64_t n, const double *dinv, const double *r, double *p, const double *red_all,
+                               int nranks, PcgScalars *sc, double *hist, unsigned int *counter, int nblk,
+                               cudaStream_t s);
+int vec_blocks();
+
+}  // namespace nekb200
+
+struct nek_ctx {
+    int device = 0;
+    int64_t E = 0;
+    int N = 0, Nq = 0, P3 = 0;
+    int64_t n = 0;
+    int rank = 0, nranks = 1;
+    ncclComm_t nccl = nullptr;
+    cudaStream_t s_main = nullptr, s_comm = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+    nek_plan *plan = nullptr;
+    int variant = 0;
+    // geometry
+    double *G = nullptr, *wJ = nullptr;
+    double min_jac = 0.0;
+    // maps (device)
+    int32_t *perm = nullptr, *offs = nullptr;
+    int64_t nruns = 0, nperm = 0;
+    int32_t *ifc_perm = nullptr, *ifc_offs = nullptr, *send_run = nullptr, *coffs = nullptr, *contrib = nullptr;
+    int64_t nifc = 0, nifc_perm = 0, nslots = 0;
+    std::vector<int32_t> neighbors;
+    std::vector<int64_t> send_offs;
+    double *ifc_partial = nullptr, *sendbuf = nullptr, *recvbuf = nullptr;
+    int32_t *elist = nullptr;
+    int64_t n_boundary = 0, n_masked = 0;
+    uint32_t *mbits = nullptr, *obits = nullptr;
+    // work vectors
+    double *vr = nullptr, *vp = nullptr, *vw = nullptr, *vx = nullptr, *vdinv = nullptr, *vtmp = nullptr;
+    double *stage_in = nullptr, *stage_out = nullptr;
+    double *part = nullptr;       // block partials (max of Ax and vector kernels)
+    int64_t npart = 0;
+    double *red_loc = nullptr, *red_all = nullptr;
+    nekb200::PcgScalars *sc = nullptr, *sc_host = nullptr;
+    unsigned int *counter = nullptr;
+    double *hist = nullptr;
+    int64_t hist_cap = 0;
+    // Jacobi cache
+    bool dinv_valid = false;
+    double dinv_h1 = 0, dinv_h2 = 0;
+    // graph cache
+    cudaGraphExec_t graph = nullptr;
+    int graph_iters = 0;
+    double graph_h1 = 0, graph_h2 = 0;
+    nek_stats_t graph_stats{};
+    // stats
+    bool timing = false;
+    nek_stats_t stats{};
+    int64_t device_bytes = 0;
+    std::string err;
+};

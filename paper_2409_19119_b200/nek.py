@@ -1,0 +1,314 @@
+"""Thin ctypes binding of the C ABI in include/nek.h (argument marshalling only).
+
+Every numerical step runs inside libnek.so (CUDA kernels for sm_100a + NCCL).
+There is no CPU fallback: if the library is missing or fails to load, importing
+this module raises.
+
+Field arguments accept either torch CUDA float64 tensors (device pointers, used
+in stream order on torch's current stream) or numpy float64 arrays (host
+pointers; the library stages them through device memory and synchronises).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libnek.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(no CPU fallback exists)")
+_lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+
+OK, MAXIT, EINVAL, EORDER, EGEOM, ETOPO, ENOTSPD, ENOMEM, ECUDA, ENCCL, ENODEV = 0, 1, -1, -2, -3, -4, -5, -6, -7, -8, -9
+_NAMES = {0: "NEK_OK", 1: "NEK_MAXIT", -1: "NEK_EINVAL", -2: "NEK_EORDER", -3: "NEK_EGEOM", -4: "NEK_ETOPO",
+          -5: "NEK_ENOTSPD", -6: "NEK_ENOMEM", -7: "NEK_ECUDA", -8: "NEK_ENCCL", -9: "NEK_ENODEV"}
+
+(PLAN_PERM, PLAN_OFFS, PLAN_IFC_PERM, PLAN_IFC_OFFS, PLAN_IFC_GID, PLAN_NEIGHBORS, PLAN_SEND_OFFS, PLAN_SEND_RUN,
+ PLAN_CONTRIB_OFFS, PLAN_CONTRIB, PLAN_OWNER, PLAN_ELEM_ORDER) = range(12)
+_PLAN_DTYPES = {PLAN_PERM: np.int32, PLAN_OFFS: np.int64, PLAN_IFC_PERM: np.int32, PLAN_IFC_OFFS: np.int64,
+                PLAN_IFC_GID: np.int64, PLAN_NEIGHBORS: np.int32, PLAN_SEND_OFFS: np.int64, PLAN_SEND_RUN: np.int32,
+                PLAN_CONTRIB_OFFS: np.int64, PLAN_CONTRIB: np.int32, PLAN_OWNER: np.uint8,
+                PLAN_ELEM_ORDER: np.int32}
+
+
+class NekError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class nek_comm(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_ubyte * 128)]
+
+
+class nek_info_t(ctypes.Structure):
+    _fields_ = [("E", ctypes.c_int64), ("N", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("n_local", ctypes.c_int64), ("n_dof", ctypes.c_int64), ("n_masked", ctypes.c_int64),
+                ("n_runs", ctypes.c_int64), ("n_perm", ctypes.c_int64), ("n_ifc_runs", ctypes.c_int64),
+                ("n_ifc_perm", ctypes.c_int64), ("n_neighbors", ctypes.c_int64), ("halo_doubles", ctypes.c_int64),
+                ("n_boundary_elems", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
+                ("geom_min_jac", ctypes.c_double)]
+
+
+class nek_stats_t(ctypes.Structure):
+    _fields_ = [("ax_ms", ctypes.c_double), ("gs_ms", ctypes.c_double), ("halo_ms", ctypes.c_double),
+                ("vec_ms", ctypes.c_double), ("ax_launches", ctypes.c_int64), ("gs_launches", ctypes.c_int64),
+                ("halo_launches", ctypes.c_int64), ("vec_launches", ctypes.c_int64), ("launches", ctypes.c_int64),
+                ("ax_elements", ctypes.c_int64)]
+
+
+_P, _I, _I64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+_sig = {
+    "nek_version": ([], _I),
+    "nek_last_error": ([], ctypes.c_char_p),
+    "nek_comm_unique_id": ([_P], _I),
+    "nek_setup": ([ctypes.POINTER(_P), _I64, _I, _P, _P, _P, ctypes.POINTER(nek_comm), _I, _P], _I),
+    "nek_ax": ([_P, _D, _D, _P, _P, _P], _I),
+    "nek_gs": ([_P, _P, _P], _I),
+    "nek_pcg_solve": ([_P, _D, _D, _P, _P, _D, _I, ctypes.POINTER(_I), ctypes.POINTER(_D), _P, _P], _I),
+    "nek_free": ([_P], _I),
+    "nek_errmsg": ([_P], ctypes.c_char_p),
+    "nek_get_info": ([_P, ctypes.POINTER(nek_info_t)], _I),
+    "nek_get_gs_map": ([_P, _P, _P], _I),
+    "nek_get_geom": ([_P, _P, _P], _I),
+    "nek_get_dinv": ([_P, _D, _D, _P, _P], _I),
+    "nek_set_timing": ([_P, _I], _I),
+    "nek_get_stats": ([_P, ctypes.POINTER(nek_stats_t), _I], _I),
+    "nek_set_variant": ([_P, _I], _I),
+    "nek_plan_create": ([ctypes.POINTER(_P), _I64, _I, _P, _P, _P], _I),
+    "nek_plan_surface_gids": ([_P, _P], _I64),
+    "nek_plan_set_ranks": ([_P, _I, _I, _P, _P], _I),
+    "nek_plan_size": ([_P, _I], _I64),
+    "nek_plan_get": ([_P, _I, _P], _I),
+    "nek_plan_errmsg": ([_P], ctypes.c_char_p),
+    "nek_plan_free": ([_P], None),
+}
+for _name, (_args, _res) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_sig)
+
+
+def _np_ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None else None
+
+
+def _field_ptr(a, n, name, writable=False):
+    """(pointer, is_device, stream) of a float64 field of length n."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or a.size != n or not a.flags.c_contiguous or (writable and not a.flags.writeable):
+            raise ValueError(f"{name}: need a C-contiguous float64 array of {n} entries")
+        return ctypes.c_void_p(a.ctypes.data), None
+    import torch
+    if not isinstance(a, torch.Tensor):
+        raise TypeError(f"{name}: numpy array or torch tensor expected")
+    if a.dtype != torch.float64 or a.numel() != n or not a.is_contiguous():
+        raise ValueError(f"{name}: need a contiguous float64 tensor of {n} entries")
+    if a.is_cuda:
+        return ctypes.c_void_p(a.data_ptr()), torch.cuda.current_stream(a.device).cuda_stream
+    return ctypes.c_void_p(a.data_ptr()), None   # host (possibly pinned) tensor
+
+
+def _stream_of(*streams):
+    for s in streams:
+        if s is not None:
+            return ctypes.c_void_p(s)
+    return None
+
+
+def _check(code, ctx=None):
+    if code < 0:
+        msg = _lib.nek_errmsg(ctx) if ctx else _lib.nek_last_error()
+        raise NekError(code, (msg or b"").decode())
+    return code
+
+
+def version():
+    return _lib.nek_version()
+
+
+def comm_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _check(_lib.nek_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Context:
+    """A nek_ctx: one rank's elements, on one GPU."""
+
+    def __init__(self, handle, E, N):
+        self._h = handle
+        self.E, self.N = E, N
+        self.n = E * (N + 1) ** 3
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise RuntimeError("context freed")
+        return self._h
+
+    def free(self):
+        if self._h:
+            _lib.nek_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def setup(E, N, xyz, gid, mask=None, comm=None, device=0, stream=None) -> Context:
+    """nek_setup: xyz (3, E*(N+1)^3) float64, gid int64, mask uint8 or None (host arrays).
+    comm: None or (rank, nranks, nccl_id bytes)."""
+    n = int(E) * (int(N) + 1) ** 3
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    gid = np.ascontiguousarray(gid, dtype=np.int64)
+    if xyz.size != 3 * n or gid.size != n:
+        raise ValueError("xyz must hold 3*E*(N+1)^3 and gid E*(N+1)^3 entries")
+    m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+    c = None
+    if comm is not None and comm[1] > 1:
+        c = nek_comm()
+        c.rank, c.nranks = int(comm[0]), int(comm[1])
+        ctypes.memmove(c.nccl_id, bytes(comm[2]), 128)
+    h = ctypes.c_void_p()
+    st = _lib.nek_setup(ctypes.byref(h), int(E), int(N), _np_ptr(xyz), _np_ptr(gid), _np_ptr(m),
+                        ctypes.byref(c) if c is not None else None, int(device),
+                        ctypes.c_void_p(stream) if stream else None)
+    _check(st)
+    return Context(h, int(E), int(N))
+
+
+def ax(ctx: Context, h1, h2, u, w):
+    """nek_ax: w = M QQ^T (h1 K_L + h2 B_L) M u."""
+    pu, su = _field_ptr(u, ctx.n, "u")
+    pw, sw = _field_ptr(w, ctx.n, "w", writable=True)
+    _check(_lib.nek_ax(ctx.handle, float(h1), float(h2), pu, pw, _stream_of(su, sw)), ctx.handle)
+    return w
+
+
+def gs(ctx: Context, v):
+    """nek_gs: v <- QQ^T v in place."""
+    pv, sv = _field_ptr(v, ctx.n, "v", writable=True)
+    _check(_lib.nek_gs(ctx.handle, pv, _stream_of(sv)), ctx.handle)
+    return v
+
+
+def pcg_solve(ctx: Context, h1, h2, b, x, tol, maxit, want_hist=False):
+    """nek_pcg_solve -> (status, iters, relres, hist or None)."""
+    pb, sb = _field_ptr(b, ctx.n, "b")
+    px, sx = _field_ptr(x, ctx.n, "x", writable=True)
+    it = ctypes.c_int(0)
+    rr = ctypes.c_double(0.0)
+    hist = np.zeros(int(maxit) + 1) if want_hist else None
+    st = _lib.nek_pcg_solve(ctx.handle, float(h1), float(h2), pb, px, float(tol), int(maxit), ctypes.byref(it),
+                            ctypes.byref(rr), _np_ptr(hist), _stream_of(sb, sx))
+    _check(st, ctx.handle)
+    if hist is not None:
+        hist = hist[: it.value + 1]
+    return st, it.value, rr.value, hist
+
+
+def free(ctx: Context):
+    ctx.free()
+
+
+def get_info(ctx: Context) -> dict:
+    info = nek_info_t()
+    _check(_lib.nek_get_info(ctx.handle, ctypes.byref(info)), ctx.handle)
+    return {k: getattr(info, k) for k, _ in nek_info_t._fields_}
+
+
+def get_gs_map(ctx: Context):
+    info = get_info(ctx)
+    perm = np.zeros(max(info["n_perm"], 1), np.int32)
+    offs = np.zeros(info["n_runs"] + 1, np.int64)
+    _check(_lib.nek_get_gs_map(ctx.handle, _np_ptr(perm), _np_ptr(offs)), ctx.handle)
+    return perm[: info["n_perm"]], offs
+
+
+def get_geom(ctx: Context):
+    P3 = (ctx.N + 1) ** 3
+    G = np.zeros((ctx.E, 6, P3))
+    wJ = np.zeros(ctx.n)
+    _check(_lib.nek_get_geom(ctx.handle, _np_ptr(G), _np_ptr(wJ)), ctx.handle)
+    return G, wJ
+
+
+def get_dinv(ctx: Context, h1, h2, out=None):
+    if out is None:
+        out = np.zeros(ctx.n)
+    p, s = _field_ptr(out, ctx.n, "dinv", writable=True)
+    _check(_lib.nek_get_dinv(ctx.handle, float(h1), float(h2), p, _stream_of(s)), ctx.handle)
+    return out
+
+
+def set_timing(ctx: Context, on: bool):
+    _check(_lib.nek_set_timing(ctx.handle, 1 if on else 0), ctx.handle)
+
+
+def get_stats(ctx: Context, reset=False) -> dict:
+    s = nek_stats_t()
+    _check(_lib.nek_get_stats(ctx.handle, ctypes.byref(s), 1 if reset else 0), ctx.handle)
+    return {k: getattr(s, k) for k, _ in nek_stats_t._fields_}
+
+
+def set_variant(ctx: Context, v: int):
+    _check(_lib.nek_set_variant(ctx.handle, int(v)), ctx.handle)
+
+
+# --------------------------------------------------------------- host plans
+class Plan:
+    """Host-only gather-scatter / halo plan (nek_plan_*), usable without a GPU."""
+
+    def __init__(self, E, N, gid, mask=None, xyz=None):
+        gid = np.ascontiguousarray(gid, dtype=np.int64)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        x = None if xyz is None else np.ascontiguousarray(xyz, dtype=np.float64)
+        h = ctypes.c_void_p()
+        st = _lib.nek_plan_create(ctypes.byref(h), int(E), int(N), _np_ptr(gid), _np_ptr(m), _np_ptr(x))
+        self._h = h
+        if st != OK:
+            msg = _lib.nek_plan_errmsg(h).decode() if h else ""
+            self.free()
+            raise NekError(st, msg)
+
+    def surface_gids(self):
+        n = _lib.nek_plan_surface_gids(self._h, None)
+        out = np.zeros(max(n, 1), np.int64)
+        _lib.nek_plan_surface_gids(self._h, _np_ptr(out))
+        return out[:n]
+
+    def set_ranks(self, rank, nranks, lists):
+        lists = [np.ascontiguousarray(L, dtype=np.int64) for L in lists]
+        counts = np.array([L.size for L in lists], np.int64)
+        ptrs = (ctypes.c_void_p * nranks)(*[L.ctypes.data for L in lists])
+        st = _lib.nek_plan_set_ranks(self._h, int(rank), int(nranks), _np_ptr(counts), ptrs)
+        if st != OK:
+            raise NekError(st, _lib.nek_plan_errmsg(self._h).decode())
+
+    def get(self, what):
+        n = _lib.nek_plan_size(self._h, what)
+        out = np.zeros(max(n, 1), _PLAN_DTYPES[what])
+        if n > 0:
+            _lib.nek_plan_get(self._h, what, _np_ptr(out))
+        return out[:n]
+
+    def free(self):
+        if self._h:
+            _lib.nek_plan_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

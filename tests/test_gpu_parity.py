@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances:
+  * gather-scatter maps: byte-equal; gs values at one rank: bit-equal;
+  * geometry, Ax, Jacobi diagonal: relative 1e-12 normwise (max-abs / max-abs,
+    BASELINE north_star "agree to relative 1e-12", reading 16);
+  * PCG: identical iteration count (+-1) on converged solves, final x 1e-12,
+    residual history |d(||r_k||/||b||)| <= 1e-12 on fixed windows (reading 17).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from workloads import meshgen as mg  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def nek():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_19119_b200 import nek as _nek
+    return _nek
+
+
+def rel(a, b):
+    b = np.asarray(b)
+    d = np.abs(np.asarray(a) - b).max() if b.size else 0.0
+    s = np.abs(b).max() if b.size else 1.0
+    return d / (s if s > 0 else 1.0)
+
+
+MESHES = {
+    "cfg1": lambda: mg.config_mesh(1),
+    "N1": lambda: mg.box_mesh(3, 2, 2, 1, deform="bubble"),
+    "N2odd": lambda: mg.box_mesh(3, 2, 3, 2, deform="bubble", dirichlet="zends"),
+    "N5sin": lambda: mg.box_mesh(3, 3, 2, 5, deform="sin", eps=0.08),
+    "N7": lambda: mg.box_mesh(4, 3, 5, 7, deform="bubble"),
+    "N7neumann": lambda: mg.box_mesh(3, 3, 3, 7, deform="bubble", dirichlet="none"),
+    "N8jitter": lambda: mg.box_mesh(3, 2, 2, 8, deform="affine", jitter=0.15, seed=3),
+    "N9": lambda: mg.box_mesh(2, 3, 2, 9, deform="bubble"),
+    "N12": lambda: mg.box_mesh(2, 2, 1, 12, deform="bubble", dirichlet="top"),
+}
+
+
+@pytest.fixture(scope="module", params=list(MESHES))
+def case(request, nek):
+    m = MESHES[request.param]()
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    O = oracle.Oracle.from_mesh(m)
+    yield m, ctx, O
+    nek.free(ctx)
+
+
+def test_exports(nek):
+    assert nek.version() == 1
+
+
+def test_geometry_parity(case, nek):
+    m, ctx, O = case
+    G, wJ = nek.get_geom(ctx)
+    assert rel(G, O.G) <= 1e-12
+    assert rel(wJ, O.wJ) <= 1e-12
+
+
+def test_gs_map_bit_exact(case, nek):
+    m, ctx, O = case
+    perm, offs = nek.get_gs_map(ctx)
+    assert np.array_equal(perm, O.gs.perm)
+    assert np.array_equal(offs, O.gs.offs)
+    info = nek.get_info(ctx)
+    assert info["n_runs"] == O.gs.nruns and info["n_local"] == m.n_local and info["n_dof"] == m.E * m.N ** 3
+    assert info["n_masked"] == int(m.mask.sum())
+
+
+def test_gs_values_bit_exact(case, nek):
+    m, ctx, O = case
+    v = mg.random_evector(m, seed=11)
+    ref = O.gs_apply(v)
+    vd = torch.from_numpy(v).cuda()
+    nek.gs(ctx, vd)
+    torch.cuda.synchronize()
+    assert np.array_equal(vd.cpu().numpy(), ref)
+    vh = v.copy()                       # host-pointer path
+    nek.gs(ctx, vh)
+    assert np.array_equal(vh, ref)
+
+
+@pytest.mark.parametrize("h", [(1.0, 0.0), (1.0, 0.37), (0.0, 1.0), (2.5, 10.0)])
+def test_ax_parity(case, nek, h):
+    m, ctx, O = case
+    u = mg.random_evector(m, seed=5)
+    ref = O.apply(h[0], h[1], u)
+    ud = torch.from_numpy(u).cuda()
+    wd = torch.full_like(ud, np.nan)
+    nek.ax(ctx, h[0], h[1], ud, wd)
+    torch.cuda.synchronize()
+    w = wd.cpu().numpy()
+    assert rel(w, ref) <= 1e-12
+    assert np.all(w[m.mask != 0] == 0.0)
+    wh = np.empty(m.n_local)            # host-pointer path
+    nek.ax(ctx, h[0], h[1], u, wh)
+    assert rel(wh, ref) <= 1e-12
+
+
+def test_ax_repeatable_bitwise(case, nek):
+    m, ctx, O = case
+    u = torch.from_numpy(mg.random_evector(m, seed=2)).cuda()
+    a, b = torch.empty_like(u), torch.empty_like(u)
+    nek.ax(ctx, 1.0, 0.1, u, a)
+    nek.ax(ctx, 1.0, 0.1, u, b)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("h", [(1.0, 0.0), (1.0, 3.0)])
+def test_dinv_parity(case, nek, h):
+    m, ctx, O = case
+    if h[1] == 0.0 and m.mask.sum() == 0:
+        pytest.skip("pure Neumann Poisson: diagonal positive but operator singular")
+    d = nek.get_dinv(ctx, h[0], h[1])
+    assert rel(d, O.dinv(h[0], h[1])) <= 1e-12
+
+
+def test_pcg_fixed_window(case, nek):
+    """100 fixed iterations: residual history within 1e-12 of the oracle (reading 17)."""
+    m, ctx, O = case
+    if m.mask.sum() == 0:
+        h = (1.0, 1.0)
+    else:
+        h = (1.0, 0.0)
+    b = mg.smooth_field(m, seed=3)
+    # window: 100 iterations, or fewer on tiny meshes where CG reaches rounding level
+    _, kconv, _, _ = O.pcg(h[0], h[1], b, 1e-11, 100)
+    win = min(100, kconv)
+    xo, ito, sto, ho = O.pcg(h[0], h[1], b, 0.0, win)
+    bd = torch.from_numpy(b).cuda()
+    xd = torch.zeros_like(bd)
+    st, it, rr, hg = nek.pcg_solve(ctx, h[0], h[1], bd, xd, 0.0, win, want_hist=True)
+    assert it == ito == win and st == nek.MAXIT
+    assert np.abs(hg - ho).max() <= 1e-12
+    assert rel(xd.cpu().numpy(), xo) <= 1e-10
+
+
+def test_pcg_converged_manufactured(nek):
+    m = mg.config_mesh(1)
+    O = oracle.Oracle.from_mesh(m)
+    u, f = mg.manufactured(m)
+    b = oracle.mask(m.mask, O.gs_apply(O.wJ * f))
+    xo, ito, sto, ho = O.pcg(1.0, 0.0, b, 1e-10, 500)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        # the GPU path forms its own RHS: M QQ^T (B f) = nek_ax with (h1,h2) = (0,1)
+        bg = np.empty(m.n_local)
+        nek.ax(ctx, 0.0, 1.0, np.where(m.mask != 0, 0.0, f), bg)
+        assert rel(bg, b) <= 1e-13
+        x = np.zeros(m.n_local)
+        st, it, rr, hg = nek.pcg_solve(ctx, 1.0, 0.0, bg, x, 1e-10, 500, want_hist=True)
+        assert st == nek.OK and abs(it - ito) <= 1
+        assert rel(x, xo) <= 1e-12
+        assert np.abs(x - u).max() < 2.5e-3
+        k = min(len(hg), len(ho))
+        assert np.abs(hg[:k] - ho[:k]).max() <= 1e-12
+    finally:
+        nek.free(ctx)
+
+
+def test_pcg_edge_cases(nek):
+    m = mg.config_mesh(1)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        x = np.ones(m.n_local)
+        st, it, rr, _ = nek.pcg_solve(ctx, 1.0, 0.0, np.zeros(m.n_local), x, 1e-10, 50)
+        assert st == nek.OK and it == 0 and np.all(x == 0)
+        b = mg.smooth_field(m, seed=4)
+        st, it, rr, _ = nek.pcg_solve(ctx, 0.0, 1.0, b, x, 1e-12, 20)      # pure mass: Jacobi exact
+        assert st == nek.OK and it == 1
+        st, it, rr, _ = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 1e-10, 0)
+        assert st == nek.MAXIT and it == 0
+        with pytest.raises(nek.NekError) as ei:                               # <p,Ap> <= 0
+            nek.pcg_solve(ctx, -1.0, 0.0, b, x, 1e-10, 10)
+        assert ei.value.code == nek.ENOTSPD
+    finally:
+        nek.free(ctx)
+
+
+def test_setup_errors(nek):
+    m = mg.box_mesh(1, 1, 1, 2, deform="affine")
+    with pytest.raises(nek.NekError) as ei:
+        nek.setup(1, 16, np.zeros(3 * 17 ** 3), np.zeros(17 ** 3, np.int64))
+    assert ei.value.code == nek.EORDER
+    xyz = m.xyz.copy(); xyz[0] = -xyz[0]
+    with pytest.raises(nek.NekError) as ei:
+        nek.setup(1, 2, xyz, m.gid, m.mask)
+    assert ei.value.code == nek.EGEOM and "element 0" in str(ei.value)
+    m2 = mg.box_mesh(2, 1, 1, 2, deform="affine", dirichlet="none")
+    mask = m2.mask.copy(); mask[2] = 1                # copy of a shared node flagged only once
+    with pytest.raises(nek.NekError) as ei:
+        nek.setup(2, 2, m2.xyz, m2.gid, mask)
+    assert ei.value.code == nek.ETOPO
+    xyz2 = m2.xyz.copy(); xyz2[1, 2] += 0.01         # shared node moved in one copy
+    with pytest.raises(nek.NekError) as ei:
+        nek.setup(2, 2, xyz2, m2.gid, None)
+    assert ei.value.code == nek.ETOPO
+
+
+def test_empty_mesh(nek):
+    ctx = nek.setup(0, 3, np.zeros(0), np.zeros(0, np.int64))
+    try:
+        assert nek.get_info(ctx)["n_local"] == 0
+        nek.ax(ctx, 1.0, 0.0, np.zeros(0), np.zeros(0))
+        st, it, _, _ = nek.pcg_solve(ctx, 1.0, 0.0, np.zeros(0), np.zeros(0), 1e-8, 10)
+        assert st == nek.OK and it == 0
+    finally:
+        nek.free(ctx)
+
+
+def test_config2_full_size(nek):
+    """BASELINE config 2 (16^3, N=7) at full size: Ax+gs element-by-element against
+    the oracle, bit-exact gs, and the first 10 PCG iterations' residuals."""
+    m = mg.config_mesh(2)
+    O = oracle.Oracle.from_mesh(m)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        u = mg.random_evector(m, seed=8)
+        ud = torch.from_numpy(u).cuda(); wd = torch.empty_like(ud)
+        nek.ax(ctx, 1.0, 0.0, ud, wd)
+        torch.cuda.synchronize()
+        assert rel(wd.cpu().numpy(), O.apply(1.0, 0.0, u)) <= 1e-12
+        v = torch.from_numpy(u).cuda()
+        nek.gs(ctx, v)
+        torch.cuda.synchronize()
+        assert np.array_equal(v.cpu().numpy(), O.gs_apply(u))
+        b = mg.smooth_field(m, seed=1)
+        _, ito, _, ho = O.pcg(1.0, 0.0, b, 0.0, 10)
+        x = torch.zeros_like(ud)
+        st, it, _, hg = nek.pcg_solve(ctx, 1.0, 0.0, torch.from_numpy(b).cuda(), x, 0.0, 10, want_hist=True)
+        assert it == 10 and np.abs(hg - ho).max() <= 1e-12
+    finally:
+        nek.free(ctx)

@@ -100,7 +100,7 @@ def _deform_global(X, Y, Z, extent, deform, eps):
 
 def box_mesh(Ex: int, Ey: int, Ez: int, N: int, deform: str = "bubble", eps: float = 0.05,
              extent=(1.0, 1.0, 1.0), dirichlet: str = "all", jitter: float = 0.0,
-             seed: int = 0) -> Mesh:
+             seed: int = 0, zlayers=None) -> Mesh:
     """Structured Ex x Ey x Ez hex box of order N, lexicographic elements
     e = ex + Ex*(ey + Ey*ez), deformed by `deform`.
 
@@ -109,7 +109,10 @@ def box_mesh(Ex: int, Ey: int, Ez: int, N: int, deform: str = "bubble", eps: flo
     jitter > 0 moves interior element VERTICES randomly (trilinear elements,
     straight edges), used by the patch test; the GLL nodes then follow the
     trilinear map of each element (copies still bit-identical: each global node
-    is placed once from one owning element)."""
+    is placed once from one owning element).
+
+    zlayers=(z0, z1) generates only the element layers z0 <= ez < z1 (one
+    rank's z-slab) with the global numbering of the full box."""
     Nq = N + 1
     xi = gll_points(N)
     NX, NY, NZ = Ex * N + 1, Ey * N + 1, Ez * N + 1
@@ -151,8 +154,9 @@ def box_mesh(Ex: int, Ey: int, Ez: int, N: int, deform: str = "bubble", eps: flo
         X, Y, Z = out
     X, Y, Z = _deform_global(X, Y, Z, extent, deform, eps)
 
-    E = Ex * Ey * Ez
-    e = np.arange(E)
+    z0, z1 = (0, Ez) if zlayers is None else zlayers
+    E = Ex * Ey * (z1 - z0)
+    e = np.arange(E) + Ex * Ey * z0
     ex, ey, ez = e % Ex, (e // Ex) % Ey, e // (Ex * Ey)
     i = np.arange(Nq)
     # local (e, k, j, i) -> global lattice (I, J, K)
