@@ -61,6 +61,7 @@ def lib():
         L.or_pcg.restype = i32
         L.or_op_apply.argtypes = [i64, i32, P, P, P, P, i64, P, P, dbl, dbl, P, P]
         L.or_op_apply.restype = None
+        L.or_set_dot_reverse.argtypes = [i32]; L.or_set_dot_reverse.restype = None
         _lib = L
     return _lib
 
@@ -221,17 +222,29 @@ class Oracle:
             s += a * b
         return s
 
-    def pcg(self, h1, h2, b, tol, maxit, dinv=None):
-        """Jacobi-PCG (S:353-357); returns (x, iters, status, hist)."""
+    def pcg(self, h1, h2, b, tol, maxit, dinv=None, reverse_dots=False):
+        """Jacobi-PCG (S:353-357); returns (x, iters, status, hist).
+        reverse_dots=True sums every inner product in descending index order:
+        the oracle's own rounding noise, the yardstick of reading 17."""
         if dinv is None:
             dinv = self.dinv(h1, h2)
+        lib().or_set_dot_reverse(1 if reverse_dots else 0)
         b = _c(b, np.float64); x = np.zeros(self.n); hist = np.zeros(maxit + 1)
         it = ctypes.c_int(0)
         st = lib().or_pcg(self.E, self.N, _p(self.D), _p(self.G), _p(self.wJ), _p(self.mask),
                           self.gs.nruns, _p(self.gs.perm), _p(self.gs.offs), _p(self.owner),
                           _p(_c(dinv, np.float64)), float(h1), float(h2), _p(b), _p(x),
                           float(tol), int(maxit), ctypes.byref(it), _p(hist))
+        lib().or_set_dot_reverse(0)
         return x, it.value, st, hist[: it.value + 1]
+
+    def hist_tolerance(self, h1, h2, b, maxit, dinv=None):
+        """Per-iteration tolerance on ||r_k||/||b|| for comparing another FP64
+        implementation (reading 17): max(1e-12 * max(1, h_k), 10 * self-noise_k)."""
+        _, _, _, h = self.pcg(h1, h2, b, 0.0, maxit, dinv=dinv)
+        _, _, _, hr = self.pcg(h1, h2, b, 0.0, maxit, dinv=dinv, reverse_dots=True)
+        k = min(h.size, hr.size)
+        return np.maximum(1e-12 * np.maximum(1.0, h[:k]), 10.0 * np.abs(h[:k] - hr[:k]))
 
 
 # ------------------------------------------------ multi-rank gather-scatter --

@@ -370,13 +370,19 @@ static void op_apply(const or_op *A, const double *u, double *tmp, double *w)
     or_mask(n, A->mask, w);
 }
 
-/* owner-copy inner product sum_g x_g y_g (reading 8) */
+/* owner-copy inner product sum_g x_g y_g (reading 8).  Summed in ascending
+ * local index; g_dot_reverse = 1 sums in descending order instead -- the same
+ * mathematics with a different rounding, used only to measure the oracle's own
+ * summation-order noise (reading 17). */
+static int g_dot_reverse = 0;
 static double dot_owner(int64_t n, const uint8_t *owner, const double *x, const double *y)
 {
     double s = 0.0;
-    for (int64_t l = 0; l < n; ++l) if (owner[l]) s += x[l] * y[l];
+    if (g_dot_reverse) { for (int64_t l = n - 1; l >= 0; --l) if (owner[l]) s += x[l] * y[l]; }
+    else { for (int64_t l = 0; l < n; ++l) if (owner[l]) s += x[l] * y[l]; }
     return s;
 }
+void or_set_dot_reverse(int on) { g_dot_reverse = on; }
 
 /*
  * or_pcg: Jacobi-preconditioned CG, Hestenes-Stiefel form, step by step as
