@@ -128,16 +128,14 @@ static void harvest_timers(nek_ctx *ctx)
 }
 
 // ------------------------------------------------------------ building blocks
-static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, double *part, const int *done,
-                 int64_t nelem, int64_t eoff, const int32_t *elist)
+static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, const AxLaunch &L)
 {
     Scope sc(ctx, CLS_AX);
     int nl = 0;
-    CK(launch_ax(ctx->variant, ctx->N, nelem, eoff, elist, u, ctx->G, ctx->wJ, ctx->mbits, h1, h2, w, part, done,
-                 ctx->s_main, &nl));
-    ctx->stats.ax_launches += nl;
+    CK(launch_ax(ctx->variant, ctx->N, L, u, ctx->G, ctx->wJ, ctx->mbits, h1, h2, w, ctx->s_main, &nl));
+    ctx->stats.ax_launches += L.nelem > 0;
     ctx->stats.launches += nl;
-    ctx->stats.ax_elements += nelem;
+    ctx->stats.ax_elements += L.nelem;
     return NEK_OK;
 }
 
@@ -176,7 +174,7 @@ static int halo_finish(nek_ctx *ctx, double *v, const int *done)
 static int do_gs_local(nek_ctx *ctx, double *v, const int *done)
 {
     Scope sc(ctx, CLS_GS);
-    CK(launch_gs_local(ctx->nruns, ctx->perm, ctx->offs, v, done, ctx->s_main));
+    CK(launch_gs_classes(ctx->gsc, v, done, ctx->s_main));
     ctx->stats.gs_launches += 1;
     ctx->stats.launches += (ctx->nruns > 0);
     return NEK_OK;
@@ -192,30 +190,39 @@ static int gs_full(nek_ctx *ctx, double *v, const int *done)
     return NEK_OK;
 }
 
-// w = M QQ^T (h1 K_L + h2 B_L) M u; block partials of <M u, A_L M u> into part (nullable).
-static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, double *part, const int *done)
+// w = M QQ^T (h1 K_L + h2 B_L) M u.  With dot: this rank's <M u, A_L M u> into
+// red_loc[RED_SIGMA] (then allgathered across ranks into red_all).
+static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, bool dot, const int *done)
 {
     int st;
+    AxLaunch L;
+    L.done = done;
+    L.counter = ctx->counter + 1;
+    L.dst = ctx->red_loc + RED_SIGMA;
     if (ctx->nranks == 1) {
-        if ((st = do_ax(ctx, h1, h2, u, w, part, done, ctx->E, 0, nullptr)) != NEK_OK) return st;
+        L.nelem = ctx->E;
+        if (dot) { L.part = ctx->part; L.fin_total = ax_grid(ctx->variant, ctx->N, ctx->E); }
+        if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         return do_gs_local(ctx, w, done);
     }
-    if ((st = do_ax(ctx, h1, h2, u, w, part, done, ctx->n_boundary, 0, ctx->elist)) != NEK_OK) return st;
+    const int64_t nb = ctx->n_boundary, ni = ctx->E - ctx->n_boundary;
+    const int64_t g1 = ax_grid(ctx->variant, ctx->N, nb), g2 = ax_grid(ctx->variant, ctx->N, ni);
+    L.elist = ctx->elist;
+    L.nelem = nb;
+    if (dot) { L.part = ctx->part; L.part_off = 0; L.fin_total = 0; }
+    if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
     if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
-    if ((st = do_ax(ctx, h1, h2, u, w, part, done, ctx->E - ctx->n_boundary, ctx->n_boundary, ctx->elist)) != NEK_OK)
-        return st;
+    L.nelem = ni;
+    L.eoff = nb;
+    if (dot) { L.part_off = g1; L.fin_total = g1 + g2; }
+    if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
     if ((st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
     return halo_finish(ctx, w, done);
 }
 
-static int reduce_slots(nek_ctx *ctx, const double *part, int64_t count, int nd, int slot, const int *done)
+// share this rank's reduction slots with every rank (rank-ordered; red_all == red_loc at one rank)
+static int exchange_slots(nek_ctx *ctx)
 {
-    {
-        Scope sc(ctx, CLS_VEC);
-        CK(launch_reduce(part, count, nd, ctx->red_loc + slot, done, ctx->s_main));
-        ctx->stats.launches += 1;
-        ctx->stats.vec_launches += 1;
-    }
     if (ctx->nranks > 1) NK(ncclAllGather(ctx->red_loc, ctx->red_all, RED_N, ncclDouble, ctx->nccl, ctx->s_main));
     return NEK_OK;
 }
@@ -346,6 +353,21 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     ctx->nruns = (int64_t)p->offs.size() - 1; ctx->nperm = (int64_t)p->perm.size();
     CK(upload(ctx, &ctx->perm, p->perm));
     CK(upload(ctx, &ctx->offs, to32(p->offs)));
+    {   // length classes of the local runs (same runs, same order within a class)
+        std::vector<int32_t> c2, c4, c8, cg, og(1, 0);
+        for (int64_t r = 0; r < ctx->nruns; ++r) {
+            const int64_t a = p->offs[r], len = p->offs[r + 1] - a;
+            std::vector<int32_t> &dst = len == 2 ? c2 : len == 4 ? c4 : len == 8 ? c8 : cg;
+            for (int64_t c = 0; c < len; ++c) dst.push_back(p->perm[a + c]);
+            if (len != 2 && len != 4 && len != 8) og.push_back((int32_t)cg.size());
+        }
+        CK(upload(ctx, &ctx->gs_p2, c2)); CK(upload(ctx, &ctx->gs_p4, c4)); CK(upload(ctx, &ctx->gs_p8, c8));
+        CK(upload(ctx, &ctx->gs_pg, cg)); CK(upload(ctx, &ctx->gs_og, og));
+        ctx->gsc.n2 = (int64_t)c2.size() / 2; ctx->gsc.n4 = (int64_t)c4.size() / 4; ctx->gsc.n8 = (int64_t)c8.size() / 8;
+        ctx->gsc.ng = (int64_t)og.size() - 1;
+        ctx->gsc.p2 = ctx->gs_p2; ctx->gsc.p4 = ctx->gs_p4; ctx->gsc.p8 = ctx->gs_p8;
+        ctx->gsc.pg = ctx->gs_pg; ctx->gsc.og = ctx->gs_og;
+    }
     ctx->nifc = (int64_t)p->ifc_offs.size() - 1; ctx->nifc_perm = (int64_t)p->ifc_perm.size();
     CK(upload(ctx, &ctx->ifc_perm, p->ifc_perm));
     CK(upload(ctx, &ctx->ifc_offs, to32(p->ifc_offs)));
@@ -390,15 +412,15 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     }
     // work vectors, reductions, scalars
     for (double **v : {&ctx->vr, &ctx->vp, &ctx->vw, &ctx->vx, &ctx->vdinv, &ctx->vtmp}) CK(dalloc(ctx, v, n));
-    ctx->npart = std::max<int64_t>(ax_partials_needed(ctx->variant, N, E), 2 * vec_blocks());
+    ctx->npart = std::max<int64_t>(ax_partials_needed(1, N, E), 2 * vec_blocks());
     CK(dalloc(ctx, &ctx->part, ctx->npart));
     CK(dalloc(ctx, &ctx->red_loc, RED_N));
     if (ctx->nranks > 1) CK(dalloc(ctx, &ctx->red_all, RED_N * ctx->nranks));
     else ctx->red_all = ctx->red_loc;
     CK(dalloc(ctx, &ctx->sc, 1));
     CK(cudaMallocHost(&ctx->sc_host, sizeof(PcgScalars)));
-    CK(dalloc(ctx, &ctx->counter, 1));
-    CK(cudaMemset(ctx->counter, 0, sizeof(unsigned int)));
+    CK(dalloc(ctx, &ctx->counter, 4));
+    CK(cudaMemset(ctx->counter, 0, 4 * sizeof(unsigned int)));
     CK(cudaMemset(ctx->red_loc, 0, sizeof(double) * RED_N));
     CK(cudaStreamSynchronize(ctx->s_main));
     leave(ctx, stream);
@@ -440,7 +462,8 @@ int nek_free(nek_ctx *ctx)
                     (void *)ctx->mbits, (void *)ctx->obits, (void *)ctx->vr, (void *)ctx->vp, (void *)ctx->vw,
                     (void *)ctx->vx, (void *)ctx->vdinv, (void *)ctx->vtmp, (void *)ctx->stage_in,
                     (void *)ctx->stage_out, (void *)ctx->part, (void *)ctx->red_loc, (void *)ctx->sc,
-                    (void *)ctx->counter, (void *)ctx->hist})
+                    (void *)ctx->counter, (void *)ctx->hist, (void *)ctx->gs_p2, (void *)ctx->gs_p4,
+                    (void *)ctx->gs_p8, (void *)ctx->gs_pg, (void *)ctx->gs_og})
         if (p) cudaFree(p);
     if (ctx->red_all && ctx->red_all != ctx->red_loc) cudaFree(ctx->red_all);
     if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
@@ -470,7 +493,7 @@ int nek_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, void 
     if (!du || !dw) { if ((st = ensure_stage(ctx)) != NEK_OK) return st; }
     if (!du) { CK(cudaMemcpyAsync(ctx->stage_in, u, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->s_main)); ud = ctx->stage_in; }
     if (!dw) wd = ctx->stage_out;
-    if ((st = apply_op(ctx, h1, h2, ud, wd, nullptr, nullptr)) != NEK_OK) return st;
+    if ((st = apply_op(ctx, h1, h2, ud, wd, false, nullptr)) != NEK_OK) return st;
     if (!dw) {
         CK(cudaMemcpyAsync(w, wd, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
         CK(cudaStreamSynchronize(ctx->s_main));
@@ -508,16 +531,16 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
     int st;
     const int *done = &ctx->sc->done;
     const int nb = vec_blocks();
-    if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, ctx->part, done)) != NEK_OK) return st;
-    if ((st = reduce_slots(ctx, ctx->part, ax_partials_needed(ctx->variant, ctx->N, ctx->E), 1, RED_SIGMA, done)) != NEK_OK)
-        return st;
+    if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done)) != NEK_OK) return st;
+    if ((st = exchange_slots(ctx)) != NEK_OK) return st;
     {
         Scope sc(ctx, CLS_VEC);
         CK(launch_pcg_update(ctx->n, ctx->obits, ctx->vdinv, ctx->vp, ctx->vw, ctx->vx, ctx->vr, ctx->red_all,
-                             ctx->nranks, ctx->sc, ctx->part, nb, ctx->s_main));
+                             ctx->nranks, ctx->sc, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO, ctx->counter + 2,
+                             ctx->s_main));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
-    if ((st = reduce_slots(ctx, ctx->part, nb, 2, RED_RHO, done)) != NEK_OK) return st;
+    if ((st = exchange_slots(ctx)) != NEK_OK) return st;
     {
         Scope sc(ctx, CLS_VEC);
         CK(launch_pcg_pupdate(ctx->n, ctx->vdinv, ctx->vr, ctx->vp, ctx->red_all, ctx->nranks, ctx->sc, ctx->hist,
@@ -558,10 +581,10 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     {
         Scope sc(ctx, CLS_VEC);
         CK(launch_pcg_init(ctx->n, ctx->mbits, ctx->obits, bd, ctx->vdinv, ctx->vr, ctx->vp, ctx->vx, ctx->part, nb,
-                           ctx->s_main));
+                           ctx->red_loc + RED_RHO, ctx->counter + 2, ctx->s_main));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
-    if ((st = reduce_slots(ctx, ctx->part, nb, 2, RED_RHO, nullptr)) != NEK_OK) return st;
+    if ((st = exchange_slots(ctx)) != NEK_OK) return st;
     CK(launch_pcg_init_fin(ctx->sc, ctx->red_all, ctx->nranks, ctx->hist, ctx->s_main));
     ctx->stats.launches += 1;
 

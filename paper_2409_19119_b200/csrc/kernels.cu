@@ -15,6 +15,7 @@
 
 #include <cstdint>
 
+#include "ax_tma.cuh"
 #include "nek_ctx.h"
 
 namespace nekb200 {
@@ -174,34 +175,6 @@ __global__ void __launch_bounds__(NQ *NQ)
     }
 }
 
-int ax_partials_needed(int variant, int N, int64_t E) { (void)variant; (void)N; return (int)E; }
-
-template <int NQ>
-static void ax_v0_launch(int64_t nelem, int64_t eoff, const int32_t *elist, const double *u, const double *G,
-                         const double *wJ, const uint32_t *mbits, double h1, double h2, double *w, double *part,
-                         const int *done, cudaStream_t s)
-{
-    ax_v0_kernel<NQ><<<(unsigned)nelem, NQ * NQ, 0, s>>>(eoff, elist, u, G, wJ, mbits, h1, h2, w, part, done);
-}
-
-cudaError_t launch_ax(int variant, int N, int64_t nelem, int64_t eoff, const int32_t *elist, const double *u,
-                      const double *G, const double *wJ, const uint32_t *mbits, double h1, double h2, double *w,
-                      double *part, const int *done, cudaStream_t s, int *nlaunch)
-{
-    (void)variant;
-    if (nelem <= 0) return cudaSuccess;
-    switch (N) {
-#define NEK_CASE(NN) \
-    case NN: ax_v0_launch<NN + 1>(nelem, eoff, elist, u, G, wJ, mbits, h1, h2, w, part, done, s); break;
-        NEK_CASE(1) NEK_CASE(2) NEK_CASE(3) NEK_CASE(4) NEK_CASE(5) NEK_CASE(6) NEK_CASE(7) NEK_CASE(8)
-        NEK_CASE(9) NEK_CASE(10) NEK_CASE(11) NEK_CASE(12) NEK_CASE(13) NEK_CASE(14) NEK_CASE(15)
-#undef NEK_CASE
-    default: return cudaErrorInvalidValue;
-    }
-    if (nlaunch) ++*nlaunch;
-    return cudaGetLastError();
-}
-
 // Fixed-order reduction of count x nd partials (row-major [count][nd]) into dst[nd].
 __global__ void reduce_kernel(const double *__restrict__ part, int64_t count, int nd, double *__restrict__ dst,
                               const int *done)
@@ -220,6 +193,611 @@ cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst
 {
     reduce_kernel<<<1, 1024, 0, s>>>(part, count, nd, dst, done);
     return cudaGetLastError();
+}
+
+// Last CTA to finish sums part[0..count) (fixed order) into dst[0] and resets the counter.
+__device__ __forceinline__ void last_block_finish(double *part, int64_t count, double *dst, unsigned int *counter,
+                                                  double *sred, int *s_last)
+{
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (*s_last) {
+        __threadfence();
+        double a = 0.0;
+        for (int64_t c = threadIdx.x; c < count; c += blockDim.x) a += ((volatile double *)part)[c];
+        a = block_sum(a, sred);
+        if (threadIdx.x == 0) { dst[0] = a; *counter = 0u; }
+    }
+}
+
+// ------------------------------------------------------------------- Ax v1
+template <bool HELM>
+__global__ void __launch_bounds__(AXV1_THREADS, AXV1_CTAS_PER_SM)
+    ax_v1_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *__restrict__ u,
+                 const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
+                 double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
+                 int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done)
+{
+    constexpr int NQ = AXV1_NQ, P3 = 512, N = NQ - 1;
+    constexpr uint32_t BYTES = (7 + (HELM ? 1 : 0)) * P3 * 8;
+    if (done && *(volatile const int *)done) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    AxV1Smem<HELM> &S = *reinterpret_cast<AxV1Smem<HELM> *>(smem_raw);
+    const int t = threadIdx.x, i = t & 7, j = t >> 3;
+    const int64_t nit = (int64_t)blockIdx.x < nelem ? (nelem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint64_t pol = tma::policy_evict_first();
+
+    auto elem_of = [&](int64_t it) -> int64_t {
+        const int64_t pos = eoff + blockIdx.x + it * (int64_t)gridDim.x;
+        return elist ? (int64_t)elist[pos] : pos;
+    };
+    auto issue = [&](int64_t it, int st) {
+        const int64_t e = elem_of(it);
+        tma::fence_proxy_async();
+        tma::mbar_arrive_expect_tx(&S.full[st], BYTES);
+        tma::bulk_g2s(S.stage[st], u + e * P3, P3 * 8, &S.full[st], pol);
+        tma::bulk_g2s(S.stage[st] + P3, G + e * 6 * P3, 6 * P3 * 8, &S.full[st], pol);
+        if (HELM) tma::bulk_g2s(S.stage[st] + 7 * P3, wJ + e * P3, P3 * 8, &S.full[st], pol);
+    };
+    if (t == 0) {
+        tma::mbar_init(&S.full[0], 1);
+        tma::mbar_init(&S.full[1], 1);
+        tma::fence_mbar_init();
+    }
+    __syncthreads();
+    if (t == 0) {
+        if (nit > 0) issue(0, 0);
+        if (nit > 1) issue(1, 1);
+    }
+    double Dri[NQ], Drj[NQ], Dci[NQ], Dcj[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) {
+        Dri[m] = c_D[N][i * NQ + m]; Drj[m] = c_D[N][j * NQ + m];
+        Dci[m] = c_D[N][m * NQ + i]; Dcj[m] = c_D[N][m * NQ + j];
+    }
+    S.sD[t] = c_D[N][t];                 // D row-major, read warp-uniformly for the t direction
+    double dot = 0.0;
+    for (int64_t it = 0; it < nit; ++it) {
+        const int st = (int)(it & 1);
+        const int64_t e = elem_of(it);
+        tma::mbar_wait(&S.full[st], (uint32_t)((it >> 1) & 1));
+        const double *su = S.stage[st];
+        const double *sG = su + P3;
+        double ru[NQ], ut[NQ], gt[NQ], rw[NQ];
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+            double v = su[k * 64 + t];
+            if (mbits && bit_of(mbits, e * P3 + k * 64 + t)) v = 0.0;
+            ru[k] = v;
+        }
+        // t direction on the thread's own k-column: ut = D ru
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+            double a = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 d = *reinterpret_cast<const double2 *>(&S.sD[k * NQ + m]);
+                a = fma(d.x, ru[m], a);
+                a = fma(d.y, ru[m + 1], a);
+            }
+            ut[k] = a;
+        }
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+            S.sa[t] = ru[k];
+            __syncthreads();
+            double ur = 0.0, us = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) {
+                ur = fma(Dri[m], S.sa[j * NQ + m], ur);
+                us = fma(Drj[m], S.sa[m * NQ + i], us);
+            }
+            const int q = k * 64 + t;
+            const double Grr = sG[q], Grs = sG[P3 + q], Grt = sG[2 * P3 + q];
+            const double Gss = sG[3 * P3 + q], Gst = sG[4 * P3 + q], Gtt = sG[5 * P3 + q];
+            const double gr = Grr * ur + Grs * us + Grt * ut[k];
+            const double gs = Grs * ur + Gss * us + Gst * ut[k];
+            gt[k] = Grt * ur + Gst * us + Gtt * ut[k];
+            S.sb[t] = gr;
+            S.sc[t] = gs;
+            __syncthreads();
+            double acc = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) {
+                acc = fma(Dci[m], S.sb[j * NQ + m], acc);
+                acc = fma(Dcj[m], S.sc[m * NQ + i], acc);
+            }
+            rw[k] = acc;
+        }
+        // transposed t direction: rw += D^T gt on the k-column
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 d = *reinterpret_cast<const double2 *>(&S.sD[k * NQ + m]);
+                rw[m] = fma(d.x, gt[k], rw[m]);
+                rw[m + 1] = fma(d.y, gt[k], rw[m + 1]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+            const int64_t l = e * P3 + k * 64 + t;
+            double v = h1 * rw[k];
+            if (HELM) v = fma(h2 * su[7 * P3 + k * 64 + t], ru[k], v);
+            if (mbits && bit_of(mbits, l)) v = 0.0;
+            w[l] = v;
+            dot = fma(ru[k], v, dot);
+        }
+        __syncthreads();   // stage `st` fully consumed by all threads
+        if (t == 0 && it + 2 < nit) issue(it + 2, st);
+    }
+    if (part) {
+        const double s = block_sum(dot, S.sred);
+        if (t == 0) part[part_off + blockIdx.x] = s;
+        if (fin_total > 0) last_block_finish(part, fin_total, dst, counter, S.sred, &S.last);
+    }
+}
+
+// ------------------------------------------------------------------- Ax v2
+// Same staging as v1 (2-stage TMA ring per CTA), but KS k-groups of 64 threads
+// share each element: 64*KS threads per CTA.  Accumulations are split into
+// independent partial sums (ILP) and the Dirichlet words ride along in the TMA
+// transaction.
+template <bool HELM, int KS>
+__global__ void __launch_bounds__(64 * KS, KS == 2 ? 3 : 2)
+    ax_v2_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *__restrict__ u,
+                 const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
+                 double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
+                 int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done)
+{
+    constexpr int NQ = 8, P3 = 512, N = 7, KPG = NQ / KS;
+    const uint32_t BYTES = (7 + (HELM ? 1 : 0)) * P3 * 8 + (mbits ? 64 : 0);
+    if (done && *(volatile const int *)done) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    AxV2Smem<HELM, KS> &S = *reinterpret_cast<AxV2Smem<HELM, KS> *>(smem_raw);
+    const int t = threadIdx.x, c = t & 63, g = t >> 6, i = c & 7, j = c >> 3;
+    const int k0 = g * KPG;
+    const int64_t nit = (int64_t)blockIdx.x < nelem ? (nelem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint64_t pol = tma::policy_evict_first();
+
+    auto elem_of = [&](int64_t it) -> int64_t {
+        const int64_t pos = eoff + blockIdx.x + it * (int64_t)gridDim.x;
+        return elist ? (int64_t)elist[pos] : pos;
+    };
+    auto issue = [&](int64_t it, int st) {
+        const int64_t e = elem_of(it);
+        tma::fence_proxy_async();
+        tma::mbar_arrive_expect_tx(&S.full[st], BYTES);
+        tma::bulk_g2s(S.stage[st], u + e * P3, P3 * 8, &S.full[st], pol);
+        tma::bulk_g2s(S.stage[st] + P3, G + e * 6 * P3, 6 * P3 * 8, &S.full[st], pol);
+        if (HELM) tma::bulk_g2s(S.stage[st] + 7 * P3, wJ + e * P3, P3 * 8, &S.full[st], pol);
+        if (mbits) tma::bulk_g2s(S.mstage[st], mbits + e * 16, 64, &S.full[st], pol);
+    };
+    if (t == 0) {
+        tma::mbar_init(&S.full[0], 1);
+        tma::mbar_init(&S.full[1], 1);
+        tma::fence_mbar_init();
+    }
+    if (t < 64) S.sD[t] = c_D[N][t];
+    __syncthreads();
+    if (t == 0) {
+        if (nit > 0) issue(0, 0);
+        if (nit > 1) issue(1, 1);
+    }
+    double Dri[NQ], Drj[NQ], Dci[NQ], Dcj[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) {
+        Dri[m] = S.sD[i * NQ + m]; Drj[m] = S.sD[j * NQ + m];
+        Dci[m] = S.sD[m * NQ + i]; Dcj[m] = S.sD[m * NQ + j];
+    }
+    double dot = 0.0;
+    double *sa = S.sa[g], *sb = S.sb[g], *sc = S.sc[g];
+    for (int64_t it = 0; it < nit; ++it) {
+        const int st = (int)(it & 1);
+        const int64_t e = elem_of(it);
+        tma::mbar_wait(&S.full[st], (uint32_t)((it >> 1) & 1));
+        const double *su = S.stage[st];
+        const double *sG = su + P3;
+        const uint32_t *mw = S.mstage[st];
+        // the whole k-column of u (masked): needed by the t contraction
+        double ru[NQ];
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+            double v = su[k * 64 + c];
+            if (mbits && ((mw[2 * k + (c >> 5)] >> (c & 31)) & 1u)) v = 0.0;
+            ru[k] = v;
+        }
+        double ut[KPG], gt[KPG], rw[KPG];
+#pragma unroll
+        for (int kk = 0; kk < KPG; ++kk) {
+            const double *Dk = S.sD + (k0 + kk) * NQ;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 d = *reinterpret_cast<const double2 *>(Dk + m);
+                a0 = fma(d.x, ru[m], a0);
+                a1 = fma(d.y, ru[m + 1], a1);
+            }
+            ut[kk] = a0 + a1;
+        }
+#pragma unroll
+        for (int kk = 0; kk < KPG; ++kk) {
+            const int k = k0 + kk;
+            double uk = su[k * 64 + c];
+            if (mbits && ((mw[2 * k + (c >> 5)] >> (c & 31)) & 1u)) uk = 0.0;
+            sa[c] = uk;
+            __syncthreads();
+            double ur0 = 0.0, ur1 = 0.0, us0 = 0.0, us1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 a = *reinterpret_cast<const double2 *>(sa + j * NQ + m);
+                ur0 = fma(Dri[m], a.x, ur0);
+                ur1 = fma(Dri[m + 1], a.y, ur1);
+                us0 = fma(Drj[m], sa[m * NQ + i], us0);
+                us1 = fma(Drj[m + 1], sa[(m + 1) * NQ + i], us1);
+            }
+            const double ur = ur0 + ur1, us = us0 + us1;
+            const int q = k * 64 + c;
+            const double Grr = sG[q], Grs = sG[P3 + q], Grt = sG[2 * P3 + q];
+            const double Gss = sG[3 * P3 + q], Gst = sG[4 * P3 + q], Gtt = sG[5 * P3 + q];
+            sb[c] = Grr * ur + Grs * us + Grt * ut[kk];
+            sc[c] = Grs * ur + Gss * us + Gst * ut[kk];
+            gt[kk] = Grt * ur + Gst * us + Gtt * ut[kk];
+            __syncthreads();
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 x = *reinterpret_cast<const double2 *>(sb + j * NQ + m);
+                a0 = fma(Dci[m], x.x, a0);
+                a1 = fma(Dci[m + 1], x.y, a1);
+                b0 = fma(Dcj[m], sc[m * NQ + i], b0);
+                b1 = fma(Dcj[m + 1], sc[(m + 1) * NQ + i], b1);
+            }
+            rw[kk] = (a0 + a1) + (b0 + b1);
+        }
+        // transposed t contraction: this group's slices contribute to every k
+        double pt[NQ];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) pt[m] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KPG; ++kk) {
+            const double *Dk = S.sD + (k0 + kk) * NQ;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 d = *reinterpret_cast<const double2 *>(Dk + m);
+                pt[m] = fma(d.x, gt[kk], pt[m]);
+                pt[m + 1] = fma(d.y, gt[kk], pt[m + 1]);
+            }
+        }
+        if (KS > 1) {
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) S.spart[g][m][c] = pt[m];
+            __syncthreads();
+        }
+#pragma unroll
+        for (int kk = 0; kk < KPG; ++kk) {
+            const int k = k0 + kk;
+            double tt;
+            if (KS > 1) {
+                tt = S.spart[0][k][c];
+#pragma unroll
+                for (int gg = 1; gg < KS; ++gg) tt += S.spart[gg][k][c];
+            } else {
+                tt = pt[kk];
+            }
+            const int64_t l = e * P3 + k * 64 + c;
+            const bool masked = mbits && ((mw[2 * k + (c >> 5)] >> (c & 31)) & 1u);
+            const double uk = masked ? 0.0 : su[k * 64 + c];
+            double v = h1 * (rw[kk] + tt);
+            if (HELM) v = fma(h2 * su[7 * P3 + k * 64 + c], uk, v);
+            if (masked) v = 0.0;
+            w[l] = v;
+            dot = fma(uk, v, dot);
+        }
+        __syncthreads();   // stage `st` fully consumed
+        if (t == 0 && it + 2 < nit) issue(it + 2, st);
+    }
+    if (part) {
+        const double sum = block_sum(dot, S.sred);
+        if (t == 0) part[part_off + blockIdx.x] = sum;
+        if (fin_total > 0) last_block_finish(part, fin_total, dst, counter, S.sred, &S.last);
+    }
+}
+
+template <bool HELM, int KS>
+static cudaError_t ax_v2_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
+                                const uint32_t *mbits, double h1, double h2, double *w, int64_t grid, cudaStream_t s)
+{
+    static bool attr = false;
+    const size_t smem = sizeof(AxV2Smem<HELM, KS>);
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(ax_v2_kernel<HELM, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    ax_v2_kernel<HELM, KS><<<(unsigned)grid, 64 * KS, smem, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2,
+                                                                w, L.part, L.part_off, L.fin_total, L.dst,
+                                                                L.counter, L.done);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- Ax v3
+template <bool HELM, int KS>
+__global__ void __launch_bounds__(64 * KS, KS == 1 ? 6 : 3)
+    ax_v3_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *__restrict__ u,
+                 const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
+                 double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
+                 int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done)
+{
+    constexpr int NQ = 8, P3 = 512, N = 7, KPG = NQ / KS, PF = 2;
+    if (done && *(volatile const int *)done) return;
+    __shared__ AxV3Smem<KS> S;
+    const int t = threadIdx.x, c = t & 63, g = t >> 6, i = c & 7, j = c >> 3;
+    const int k0 = g * KPG;
+    const int64_t nit = (int64_t)blockIdx.x < nelem ? (nelem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint64_t pol = tma::policy_evict_first();
+    auto elem_of = [&](int64_t it) -> int64_t {
+        const int64_t pos = eoff + blockIdx.x + it * (int64_t)gridDim.x;
+        return elist ? (int64_t)elist[pos] : pos;
+    };
+    auto prefetch = [&](int64_t it) {
+        const int64_t e = elem_of(it);
+        tma::prefetch_l2(u + e * P3, P3 * 8);
+        tma::prefetch_l2(G + e * 6 * P3, 6 * P3 * 8);
+        if (HELM) tma::prefetch_l2(wJ + e * P3, P3 * 8);
+        if (mbits) tma::prefetch_l2(mbits + e * 16, 64);
+    };
+    if (t == 0)
+        for (int a = 0; a < PF && a < nit; ++a) prefetch(a);
+    if (t < 64) S.sD[t] = c_D[N][t];
+    __syncthreads();
+    double Dri[NQ], Drj[NQ], Dci[NQ], Dcj[NQ];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) {
+        Dri[m] = S.sD[i * NQ + m]; Drj[m] = S.sD[j * NQ + m];
+        Dci[m] = S.sD[m * NQ + i]; Dcj[m] = S.sD[m * NQ + j];
+    }
+    double dot = 0.0;
+    double *sa = S.sa[g], *sb = S.sb[g], *sc = S.sc[g];
+    for (int64_t it = 0; it < nit; ++it) {
+        const int64_t e = elem_of(it);
+        if (t == 0 && it + PF < nit) prefetch(it + PF);
+        const double *ue = u + e * P3;
+        const double *Ge = G + e * 6 * (int64_t)P3;
+        uint32_t mw[2 * NQ];
+        if (mbits) {
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) mw[2 * k] = __ldg(mbits + e * 16 + 2 * k + (c >> 5)) >> (c & 31);
+        }
+        double ru[NQ];
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+            double v = tma::ldg_ef(ue + k * 64 + c, pol);
+            if (mbits && (mw[2 * k] & 1u)) v = 0.0;
+            ru[k] = v;
+        }
+        double ut[KPG], gt[KPG], rw[KPG];
+#pragma unroll
+        for (int kk = 0; kk < KPG; ++kk) {
+            const double *Dk = S.sD + (k0 + kk) * NQ;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 d = *reinterpret_cast<const double2 *>(Dk + m);
+                a0 = fma(d.x, ru[m], a0);
+                a1 = fma(d.y, ru[m + 1], a1);
+            }
+            ut[kk] = a0 + a1;
+        }
+        double Gn[6];
+#pragma unroll
+        for (int a = 0; a < 6; ++a) Gn[a] = tma::ldg_ef(Ge + a * P3 + k0 * 64 + c, pol);
+#pragma unroll
+        for (int kk = 0; kk < KPG; ++kk) {
+            const int k = k0 + kk;
+            double Gc[6];
+#pragma unroll
+            for (int a = 0; a < 6; ++a) Gc[a] = Gn[a];
+            if (kk + 1 < KPG) {
+#pragma unroll
+                for (int a = 0; a < 6; ++a) Gn[a] = tma::ldg_ef(Ge + a * P3 + (k + 1) * 64 + c, pol);
+            }
+            if (KS == 1) {
+                sa[c] = ru[kk];
+            } else {
+                double uk = ue[k * 64 + c];
+                if (mbits && ((__ldg(mbits + e * 16 + 2 * k + (c >> 5)) >> (c & 31)) & 1u)) uk = 0.0;
+                sa[c] = uk;
+            }
+            __syncthreads();
+            double ur0 = 0.0, ur1 = 0.0, us0 = 0.0, us1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 a = *reinterpret_cast<const double2 *>(sa + j * NQ + m);
+                ur0 = fma(Dri[m], a.x, ur0);
+                ur1 = fma(Dri[m + 1], a.y, ur1);
+                us0 = fma(Drj[m], sa[m * NQ + i], us0);
+                us1 = fma(Drj[m + 1], sa[(m + 1) * NQ + i], us1);
+            }
+            const double ur = ur0 + ur1, us = us0 + us1;
+            sb[c] = Gc[0] * ur + Gc[1] * us + Gc[2] * ut[kk];
+            sc[c] = Gc[1] * ur + Gc[3] * us + Gc[4] * ut[kk];
+            gt[kk] = Gc[2] * ur + Gc[4] * us + Gc[5] * ut[kk];
+            __syncthreads();
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 x = *reinterpret_cast<const double2 *>(sb + j * NQ + m);
+                a0 = fma(Dci[m], x.x, a0);
+                a1 = fma(Dci[m + 1], x.y, a1);
+                b0 = fma(Dcj[m], sc[m * NQ + i], b0);
+                b1 = fma(Dcj[m + 1], sc[(m + 1) * NQ + i], b1);
+            }
+            rw[kk] = (a0 + a1) + (b0 + b1);
+        }
+        double pt[NQ];
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) pt[m] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KPG; ++kk) {
+            const double *Dk = S.sD + (k0 + kk) * NQ;
+#pragma unroll
+            for (int m = 0; m < NQ; m += 2) {
+                const double2 d = *reinterpret_cast<const double2 *>(Dk + m);
+                pt[m] = fma(d.x, gt[kk], pt[m]);
+                pt[m + 1] = fma(d.y, gt[kk], pt[m + 1]);
+            }
+        }
+        if (KS > 1) {
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) S.spart[g][m][c] = pt[m];
+            __syncthreads();
+        }
+#pragma unroll
+        for (int kk = 0; kk < KPG; ++kk) {
+            const int k = k0 + kk;
+            double tt;
+            if (KS > 1) {
+                tt = S.spart[0][k][c];
+#pragma unroll
+                for (int gg = 1; gg < KS; ++gg) tt += S.spart[gg][k][c];
+            } else {
+                tt = pt[kk];
+            }
+            const int64_t l = e * P3 + k * 64 + c;
+            bool masked;
+            double uk;
+            if (KS == 1) { uk = ru[kk]; masked = mbits && (mw[2 * kk] & 1u); }
+            else {
+                masked = mbits && ((__ldg(mbits + e * 16 + 2 * k + (c >> 5)) >> (c & 31)) & 1u);
+                uk = masked ? 0.0 : ue[k * 64 + c];
+            }
+            double v = h1 * (rw[kk] + tt);
+            if (HELM) v = fma(h2 * wJ[l], uk, v);
+            if (masked) v = 0.0;
+            w[l] = v;
+            dot = fma(uk, v, dot);
+        }
+        if (KS > 1) __syncthreads();   // spart reuse
+    }
+    if (part) {
+        const double sum = block_sum(dot, S.sred);
+        if (t == 0) part[part_off + blockIdx.x] = sum;
+        if (fin_total > 0) last_block_finish(part, fin_total, dst, counter, S.sred, &S.last);
+    }
+}
+
+template <bool HELM, int KS>
+static cudaError_t ax_v3_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
+                                const uint32_t *mbits, double h1, double h2, double *w, int64_t grid, cudaStream_t s)
+{
+    ax_v3_kernel<HELM, KS><<<(unsigned)grid, 64 * KS, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
+                                                             L.part, L.part_off, L.fin_total, L.dst, L.counter,
+                                                             L.done);
+    return cudaGetLastError();
+}
+
+// variant (N = 7): 0 = default (v3, 1 k-group), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
+// 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups
+static int per_sm_of(int variant)
+{
+    switch (variant) {
+    case 0: return 6;
+    case 2: return 3;
+    case 3: return 3;
+    case 4: return 2;
+    case 5: return 3;
+    default: return 0;
+    }
+}
+int64_t ax_grid(int variant, int N, int64_t nelem)
+{
+    if (nelem <= 0) return 0;
+    if (N == 7 && per_sm_of(variant) > 0) return std::min<int64_t>(nelem, (int64_t)per_sm_of(variant) * 148);
+    return nelem;
+}
+
+int ax_partials_needed(int variant, int N, int64_t E) { return (int)std::max<int64_t>(2 * ax_grid(variant, N, E), E); }
+
+template <bool HELM>
+static cudaError_t ax_v1_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
+                                const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s)
+{
+    static bool attr = false;
+    const size_t smem = sizeof(AxV1Smem<HELM>);
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(ax_v1_kernel<HELM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t grid = ax_grid(2, 7, L.nelem);
+    ax_v1_kernel<HELM><<<(unsigned)grid, AXV1_THREADS, smem, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
+                                                                  L.part, L.part_off, L.fin_total, L.dst, L.counter,
+                                                                  L.done);
+    return cudaGetLastError();
+}
+
+template <int NQ>
+static void ax_v0_launch(int64_t nelem, int64_t eoff, const int32_t *elist, const double *u, const double *G,
+                         const double *wJ, const uint32_t *mbits, double h1, double h2, double *w, double *part,
+                         const int *done, cudaStream_t s)
+{
+    ax_v0_kernel<NQ><<<(unsigned)nelem, NQ * NQ, 0, s>>>(eoff, elist, u, G, wJ, mbits, h1, h2, w, part, done);
+}
+
+cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
+                      const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch)
+{
+    if (L.nelem <= 0) {
+        if (L.fin_total > 0 && L.part) {   // nothing to compute here, but the reduction must still happen
+            if (nlaunch) ++*nlaunch;
+            return launch_reduce(L.part, L.fin_total, 1, L.dst, L.done, s);
+        }
+        return cudaSuccess;
+    }
+    if (N == 7 && variant == 2) {
+        if (nlaunch) ++*nlaunch;
+        return h2 != 0.0 ? ax_v1_launch<true>(L, u, G, wJ, mbits, h1, h2, w, s)
+                         : ax_v1_launch<false>(L, u, G, wJ, mbits, h1, h2, w, s);
+    }
+    if (N == 7 && (variant == 3 || variant == 4)) {
+        if (nlaunch) ++*nlaunch;
+        const int64_t grid = ax_grid(variant, N, L.nelem);
+        if (variant == 4)
+            return h2 != 0.0 ? ax_v2_launch<true, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                             : ax_v2_launch<false, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+        return h2 != 0.0 ? ax_v2_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                         : ax_v2_launch<false, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+    }
+    if (N == 7 && (variant == 0 || variant == 5)) {
+        if (nlaunch) ++*nlaunch;
+        const int64_t grid = ax_grid(variant, N, L.nelem);
+        if (variant == 0)
+            return h2 != 0.0 ? ax_v3_launch<true, 1>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                             : ax_v3_launch<false, 1>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+        return h2 != 0.0 ? ax_v3_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                         : ax_v3_launch<false, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+    }
+    double *part = L.part ? L.part + L.part_off - L.eoff : nullptr;   // v0 writes part[eoff + block]
+    switch (N) {
+#define NEK_CASE(NN) \
+    case NN: ax_v0_launch<NN + 1>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w, part, L.done, s); break;
+        NEK_CASE(1) NEK_CASE(2) NEK_CASE(3) NEK_CASE(4) NEK_CASE(5) NEK_CASE(6) NEK_CASE(7) NEK_CASE(8)
+        NEK_CASE(9) NEK_CASE(10) NEK_CASE(11) NEK_CASE(12) NEK_CASE(13) NEK_CASE(14) NEK_CASE(15)
+#undef NEK_CASE
+    default: return cudaErrorInvalidValue;
+    }
+    if (nlaunch) ++*nlaunch;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (L.fin_total > 0 && L.part) {
+        if (nlaunch) ++*nlaunch;
+        return launch_reduce(L.part, L.fin_total, 1, L.dst, L.done, s);
+    }
+    return cudaSuccess;
 }
 
 // ---------------------------------------------------------- gather-scatter
@@ -241,6 +819,82 @@ cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *o
 {
     if (nruns <= 0) return cudaSuccess;
     gs_local_kernel<<<(unsigned)((nruns + 255) / 256), 256, 0, s>>>(nruns, perm, offs, v, done);
+    return cudaGetLastError();
+}
+
+// Runs grouped by length (2: face, 4: edge, 8: vertex nodes of a box; anything
+// else generic), each class kept in canonical first-touch order, copies
+// ascending: the sum order of every run is unchanged (bit-exact with the
+// oracle) but fixed-length runs need no offsets and load their indices as one
+// vector (one dependent load level fewer).
+constexpr int GS_PAIRS_PER_THREAD = 4, GS_QUADS_PER_THREAD = 2;
+
+__global__ void __launch_bounds__(256)
+    gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
+                      const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
+                      const int32_t *__restrict__ og, double *__restrict__ v, const int *done)
+{
+    if (done && *(volatile const int *)done) return;
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t w2 = (n2 + GS_PAIRS_PER_THREAD - 1) / GS_PAIRS_PER_THREAD;
+    const int64_t w4 = (n4 + GS_QUADS_PER_THREAD - 1) / GS_QUADS_PER_THREAD;
+    if (r < w2) {   // up to 4 face pairs: all index loads, then all value loads, then the stores
+        const int64_t r0 = r * GS_PAIRS_PER_THREAD;
+        const int cnt = (int)(n2 - r0 < GS_PAIRS_PER_THREAD ? n2 - r0 : GS_PAIRS_PER_THREAD);
+        int2 c[GS_PAIRS_PER_THREAD];
+        double a[GS_PAIRS_PER_THREAD], b[GS_PAIRS_PER_THREAD];
+#pragma unroll
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (q < cnt) c[q] = p2[r0 + q];
+#pragma unroll
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (q < cnt) { a[q] = v[c[q].x]; b[q] = v[c[q].y]; }
+#pragma unroll
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
+            if (q < cnt) { const double s = a[q] + b[q]; v[c[q].x] = s; v[c[q].y] = s; }
+        return;
+    }
+    r -= w2;
+    if (r < w4) {
+        const int64_t r0 = r * GS_QUADS_PER_THREAD;
+        const int cnt = (int)(n4 - r0 < GS_QUADS_PER_THREAD ? n4 - r0 : GS_QUADS_PER_THREAD);
+        int4 c[GS_QUADS_PER_THREAD];
+        double a[GS_QUADS_PER_THREAD][4];
+#pragma unroll
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (q < cnt) c[q] = p4[r0 + q];
+#pragma unroll
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
+            if (q < cnt) { a[q][0] = v[c[q].x]; a[q][1] = v[c[q].y]; a[q][2] = v[c[q].z]; a[q][3] = v[c[q].w]; }
+#pragma unroll
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
+            if (q < cnt) {
+                const double s = ((a[q][0] + a[q][1]) + a[q][2]) + a[q][3];
+                v[c[q].x] = s; v[c[q].y] = s; v[c[q].z] = s; v[c[q].w] = s;
+            }
+        return;
+    }
+    r -= w4;
+    if (r < n8) {
+        const int4 a = p8[2 * r], b = p8[2 * r + 1];
+        const double s = ((((((v[a.x] + v[a.y]) + v[a.z]) + v[a.w]) + v[b.x]) + v[b.y]) + v[b.z]) + v[b.w];
+        v[a.x] = s; v[a.y] = s; v[a.z] = s; v[a.w] = s;
+        v[b.x] = s; v[b.y] = s; v[b.z] = s; v[b.w] = s;
+        return;
+    }
+    r -= n8;
+    if (r < ng) {
+        const int o0 = og[r], o1 = og[r + 1];
+        double s = v[pg[o0]];
+        for (int c = o0 + 1; c < o1; ++c) s += v[pg[c]];
+        for (int c = o0; c < o1; ++c) v[pg[c]] = s;
+    }
+}
+
+cudaError_t launch_gs_classes(const GsClasses &C, double *v, const int *done, cudaStream_t s)
+{
+    const int64_t tot = (C.n2 + GS_PAIRS_PER_THREAD - 1) / GS_PAIRS_PER_THREAD +
+                        (C.n4 + GS_QUADS_PER_THREAD - 1) / GS_QUADS_PER_THREAD + C.n8 + C.ng;
+    if (tot <= 0) return cudaSuccess;
+    gs_classes_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4,
+                                                                    C.n8, (const int4 *)C.p8, C.ng, C.pg, C.og, v, done);
     return cudaGetLastError();
 }
 
@@ -365,15 +1019,47 @@ cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const double *src
 
 // --------------------------------------------------------------------- PCG
 constexpr int VEC_THREADS = 256;
-int vec_blocks() { return 148 * 8; }
+constexpr int VEC_UNROLL = 4;
+int vec_blocks() { return 148 * 4; }
+int upd_blocks() { return 148 * 2; }
 
-// r = M b, p = Dinv r, x = 0; partials [<r, Dinv r>_o, <r, r>_o] per block.
+// red_all holds [nranks][RED_N]; sums are taken in rank order.
+__device__ __forceinline__ double rank_sum(const double *red_all, int nranks, int slot)
+{
+    double s = red_all[slot];
+    for (int q = 1; q < nranks; ++q) s += red_all[q * RED_N + slot];
+    return s;
+}
+
+// r = M b, p = Dinv r, x = 0; [<r, Dinv r>_o, <r, r>_o] reduced by the last CTA into dst[0..1].
+__device__ __forceinline__ void last_block_finish2(double *part, int nblk, double *dst, unsigned int *counter,
+                                                   double *sred, int *s_last)
+{
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (*s_last) {
+        __threadfence();
+        double a0 = 0.0, a1 = 0.0;
+        for (int c = threadIdx.x; c < nblk; c += blockDim.x) {
+            a0 += ((volatile double *)part)[2 * c];
+            a1 += ((volatile double *)part)[2 * c + 1];
+        }
+        a0 = block_sum(a0, sred);
+        a1 = block_sum(a1, sred);
+        if (threadIdx.x == 0) { dst[0] = a0; dst[1] = a1; *counter = 0u; }
+    }
+}
+
 __global__ void __launch_bounds__(VEC_THREADS)
     pcg_init_kernel(int64_t n, const uint32_t *__restrict__ mbits, const uint32_t *__restrict__ obits,
                     const double *__restrict__ b, const double *__restrict__ dinv, double *__restrict__ r,
-                    double *__restrict__ p, double *__restrict__ x, double *__restrict__ part)
+                    double *__restrict__ p, double *__restrict__ x, double *__restrict__ part, double *dst,
+                    unsigned int *counter)
 {
     __shared__ double sred[VEC_THREADS];
+    __shared__ int s_last;
     double a0 = 0.0, a1 = 0.0;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x) {
         const double rv = bit_of(mbits, l) ? 0.0 : b[l];
@@ -386,23 +1072,17 @@ __global__ void __launch_bounds__(VEC_THREADS)
     a0 = block_sum(a0, sred);
     a1 = block_sum(a1, sred);
     if (threadIdx.x == 0) { part[2 * blockIdx.x] = a0; part[2 * blockIdx.x + 1] = a1; }
+    last_block_finish2(part, gridDim.x, dst, counter, sred, &s_last);
 }
 
 cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *obits, const double *b,
                             const double *dinv, double *r, double *p, double *x, double *part, int nblk,
-                            cudaStream_t s)
+                            double *dst, unsigned int *counter, cudaStream_t s)
 {
-    pcg_init_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, mbits, obits, b, dinv, r, p, x, part);
+    pcg_init_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, mbits, obits, b, dinv, r, p, x, part, dst, counter);
     return cudaGetLastError();
 }
 
-// red_all holds [nranks][RED_N]; sums are taken in rank order.
-__device__ __forceinline__ double rank_sum(const double *red_all, int nranks, int slot)
-{
-    double s = red_all[slot];
-    for (int q = 1; q < nranks; ++q) s += red_all[q * RED_N + slot];
-    return s;
-}
 
 __global__ void pcg_init_fin_kernel(PcgScalars *sc, const double *red_all, int nranks, double *hist)
 {
@@ -425,47 +1105,78 @@ cudaError_t launch_pcg_init_fin(PcgScalars *sc, const double *red_all, int nrank
     return cudaGetLastError();
 }
 
-// alpha = rho / sigma; x += alpha p; r -= alpha w; partials [<r, Dinv r>_o, <r, r>_o].
-__global__ void __launch_bounds__(VEC_THREADS)
+// alpha = rho / sigma; x += alpha p; r -= alpha w; [<r, Dinv r>_o, <r, r>_o]
+// reduced by the last CTA into dst[0..1].  Two points per thread (16-byte loads).
+__global__ void __launch_bounds__(VEC_THREADS, 2)
     pcg_update_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                       const double *__restrict__ p, const double *__restrict__ w, double *__restrict__ x,
                       double *__restrict__ r, const double *__restrict__ red_all, int nranks, PcgScalars *sc,
-                      double *__restrict__ part)
+                      double *__restrict__ part, double *dst, unsigned int *counter)
 {
     __shared__ double sred[VEC_THREADS];
+    __shared__ int s_last;
     if (*(volatile int *)&sc->done) return;
     const double sigma = rank_sum(red_all, nranks, RED_SIGMA);
     if (!(sigma > 0.0)) {                       // breakdown: <p, A p> <= 0
-        if (blockIdx.x == 0 && threadIdx.x == 0) { sc->status = NEK_ENOTSPD; }
+        if (blockIdx.x == 0 && threadIdx.x == 0) sc->status = NEK_ENOTSPD;
         return;
     }
     const double alpha = sc->rho / sigma;
     double a0 = 0.0, a1 = 0.0;
-    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n2 = n >> 1;
+    const double2 *p2 = reinterpret_cast<const double2 *>(p), *w2 = reinterpret_cast<const double2 *>(w);
+    const double2 *d2 = reinterpret_cast<const double2 *>(dinv);
+    double2 *x2 = reinterpret_cast<double2 *>(x), *r2 = reinterpret_cast<double2 *>(r);
+    // VEC_UNROLL double2 per thread per tile, strided by blockDim (coalesced), all loads issued first
+    const int64_t tile = (int64_t)VEC_UNROLL * blockDim.x;
+    for (int64_t base = blockIdx.x * tile + threadIdx.x; base < n2; base += (int64_t)gridDim.x * tile) {
+        double2 pv[VEC_UNROLL], wv[VEC_UNROLL], dv[VEC_UNROLL], xv[VEC_UNROLL], rv[VEC_UNROLL];
+        uint32_t ow[VEC_UNROLL];
+#pragma unroll
+        for (int q = 0; q < VEC_UNROLL; ++q) {
+            const int64_t h = base + (int64_t)q * blockDim.x;
+            if (h < n2) {
+                pv[q] = p2[h]; wv[q] = w2[h]; dv[q] = d2[h]; xv[q] = x2[h]; rv[q] = r2[h];
+                ow[q] = __ldg(obits + ((2 * h) >> 5)) >> ((2 * h) & 31);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < VEC_UNROLL; ++q) {
+            const int64_t h = base + (int64_t)q * blockDim.x;
+            if (h < n2) {
+                xv[q].x = fma(alpha, pv[q].x, xv[q].x); xv[q].y = fma(alpha, pv[q].y, xv[q].y);
+                rv[q].x = fma(-alpha, wv[q].x, rv[q].x); rv[q].y = fma(-alpha, wv[q].y, rv[q].y);
+                x2[h] = xv[q]; r2[h] = rv[q];
+                if (ow[q] & 1u) { a0 = fma(rv[q].x, dv[q].x * rv[q].x, a0); a1 = fma(rv[q].x, rv[q].x, a1); }
+                if (ow[q] & 2u) { a0 = fma(rv[q].y, dv[q].y * rv[q].y, a0); a1 = fma(rv[q].y, rv[q].y, a1); }
+            }
+        }
+    }
+    if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        const int64_t l = n - 1;
         x[l] = fma(alpha, p[l], x[l]);
         const double rv = fma(-alpha, w[l], r[l]);
         r[l] = rv;
-        if (bit_of(obits, l)) {
-            a0 = fma(rv, dinv[l] * rv, a0);
-            a1 = fma(rv, rv, a1);
-        }
+        if (bit_of(obits, l)) { a0 = fma(rv, dinv[l] * rv, a0); a1 = fma(rv, rv, a1); }
     }
     a0 = block_sum(a0, sred);
     a1 = block_sum(a1, sred);
     if (threadIdx.x == 0) { part[2 * blockIdx.x] = a0; part[2 * blockIdx.x + 1] = a1; }
+    last_block_finish2(part, gridDim.x, dst, counter, sred, &s_last);
 }
 
 cudaError_t launch_pcg_update(int64_t n, const uint32_t *obits, const double *dinv, const double *p,
                               const double *w, double *x, double *r, const double *red_all, int nranks,
-                              PcgScalars *sc, double *part, int nblk, cudaStream_t s)
+                              PcgScalars *sc, double *part, int nblk, double *dst, unsigned int *counter,
+                              cudaStream_t s)
 {
-    pcg_update_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, p, w, x, r, red_all, nranks, sc, part);
+    pcg_update_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, p, w, x, r, red_all, nranks, sc, part, dst, counter);
     return cudaGetLastError();
 }
 
 // beta = rho'/rho; p = Dinv r + beta p.  The last block to finish updates the
 // scalars (rho <- rho', iteration count, history, convergence, breakdown).
-__global__ void __launch_bounds__(VEC_THREADS)
+__global__ void __launch_bounds__(VEC_THREADS, 4)
     pcg_pupdate_kernel(int64_t n, const double *__restrict__ dinv, const double *__restrict__ r,
                        double *__restrict__ p, const double *__restrict__ red_all, int nranks, PcgScalars *sc,
                        double *__restrict__ hist, unsigned int *counter)
@@ -478,8 +1189,28 @@ __global__ void __launch_bounds__(VEC_THREADS)
     const bool conv = sqrt(rr) <= tol * bb;
     if (!breakdown && !conv) {
         const double beta = rho1 / rho;
-        for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x)
-            p[l] = fma(beta, p[l], dinv[l] * r[l]);
+        const int64_t n2 = n >> 1;
+        const double2 *d2 = reinterpret_cast<const double2 *>(dinv), *r2 = reinterpret_cast<const double2 *>(r);
+        double2 *p2 = reinterpret_cast<double2 *>(p);
+        const int64_t tile = (int64_t)VEC_UNROLL * blockDim.x;
+        for (int64_t base = blockIdx.x * tile + threadIdx.x; base < n2; base += (int64_t)gridDim.x * tile) {
+            double2 dv[VEC_UNROLL], rv[VEC_UNROLL], pv[VEC_UNROLL];
+#pragma unroll
+            for (int q = 0; q < VEC_UNROLL; ++q) {
+                const int64_t h = base + (int64_t)q * blockDim.x;
+                if (h < n2) { dv[q] = d2[h]; rv[q] = r2[h]; pv[q] = p2[h]; }
+            }
+#pragma unroll
+            for (int q = 0; q < VEC_UNROLL; ++q) {
+                const int64_t h = base + (int64_t)q * blockDim.x;
+                if (h < n2) {
+                    pv[q].x = fma(beta, pv[q].x, dv[q].x * rv[q].x);
+                    pv[q].y = fma(beta, pv[q].y, dv[q].y * rv[q].y);
+                    p2[h] = pv[q];
+                }
+            }
+        }
+        if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) p[n - 1] = fma(beta, p[n - 1], dinv[n - 1] * r[n - 1]);
     }
     __threadfence();
     __syncthreads();

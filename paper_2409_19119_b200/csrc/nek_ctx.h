@@ -42,10 +42,29 @@ void deriv_matrix(int N, const double *x, double *D);
 cudaError_t upload_D(int N, const double *D);
 cudaError_t launch_geom(int N, int64_t E, const double *xyz, double *G, double *wJ, const double *wq,
                         unsigned long long *bad, cudaStream_t s);
-cudaError_t launch_ax(int variant, int N, int64_t nelem, int64_t eoff, const int32_t *elist, const double *u,
-                      const double *G, const double *wJ, const uint32_t *mbits, double h1, double h2, double *w,
-                      double *part, const int *done, cudaStream_t s, int *nlaunch);
+// One Ax launch over elements [eoff, eoff + nelem) of `elist` (or of 0..E-1 when
+// elist is NULL).  part/part_off: where its per-CTA <u, w> partials go; when
+// fin_total > 0 the launch also reduces part[0..fin_total) into dst[0].
+struct AxLaunch {
+    int64_t nelem = 0, eoff = 0;
+    const int32_t *elist = nullptr;
+    double *part = nullptr;
+    int64_t part_off = 0, fin_total = 0;
+    double *dst = nullptr;
+    unsigned int *counter = nullptr;   // [0] pupdate, [1] Ax, [2] init/update
+    const int *done = nullptr;
+};
+cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
+                      const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch);
+int64_t ax_grid(int variant, int N, int64_t nelem);      // partial slots one launch writes
 int ax_partials_needed(int variant, int N, int64_t E);
+
+// gather-scatter runs grouped by length (see kernels.cu)
+struct GsClasses {
+    int64_t n2 = 0, n4 = 0, n8 = 0, ng = 0;
+    const int32_t *p2 = nullptr, *p4 = nullptr, *p8 = nullptr, *pg = nullptr, *og = nullptr;
+};
+cudaError_t launch_gs_classes(const GsClasses &C, double *v, const int *done, cudaStream_t s);
 cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst, const int *done, cudaStream_t s);
 cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *offs, double *v, const int *done,
                             cudaStream_t s);
@@ -61,15 +80,17 @@ cudaError_t launch_dinv(int64_t n, const uint32_t *mbits, const double *d, doubl
 cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const double *src, double *dst, cudaStream_t s);
 cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *obits, const double *b,
                             const double *dinv, double *r, double *p, double *x, double *part, int nblk,
-                            cudaStream_t s);
+                            double *dst, unsigned int *counter, cudaStream_t s);
 cudaError_t launch_pcg_init_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_update(int64_t n, const uint32_t *obits, const double *dinv, const double *p,
                               const double *w, double *x, double *r, const double *red_all, int nranks,
-                              PcgScalars *sc, double *part, int nblk, cudaStream_t s);
+                              PcgScalars *sc, double *part, int nblk, double *dst, unsigned int *counter,
+                              cudaStream_t s);
 cudaError_t launch_pcg_pupdate(int64_t n, const double *dinv, const double *r, double *p, const double *red_all,
                                int nranks, PcgScalars *sc, double *hist, unsigned int *counter, int nblk,
                                cudaStream_t s);
 int vec_blocks();
+int upd_blocks();
 
 }  // namespace nekb200
 
@@ -91,6 +112,8 @@ struct nek_ctx {
     // maps (device)
     int32_t *perm = nullptr, *offs = nullptr;
     int64_t nruns = 0, nperm = 0;
+    int32_t *gs_p2 = nullptr, *gs_p4 = nullptr, *gs_p8 = nullptr, *gs_pg = nullptr, *gs_og = nullptr;
+    nekb200::GsClasses gsc;
     int32_t *ifc_perm = nullptr, *ifc_offs = nullptr, *send_run = nullptr, *coffs = nullptr, *contrib = nullptr;
     int64_t nifc = 0, nifc_perm = 0, nslots = 0;
     std::vector<int32_t> neighbors;
@@ -106,7 +129,7 @@ struct nek_ctx {
     int64_t npart = 0;
     double *red_loc = nullptr, *red_all = nullptr;
     nekb200::PcgScalars *sc = nullptr, *sc_host = nullptr;
-    unsigned int *counter = nullptr;
+    unsigned int *counter = nullptr;   // [0] pupdate, [1] Ax, [2] init/update
     double *hist = nullptr;
     int64_t hist_cap = 0;
     // Jacobi cache
