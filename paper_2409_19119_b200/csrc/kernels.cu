@@ -700,12 +700,379 @@ static cudaError_t ax_v3_launch(const AxLaunch &L, const double *u, const double
     return cudaGetLastError();
 }
 
-// variant (N = 7): 0 = default (v3, 1 k-group), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
-// 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups
+// ------------------------------------------------------------------- Ax v4
+// FP64 tensor cores (DMMA, mma.sync m8n8k4 f64) for the r and t contractions,
+// registers for the s contraction, no shared-memory staging of the streams.
+// One CTA = 4 warps per element; warp w owns the j-slabs {2w, 2w+1}; lane
+// (q = lane & 3, r = lane >> 2) owns the points (i = 2q + v, j, k = r),
+// v in {0,1}, which is exactly the m8n8 accumulator layout of an 8x8 (k, i)
+// slab.  Contractions over i use a permuted K order (K = 2q + s) so the
+// accumulator of one product feeds the A operand of the next without shuffles;
+// the contraction over k needs k in the K position, so u is also loaded in
+// the transposed layout (an L1 hit) and g_t goes through a per-warp shared
+// transpose.  The j contraction stays inside each thread's j-line (u) or goes
+// through one CTA-wide exchange (g_s).
+__device__ __forceinline__ void dmma8x8x4(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+struct AxV4Smem {
+    alignas(16) double sD[64];
+    alignas(16) double sGS[2][8][8][8];    // [parity][k][j][i] g_s exchange
+    alignas(16) double sGT[4][2][8][8];    // [warp][slab][k][i] g_t transpose
+    double sred[128];
+    int last;
+};
+
+template <bool HELM>
+__global__ void __launch_bounds__(128, 3)
+    ax_v4_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *__restrict__ u,
+                 const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
+                 double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
+                 int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done)
+{
+    constexpr int P3 = 512, N = 7;
+    if (done && *(volatile const int *)done) return;
+    __shared__ AxV4Smem S;
+    const int t = threadIdx.x, lane = t & 31, wq = t >> 5, q = lane & 3, r = lane >> 2;
+    const int64_t nit = (int64_t)blockIdx.x < nelem ? (nelem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint64_t pol = tma::policy_evict_first();
+    if (t < 64) S.sD[t] = c_D[N][t];
+    __syncthreads();
+    // D fragments
+    double Br[2], At[2], Bt[2], Atr[2];
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+        Br[s2] = S.sD[r * 8 + 2 * q + s2];       // r fwd   B(K=(s,q), n=r) = D(i_out=r, m=2q+s)
+        At[s2] = S.sD[r * 8 + 4 * s2 + q];       // t fwd   A(r, K=(s,q))   = D(k_out=r, m=4s+q)
+        Bt[s2] = S.sD[(2 * q + s2) * 8 + r];     // r trans B(K=(s,q), n=r) = D(i=2q+s, i'=r)
+        Atr[s2] = S.sD[(4 * s2 + q) * 8 + r];    // t trans A(r, K=(s,q))   = D(k=4s+q, k'=r)
+    }
+    const int jb = 2 * wq;                       // this warp's first slab
+    double dot = 0.0;
+    for (int64_t it = 0; it < nit; ++it) {
+        const int64_t pos = eoff + blockIdx.x + it * (int64_t)gridDim.x;
+        const int64_t e = elist ? (int64_t)elist[pos] : pos;
+        const double *ue = u + e * P3;
+        const double *Ge = G + e * 6 * (int64_t)P3;
+        const int par = (int)(it & 1);
+        // Dirichlet words of the element: lanes 0..15 hold one each
+        uint32_t mword = 0u;
+        if (mbits && lane < 16) mword = __ldg(mbits + e * 16 + lane);
+        // ---- loads: own j-lines of u, transposed u for the t-fwd B operand, own metric factors
+        double2 uo[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) uo[m] = *reinterpret_cast<const double2 *>(ue + 64 * r + 8 * m + 2 * q);
+        double ub[2][2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) ub[jj][s2] = ue[64 * (4 * s2 + q) + 8 * (jb + jj) + r];
+        double2 Gv[2][6];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int a = 0; a < 6; ++a)
+                Gv[jj][a] = *reinterpret_cast<const double2 *>(Ge + a * P3 + 64 * r + 8 * (jb + jj) + 2 * q);
+        if (mbits) {
+            const uint32_t w0 = __shfl_sync(0xffffffffu, mword, 2 * r), w1 = __shfl_sync(0xffffffffu, mword, 2 * r + 1);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const uint32_t wd = (m < 4 ? w0 : w1) >> (8 * (m & 3) + 2 * q);
+                if (wd & 1u) uo[m].x = 0.0;
+                if (wd & 2u) uo[m].y = 0.0;
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const uint32_t wd = __shfl_sync(0xffffffffu, mword, 2 * (4 * s2 + q) + (wq >> 1));
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj)
+                    if ((wd >> (8 * ((jb + jj) & 3) + r)) & 1u) ub[jj][s2] = 0.0;
+            }
+        }
+        // ---- per own slab: r and t forward (DMMA), s forward (registers), metric, r transposed (DMMA)
+        double2 acc[2], uj[2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {   // this warp's two slabs of u again (L1 hit; a runtime index
+            const int j = jb + jj;         // into uo[] would go to local memory)
+            uj[jj] = *reinterpret_cast<const double2 *>(ue + 64 * r + 8 * j + 2 * q);
+            if (mbits) {
+                const uint32_t wd = __shfl_sync(0xffffffffu, mword, 2 * r + (j >> 2)) >> (8 * (j & 3) + 2 * q);
+                if (wd & 1u) uj[jj].x = 0.0;
+                if (wd & 2u) uj[jj].y = 0.0;
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int j = jb + jj;
+            double ur0 = 0.0, ur1 = 0.0, ut0 = 0.0, ut1 = 0.0;
+            dmma8x8x4(ur0, ur1, uj[jj].x, Br[0]);
+            dmma8x8x4(ur0, ur1, uj[jj].y, Br[1]);
+            dmma8x8x4(ut0, ut1, At[0], ub[jj][0]);
+            dmma8x8x4(ut0, ut1, At[1], ub[jj][1]);
+            double us0a = 0.0, us0b = 0.0, us1a = 0.0, us1b = 0.0;
+#pragma unroll
+            for (int m = 0; m < 8; m += 2) {
+                const double2 d = *reinterpret_cast<const double2 *>(S.sD + j * 8 + m);
+                us0a = fma(d.x, uo[m].x, us0a); us0b = fma(d.y, uo[m + 1].x, us0b);
+                us1a = fma(d.x, uo[m].y, us1a); us1b = fma(d.y, uo[m + 1].y, us1b);
+            }
+            const double us0 = us0a + us0b, us1 = us1a + us1b;
+            const double2 *Gj = Gv[jj];
+            const double gr0 = Gj[0].x * ur0 + Gj[1].x * us0 + Gj[2].x * ut0;
+            const double gr1 = Gj[0].y * ur1 + Gj[1].y * us1 + Gj[2].y * ut1;
+            const double gs0 = Gj[1].x * ur0 + Gj[3].x * us0 + Gj[4].x * ut0;
+            const double gs1 = Gj[1].y * ur1 + Gj[3].y * us1 + Gj[4].y * ut1;
+            const double gt0 = Gj[2].x * ur0 + Gj[4].x * us0 + Gj[5].x * ut0;
+            const double gt1 = Gj[2].y * ur1 + Gj[4].y * us1 + Gj[5].y * ut1;
+            double wr0 = 0.0, wr1 = 0.0;
+            dmma8x8x4(wr0, wr1, gr0, Bt[0]);
+            dmma8x8x4(wr0, wr1, gr1, Bt[1]);
+            acc[jj] = make_double2(wr0, wr1);
+            *reinterpret_cast<double2 *>(&S.sGS[par][r][j][2 * q]) = make_double2(gs0, gs1);
+            *reinterpret_cast<double2 *>(&S.sGT[wq][jj][r][2 * q]) = make_double2(gt0, gt1);
+        }
+        __syncwarp();
+        // ---- t transposed (DMMA) from the per-warp transpose buffer
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            double wt0 = 0.0, wt1 = 0.0;
+            dmma8x8x4(wt0, wt1, Atr[0], S.sGT[wq][jj][q][r]);
+            dmma8x8x4(wt0, wt1, Atr[1], S.sGT[wq][jj][4 + q][r]);
+            acc[jj].x += wt0;
+            acc[jj].y += wt1;
+        }
+        __syncthreads();                                  // sGS[par] complete
+        // ---- s transposed: w_s(i, j', k) = sum_j D(j, j') g_s(i, j, k)
+        double2 gsl[8];
+#pragma unroll
+        for (int jx = 0; jx < 8; ++jx) gsl[jx] = *reinterpret_cast<const double2 *>(&S.sGS[par][r][jx][2 * q]);
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int j = jb + jj;
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+            for (int jx = 0; jx < 8; jx += 2) {
+                const double d0 = S.sD[jx * 8 + j], d1 = S.sD[(jx + 1) * 8 + j];
+                a0 = fma(d0, gsl[jx].x, a0); b0 = fma(d1, gsl[jx + 1].x, b0);
+                a1 = fma(d0, gsl[jx].y, a1); b1 = fma(d1, gsl[jx + 1].y, b1);
+            }
+            const int64_t l = e * P3 + 64 * r + 8 * j + 2 * q;
+            double v0 = h1 * (acc[jj].x + (a0 + b0)), v1 = h1 * (acc[jj].y + (a1 + b1));
+            if (HELM) {
+                const double2 wj = *reinterpret_cast<const double2 *>(wJ + l);
+                v0 = fma(h2 * wj.x, uj[jj].x, v0);
+                v1 = fma(h2 * wj.y, uj[jj].y, v1);
+            }
+            if (mbits) {
+                const uint32_t wd = __shfl_sync(0xffffffffu, mword, 2 * r + (j >> 2)) >> (8 * (j & 3) + 2 * q);
+                if (wd & 1u) v0 = 0.0;
+                if (wd & 2u) v1 = 0.0;
+            }
+            *reinterpret_cast<double2 *>(w + l) = make_double2(v0, v1);
+            dot = fma(uj[jj].x, v0, dot);
+            dot = fma(uj[jj].y, v1, dot);
+        }
+    }
+    if (part) {
+        const double sum = block_sum(dot, S.sred);
+        if (t == 0) part[part_off + blockIdx.x] = sum;
+        if (fin_total > 0) last_block_finish(part, fin_total, dst, counter, S.sred, &S.last);
+    }
+    (void)pol;
+}
+
+template <bool HELM>
+static cudaError_t ax_v4_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
+                                const uint32_t *mbits, double h1, double h2, double *w, int64_t grid, cudaStream_t s)
+{
+    ax_v4_kernel<HELM><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w, L.part,
+                                                       L.part_off, L.fin_total, L.dst, L.counter, L.done);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- Ax v5
+// v4 with the roles of j and k exchanged: a warp owns the k-slabs {2w, 2w+1},
+// lane (q, r) the points (i = 2q + v, j = r, k).  Every per-slab load or store
+// of a warp is then one contiguous 512-byte (j, i) plane (4 L1 wavefronts
+// instead of 8), the t contraction runs on the thread's own k-line in
+// registers, and DMMA does the r (over i) and s (over j) contractions.
+struct AxV5Smem {
+    alignas(16) double sD[64];
+    alignas(16) double sGT[2][8][8][8];    // [parity][k][j][i] g_t exchange (CTA-wide)
+    alignas(16) double sGS[4][2][8][8];    // [warp][slab][j][i] g_s transpose (per warp)
+    double sred[128];
+    int last;
+};
+
+template <bool HELM>
+__global__ void __launch_bounds__(128, 3)
+    ax_v5_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *__restrict__ u,
+                 const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
+                 double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
+                 int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done)
+{
+    constexpr int P3 = 512, N = 7;
+    if (done && *(volatile const int *)done) return;
+    __shared__ AxV5Smem S;
+    const int t = threadIdx.x, lane = t & 31, wq = t >> 5, q = lane & 3, r = lane >> 2;
+    const int64_t nit = (int64_t)blockIdx.x < nelem ? (nelem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (t < 64) S.sD[t] = c_D[N][t];
+    __syncthreads();
+    double Br[2], As[2], Bt[2], Ast[2];
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+        Br[s2] = S.sD[r * 8 + 2 * q + s2];       // r fwd   B(K=(s,q), n=r) = D(i_out=r, m=2q+s)
+        As[s2] = S.sD[r * 8 + 4 * s2 + q];       // s fwd   A(r, K=(s,q))   = D(j_out=r, m=4s+q)
+        Bt[s2] = S.sD[(2 * q + s2) * 8 + r];     // r trans B(K=(s,q), n=r) = D(i=2q+s, i'=r)
+        Ast[s2] = S.sD[(4 * s2 + q) * 8 + r];    // s trans A(r, K=(s,q))   = D(j=4s+q, j'=r)
+    }
+    const int kb = 2 * wq;                       // this warp's first k-slab
+    double dot = 0.0;
+    for (int64_t it = 0; it < nit; ++it) {
+        const int64_t pos = eoff + blockIdx.x + it * (int64_t)gridDim.x;
+        const int64_t e = elist ? (int64_t)elist[pos] : pos;
+        const double *ue = u + e * P3;
+        const double *Ge = G + e * 6 * (int64_t)P3;
+        const int par = (int)(it & 1);
+        uint32_t mword = 0u;
+        if (mbits && lane < 16) mword = __ldg(mbits + e * 16 + lane);
+        double2 uc[8];                           // own k-line
+#pragma unroll
+        for (int m = 0; m < 8; ++m) uc[m] = *reinterpret_cast<const double2 *>(ue + 64 * m + 8 * r + 2 * q);
+        double2 uk[2];                           // own slabs (L1 hits)
+        double ub[2][2];                         // s-fwd B operand: u(i = r, j = 4s+q, k)
+        double2 Gv[2][6];
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            const int k = kb + kk;
+            uk[kk] = *reinterpret_cast<const double2 *>(ue + 64 * k + 8 * r + 2 * q);
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) ub[kk][s2] = ue[64 * k + 8 * (4 * s2 + q) + r];
+#pragma unroll
+            for (int a = 0; a < 6; ++a)
+                Gv[kk][a] = *reinterpret_cast<const double2 *>(Ge + a * P3 + 64 * k + 8 * r + 2 * q);
+        }
+        if (mbits) {
+            // own point (i=2q+v, j=r, k): word 2k + (r >> 2), bit 8 (r & 3) + 2q + v
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const uint32_t wd = __shfl_sync(0xffffffffu, mword, 2 * m + (r >> 2)) >> (8 * (r & 3) + 2 * q);
+                if (wd & 1u) uc[m].x = 0.0;
+                if (wd & 2u) uc[m].y = 0.0;
+            }
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                const int k = kb + kk;
+                const uint32_t wd = __shfl_sync(0xffffffffu, mword, 2 * k + (r >> 2)) >> (8 * (r & 3) + 2 * q);
+                if (wd & 1u) uk[kk].x = 0.0;
+                if (wd & 2u) uk[kk].y = 0.0;
+                // (i = r, j = 4s+q, k): word 2k + (j >> 2) = 2k + s, bit 8 (q) + r
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const uint32_t wb = __shfl_sync(0xffffffffu, mword, 2 * k + s2);
+                    if ((wb >> (8 * q + r)) & 1u) ub[kk][s2] = 0.0;
+                }
+            }
+        }
+        double2 acc[2];
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            const int k = kb + kk;
+            double ur0 = 0.0, ur1 = 0.0, us0 = 0.0, us1 = 0.0;
+            dmma8x8x4(ur0, ur1, uk[kk].x, Br[0]);
+            dmma8x8x4(ur0, ur1, uk[kk].y, Br[1]);
+            dmma8x8x4(us0, us1, As[0], ub[kk][0]);
+            dmma8x8x4(us0, us1, As[1], ub[kk][1]);
+            double ut0a = 0.0, ut0b = 0.0, ut1a = 0.0, ut1b = 0.0;
+#pragma unroll
+            for (int m = 0; m < 8; m += 2) {
+                const double2 d = *reinterpret_cast<const double2 *>(S.sD + k * 8 + m);
+                ut0a = fma(d.x, uc[m].x, ut0a); ut0b = fma(d.y, uc[m + 1].x, ut0b);
+                ut1a = fma(d.x, uc[m].y, ut1a); ut1b = fma(d.y, uc[m + 1].y, ut1b);
+            }
+            const double ut0 = ut0a + ut0b, ut1 = ut1a + ut1b;
+            const double2 *Gk = Gv[kk];
+            const double gr0 = Gk[0].x * ur0 + Gk[1].x * us0 + Gk[2].x * ut0;
+            const double gr1 = Gk[0].y * ur1 + Gk[1].y * us1 + Gk[2].y * ut1;
+            const double gs0 = Gk[1].x * ur0 + Gk[3].x * us0 + Gk[4].x * ut0;
+            const double gs1 = Gk[1].y * ur1 + Gk[3].y * us1 + Gk[4].y * ut1;
+            const double gt0 = Gk[2].x * ur0 + Gk[4].x * us0 + Gk[5].x * ut0;
+            const double gt1 = Gk[2].y * ur1 + Gk[4].y * us1 + Gk[5].y * ut1;
+            double wr0 = 0.0, wr1 = 0.0;
+            dmma8x8x4(wr0, wr1, gr0, Bt[0]);
+            dmma8x8x4(wr0, wr1, gr1, Bt[1]);
+            acc[kk] = make_double2(wr0, wr1);
+            *reinterpret_cast<double2 *>(&S.sGS[wq][kk][r][2 * q]) = make_double2(gs0, gs1);
+            *reinterpret_cast<double2 *>(&S.sGT[par][k][r][2 * q]) = make_double2(gt0, gt1);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {         // s transposed (DMMA)
+            double ws0 = 0.0, ws1 = 0.0;
+            dmma8x8x4(ws0, ws1, Ast[0], S.sGS[wq][kk][q][r]);
+            dmma8x8x4(ws0, ws1, Ast[1], S.sGS[wq][kk][4 + q][r]);
+            acc[kk].x += ws0;
+            acc[kk].y += ws1;
+        }
+        __syncthreads();                         // sGT[par] complete
+        double2 gtl[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) gtl[m] = *reinterpret_cast<const double2 *>(&S.sGT[par][m][r][2 * q]);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            const int k = kb + kk;
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < 8; m += 2) {
+                const double d0 = S.sD[m * 8 + k], d1 = S.sD[(m + 1) * 8 + k];
+                a0 = fma(d0, gtl[m].x, a0); b0 = fma(d1, gtl[m + 1].x, b0);
+                a1 = fma(d0, gtl[m].y, a1); b1 = fma(d1, gtl[m + 1].y, b1);
+            }
+            const int64_t l = e * P3 + 64 * k + 8 * r + 2 * q;
+            double v0 = h1 * (acc[kk].x + (a0 + b0)), v1 = h1 * (acc[kk].y + (a1 + b1));
+            if (HELM) {
+                const double2 wj = *reinterpret_cast<const double2 *>(wJ + l);
+                v0 = fma(h2 * wj.x, uk[kk].x, v0);
+                v1 = fma(h2 * wj.y, uk[kk].y, v1);
+            }
+            if (mbits) {
+                const uint32_t wd = __shfl_sync(0xffffffffu, mword, 2 * k + (r >> 2)) >> (8 * (r & 3) + 2 * q);
+                if (wd & 1u) v0 = 0.0;
+                if (wd & 2u) v1 = 0.0;
+            }
+            *reinterpret_cast<double2 *>(w + l) = make_double2(v0, v1);
+            dot = fma(uk[kk].x, v0, dot);
+            dot = fma(uk[kk].y, v1, dot);
+        }
+    }
+    if (part) {
+        const double sum = block_sum(dot, S.sred);
+        if (t == 0) part[part_off + blockIdx.x] = sum;
+        if (fin_total > 0) last_block_finish(part, fin_total, dst, counter, S.sred, &S.last);
+    }
+}
+
+template <bool HELM>
+static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
+                                const uint32_t *mbits, double h1, double h2, double *w, int64_t grid, cudaStream_t s)
+{
+    ax_v5_kernel<HELM><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w, L.part,
+                                                       L.part_off, L.fin_total, L.dst, L.counter, L.done);
+    return cudaGetLastError();
+}
+
+// variant (N = 7): 0 = default (v5, DMMA, k-slabs), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
+// 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups, 6 = v3 with 1 k-group, 7 = v4 (DMMA, j-slabs)
 static int per_sm_of(int variant)
 {
     switch (variant) {
-    case 0: return 6;
+    case 0: return 3;
+    case 7: return 3;
+    case 6: return 6;
     case 2: return 3;
     case 3: return 3;
     case 4: return 2;
@@ -772,10 +1139,22 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         return h2 != 0.0 ? ax_v2_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                          : ax_v2_launch<false, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
     }
-    if (N == 7 && (variant == 0 || variant == 5)) {
+    if (N == 7 && variant == 0) {
         if (nlaunch) ++*nlaunch;
         const int64_t grid = ax_grid(variant, N, L.nelem);
-        if (variant == 0)
+        return h2 != 0.0 ? ax_v5_launch<true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                         : ax_v5_launch<false>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+    }
+    if (N == 7 && variant == 7) {
+        if (nlaunch) ++*nlaunch;
+        const int64_t grid = ax_grid(variant, N, L.nelem);
+        return h2 != 0.0 ? ax_v4_launch<true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                         : ax_v4_launch<false>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+    }
+    if (N == 7 && (variant == 6 || variant == 5)) {
+        if (nlaunch) ++*nlaunch;
+        const int64_t grid = ax_grid(variant, N, L.nelem);
+        if (variant == 6)
             return h2 != 0.0 ? ax_v3_launch<true, 1>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v3_launch<false, 1>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
         return h2 != 0.0 ? ax_v3_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)

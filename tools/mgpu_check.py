@@ -1,0 +1,113 @@
+"""Multi-GPU parity check (run under torchrun, one process per GPU).
+
+Each rank owns a z-slab (or a block) of the elements of one mesh, sets up the
+library with an NCCL communicator, and runs nek_ax, nek_gs and nek_pcg_solve.
+Rank 0 gathers the per-rank results and compares them with the CPU oracle on
+the whole mesh (single-rank oracle; gs also against the oracle's multi-rank
+emulation, bit for bit).  Prints one JSON line on rank 0 and exits non-zero on
+failure.
+
+  python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/mgpu_check.py
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2409_19119_b200 import nek  # noqa: E402
+from workloads import meshgen as mg  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        idt.copy_(torch.frombuffer(bytearray(nek.comm_unique_id()), dtype=torch.uint8))
+    dist.broadcast(idt, 0)
+    comm = (rank, world, bytes(idt.cpu().numpy().tobytes()))
+    results = {}
+    ok = True
+    cases = [("slab_N7", lambda: mg.box_mesh(4, 3, 2 * world, 7, deform="bubble"), "slab"),
+             ("slab_N3", lambda: mg.box_mesh(3, 3, 2 * world, 3, deform="sin", eps=0.05, dirichlet="zends"), "slab"),
+             ("block_N5", lambda: mg.box_mesh(4, 4, 4, 5, deform="bubble"), "block")]
+    for name, mk, kind in cases:
+        m = mk()
+        if kind == "slab":
+            parts = mg.slab_partition(m, world)
+        else:
+            if world == 2:
+                parts = mg.block_partition(m, 2, 1, 1)
+            elif world == 4:
+                parts = mg.block_partition(m, 2, 2, 1)
+            else:
+                parts = mg.block_partition(m, 2, 2, 2)
+        sub = mg.submesh(m, parts[rank])
+        ctx = nek.setup(sub.E, sub.N, sub.xyz, sub.gid, sub.mask, comm=comm, device=local)
+        info = nek.get_info(ctx)
+        P3 = m.Nq ** 3
+        loc = (parts[rank][:, None] * P3 + np.arange(P3)).reshape(-1)
+        u = mg.random_evector(m, seed=5)[loc]
+        ud = torch.from_numpy(u).to(dev)
+        wd = torch.empty_like(ud)
+        nek.ax(ctx, 1.0, 0.3, ud, wd)
+        vd = ud.clone()
+        nek.gs(ctx, vd)
+        b = mg.smooth_field(m, seed=3)[loc]
+        xd = torch.zeros_like(ud)
+        st, it, rr, hist = nek.pcg_solve(ctx, 1.0, 0.0, torch.from_numpy(b).to(dev), xd, 0.0, 40, want_hist=True)
+        torch.cuda.synchronize()
+        payload = {"w": wd.cpu().numpy(), "v": vd.cpu().numpy(), "x": xd.cpu().numpy(), "hist": hist, "it": it,
+                   "info": info}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, payload)
+        if rank == 0:
+            import oracle
+            O = oracle.Oracle.from_mesh(m)
+            uf = mg.random_evector(m, seed=5)
+            wref = O.apply(1.0, 0.3, uf)
+            wgot = np.zeros(m.n_local); vgot = np.zeros(m.n_local); xgot = np.zeros(m.n_local)
+            for r_, pl in enumerate(gathered):
+                lr = (parts[r_][:, None] * P3 + np.arange(P3)).reshape(-1)
+                wgot[lr] = pl["w"]; vgot[lr] = pl["v"]; xgot[lr] = pl["x"]
+            ax_err = float(np.abs(wgot - wref).max() / np.abs(wref).max())
+            gs_ref_multi = oracle.gs_multi([mg.submesh(m, p).gid for p in parts],
+                                           [uf[(p[:, None] * P3 + np.arange(P3)).reshape(-1)] for p in parts])
+            gs_bit = all(np.array_equal(pl["v"], gr) for pl, gr in zip(gathered, gs_ref_multi))
+            gs_err = float(np.abs(vgot - O.gs_apply(uf)).max() / np.abs(O.gs_apply(uf)).max())
+            bf = mg.smooth_field(m, seed=3)
+            xo, ito, sto, ho = O.pcg(1.0, 0.0, bf, 0.0, 40)
+            tol = O.hist_tolerance(1.0, 0.0, bf, 40)
+            h0 = gathered[0]["hist"]
+            hist_ok = bool(np.all(np.abs(h0 - ho) <= tol)) and all(np.array_equal(pl["hist"], h0) for pl in gathered)
+            x_err = float(np.abs(xgot - xo).max() / np.abs(xo).max())
+            # copies of a node bit-identical across ranks
+            allg = np.concatenate([mg.submesh(m, p).gid for p in parts])
+            allw = np.concatenate([pl["w"] for pl in gathered])
+            order = np.argsort(allg, kind="stable")
+            sg, sw = allg[order], allw[order]
+            same = np.all((sg[1:] != sg[:-1]) | (sw[1:] == sw[:-1]))
+            case_ok = ax_err <= 1e-12 and gs_bit and gs_err <= 1e-14 and hist_ok and x_err <= 1e-10 and bool(same)
+            ok &= case_ok
+            results[name] = {"ax_err": ax_err, "gs_bitexact_vs_multirank_oracle": gs_bit, "gs_err_vs_1rank": gs_err,
+                             "hist_ok": hist_ok, "x_err": x_err, "copies_identical": bool(same), "iters": ito,
+                             "halo_doubles": [pl["info"]["halo_doubles"] for pl in gathered],
+                             "neighbors": [pl["info"]["n_neighbors"] for pl in gathered], "ok": case_ok}
+        nek.free(ctx)
+    if rank == 0:
+        print(json.dumps({"world": world, "ok": bool(ok), "cases": results}))
+    okt = torch.tensor([1 if ok else 0], device=dev)
+    dist.broadcast(okt, 0)
+    dist.destroy_process_group()
+    return 0 if okt.item() == 1 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -18,6 +18,7 @@ ap.add_argument("--h2", type=float, default=0.0)
 ap.add_argument("--ez", type=int, default=16)
 ap.add_argument("--order", type=int, default=7)
 ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--flush", action="store_true", help="write 256 MiB before every nek_ax (cold L2)")
 a = ap.parse_args()
 m = mg.box_mesh(16, 16, a.ez, a.order, deform="bubble", dirichlet="all")
 ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask)
@@ -26,7 +27,10 @@ nek.set_timing(ctx, True)   # eager launches (one kernel per node in the profile
 b = torch.from_numpy(mg.smooth_field(m, 1)).cuda()
 x = torch.zeros_like(b)
 w = torch.empty_like(b)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(a.ax):
+    if a.flush:
+        flush.fill_(1)
     nek.ax(ctx, 1.0, a.h2, b, w)
 for _ in range(a.solves):
     nek.pcg_solve(ctx, 1.0, a.h2, b, x, 0.0, a.iters)
