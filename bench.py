@@ -85,7 +85,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thr = threading.Thread(target=self._read, daemon=True)
             self.thr.start()
@@ -98,7 +98,12 @@ class ClockSampler:
             if len(parts) == len(self.FIELDS):
                 self.samples.append(parts)
 
+    def mark(self):
+        """Samples before this call are outside the timed region."""
+        self.start_idx = len(self.samples)
+
     def stop(self):
+        self.samples = self.samples[getattr(self, "start_idx", 0):] or self.samples[-3:]
         if self.proc:
             self.proc.terminate()
             try:
@@ -172,11 +177,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(nek.comm_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        comm = (rank, world, bytes(idt.cpu().numpy().tobytes()))
+        comm = nek.comm_from_torch(dev)
     else:
         dist = None
         comm = None
@@ -196,6 +197,9 @@ def main():
     timing = not args.graph
     nek.set_timing(ctx, timing)
 
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(1.0)   # let nvidia-smi start sampling before the timed region
     # warm-up (also builds the Jacobi diagonal and, with --graph, the CUDA graph)
     for _ in range(args.warmup):
         nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, args.iters)
@@ -203,9 +207,8 @@ def main():
     nek.get_stats(ctx, reset=True)
 
     # ---- timed region: K PCG solves, each bracketed by events; L2 flushed between
-    clk = ClockSampler(local)
-    clk.start()
     barrier(); torch.cuda.synchronize()
+    clk.mark()
     evs = []
     for _ in range(args.steps):
         flush.fill_(1)
@@ -275,7 +278,7 @@ def main():
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
         if timing and stats["ax_launches"] > 0 and stats["ax_ms"] > 0:
             per_launch_ms = stats["ax_ms"] / stats["ax_launches"]
-            per_launch_bytes = ax_bytes_per_elem * stats["ax_elements"] / stats["ax_launches"]
+            per_launch_bytes = stats["ax_bytes"] / stats["ax_launches"]
             achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
             traffic = None
             try:
@@ -309,7 +312,7 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(mesh, 50)
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
     nek.free(ctx)
     if dist:
         dist.destroy_process_group()

@@ -67,7 +67,8 @@ enum {
 /* Communicator for multi-GPU runs.  nranks == 1 (or a NULL comm) = single GPU,
  * no NCCL.  nccl_id: the 128-byte ncclUniqueId produced on rank 0 by
  * nek_comm_unique_id and broadcast to every rank by the caller (the Python
- * binding uses torch.distributed). */
+ * binding uses torch.distributed).  An id bootstraps exactly one communicator:
+ * every nek_setup with nranks > 1 needs a fresh id. */
 typedef struct {
     int rank;
     int nranks;
@@ -190,6 +191,7 @@ typedef struct {
     int64_t ax_launches, gs_launches, halo_launches, vec_launches;
     int64_t launches;                          /* all kernels launched by the library */
     int64_t ax_elements;                       /* elements processed by Ax launches  */
+    double  ax_bytes;                          /* algorithmic HBM bytes of those launches */
 } nek_stats_t;
 
 int nek_set_timing(nek_ctx *ctx, int on);

@@ -136,6 +136,10 @@ static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w,
     ctx->stats.ax_launches += L.nelem > 0;
     ctx->stats.launches += nl;
     ctx->stats.ax_elements += L.nelem;
+    // algorithmic HBM bytes: u, 6 metric factors, w (+ wJ for Helmholtz),
+    // + r, Dinv, x, p in and p, x out when the PCG direction update is fused into the prologue
+    const double per_pt = 8.0 * (1 + 6 + 1 + (h2 != 0.0 ? 1 : 0) + (L.fused ? 5 : 0));
+    ctx->stats.ax_bytes += per_pt * (double)ctx->P3 * (double)L.nelem;
     return NEK_OK;
 }
 
@@ -191,12 +195,18 @@ static int gs_full(nek_ctx *ctx, double *v, const int *done)
 }
 
 // w = M QQ^T (h1 K_L + h2 B_L) M u.  With dot: this rank's <M u, A_L M u> into
-// red_loc[RED_SIGMA] (then allgathered across ranks into red_all).
-static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, bool dot, const int *done)
+// red_loc[RED_SIGMA] (then allgathered across ranks into red_all).  fused: the
+// PCG direction / deferred x update is applied in the Ax prologue (u == vp).
+static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, bool dot, const int *done,
+                    bool fused = false)
 {
     int st;
     AxLaunch L;
     L.done = done;
+    if (fused) {
+        L.fused = true;
+        L.p = ctx->vp; L.x = ctx->vx; L.r = ctx->vr; L.dinv = ctx->vdinv; L.sc = ctx->sc;
+    }
     L.counter = ctx->counter + 1;
     L.dst = ctx->red_loc + RED_SIGMA;
     if (ctx->nranks == 1) {
@@ -525,12 +535,32 @@ int nek_gs(nek_ctx *ctx, double *v, void *stream)
     return NEK_OK;
 }
 
+static bool use_fused(const nek_ctx *ctx) { return ax_has_fused(ctx->variant, ctx->N); }
+
 // one PCG iteration (device-resident, skipped once sc->done is set)
 static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
 {
     int st;
     const int *done = &ctx->sc->done;
     const int nb = vec_blocks();
+    if (use_fused(ctx)) {
+        // Ax prologue: p = Dinv r + beta p, x += alpha p (deferred); then w = A p, sigma
+        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
+        if ((st = exchange_slots(ctx)) != NEK_OK) return st;
+        {
+            Scope sc(ctx, CLS_VEC);
+            CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
+                                       ctx->sc, ctx->hist, ctx->part, vec_blocks(), ctx->red_loc + RED_RHO,
+                                       ctx->counter + 2, ctx->s_main));
+            ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
+        }
+        if (ctx->nranks > 1) {
+            if ((st = exchange_slots(ctx)) != NEK_OK) return st;
+            CK(launch_pcg_iter_fin(ctx->sc, ctx->red_all, ctx->nranks, ctx->hist, ctx->s_main));
+            ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
+        }
+        return NEK_OK;
+    }
     if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done)) != NEK_OK) return st;
     if ((st = exchange_slots(ctx)) != NEK_OK) return st;
     {
@@ -581,7 +611,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     {
         Scope sc(ctx, CLS_VEC);
         CK(launch_pcg_init(ctx->n, ctx->mbits, ctx->obits, bd, ctx->vdinv, ctx->vr, ctx->vp, ctx->vx, ctx->part, nb,
-                           ctx->red_loc + RED_RHO, ctx->counter + 2, ctx->s_main));
+                           ctx->red_loc + RED_RHO, ctx->counter + 2, use_fused(ctx), ctx->s_main));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
     if ((st = exchange_slots(ctx)) != NEK_OK) return st;
@@ -610,6 +640,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
         ctx->graph_stats.gs_launches -= saved.gs_launches;
         ctx->graph_stats.halo_launches -= saved.halo_launches;
         ctx->graph_stats.vec_launches -= saved.vec_launches;
+        ctx->graph_stats.ax_bytes -= saved.ax_bytes;
         ctx->stats = saved;
         CK(cudaGraphInstantiate(&ctx->graph, g, 0));
         cudaGraphDestroy(g);
@@ -620,6 +651,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
         if (use_graph) {
             CK(cudaGraphLaunch(ctx->graph, ctx->s_main));
             const nek_stats_t &g = ctx->graph_stats;
+            ctx->stats.ax_bytes += g.ax_bytes;
             ctx->stats.launches += g.launches; ctx->stats.ax_launches += g.ax_launches;
             ctx->stats.ax_elements += g.ax_elements; ctx->stats.gs_launches += g.gs_launches;
             ctx->stats.halo_launches += g.halo_launches; ctx->stats.vec_launches += g.vec_launches;
@@ -633,6 +665,10 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
             CK(cudaStreamSynchronize(ctx->s_main));
             if (H->done) break;
         }
+    }
+    if (use_fused(ctx)) {   // the deferred x += alpha p of the last iteration
+        CK(launch_pcg_xfinal(ctx->n, ctx->sc, ctx->vp, ctx->vx, ctx->s_main));
+        ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
     CK(cudaMemcpyAsync(H, ctx->sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, ctx->s_main));
     if (dx) CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->s_main));

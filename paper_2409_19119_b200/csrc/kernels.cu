@@ -902,22 +902,27 @@ static cudaError_t ax_v4_launch(const AxLaunch &L, const double *u, const double
 // registers, and DMMA does the r (over i) and s (over j) contractions.
 struct AxV5Smem {
     alignas(16) double sD[64];
+    alignas(16) double sU[2][8][8][8];     // [parity][k][j][i] new p (fused PCG prologue)
     alignas(16) double sGT[2][8][8][8];    // [parity][k][j][i] g_t exchange (CTA-wide)
     alignas(16) double sGS[4][2][8][8];    // [warp][slab][j][i] g_s transpose (per warp)
     double sred[128];
     int last;
 };
 
-template <bool HELM>
+template <bool HELM, bool FUSED>
 __global__ void __launch_bounds__(128, 3)
-    ax_v5_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *__restrict__ u,
+    ax_v5_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *u,
                  const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
                  double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
-                 int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done)
+                 int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done,
+                 double *pvec, double *__restrict__ xvec, const double *__restrict__ rvec,
+                 const double *__restrict__ dvec, const PcgScalars *sc)
 {
     constexpr int P3 = 512, N = 7;
     if (done && *(volatile const int *)done) return;
     __shared__ AxV5Smem S;
+    double beta = 0.0, alpha = 0.0;
+    if (FUSED) { beta = sc->beta; alpha = sc->alpha; }
     const int t = threadIdx.x, lane = t & 31, wq = t >> 5, q = lane & 3, r = lane >> 2;
     const int64_t nit = (int64_t)blockIdx.x < nelem ? (nelem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (t < 64) S.sD[t] = c_D[N][t];
@@ -941,11 +946,41 @@ __global__ void __launch_bounds__(128, 3)
         uint32_t mword = 0u;
         if (mbits && lane < 16) mword = __ldg(mbits + e * 16 + lane);
         double2 uc[8];                           // own k-line
-#pragma unroll
-        for (int m = 0; m < 8; ++m) uc[m] = *reinterpret_cast<const double2 *>(ue + 64 * m + 8 * r + 2 * q);
-        double2 uk[2];                           // own slabs (L1 hits)
+        double2 uk[2];                           // own slabs
         double ub[2][2];                         // s-fwd B operand: u(i = r, j = 4s+q, k)
         double2 Gv[2][6];
+        if (FUSED) {
+            // p <- Dinv r + beta p and x <- x + alpha p on the own slabs, then share p
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                const int64_t l = e * P3 + 64 * (kb + kk) + 8 * r + 2 * q;
+                const double2 po = *reinterpret_cast<const double2 *>(pvec + l);
+                const double2 rv = *reinterpret_cast<const double2 *>(rvec + l);
+                const double2 dv = *reinterpret_cast<const double2 *>(dvec + l);
+                double2 xv = *reinterpret_cast<const double2 *>(xvec + l);
+                double2 pn;
+                pn.x = fma(beta, po.x, dv.x * rv.x);
+                pn.y = fma(beta, po.y, dv.y * rv.y);
+                xv.x = fma(alpha, po.x, xv.x);
+                xv.y = fma(alpha, po.y, xv.y);
+                *reinterpret_cast<double2 *>(pvec + l) = pn;
+                *reinterpret_cast<double2 *>(xvec + l) = xv;
+                *reinterpret_cast<double2 *>(&S.sU[par][kb + kk][r][2 * q]) = pn;
+                uk[kk] = pn;
+#pragma unroll
+                for (int a = 0; a < 6; ++a)
+                    Gv[kk][a] = *reinterpret_cast<const double2 *>(Ge + a * P3 + 64 * (kb + kk) + 8 * r + 2 * q);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < 8; ++m) uc[m] = *reinterpret_cast<const double2 *>(&S.sU[par][m][r][2 * q]);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) ub[kk][s2] = S.sU[par][kb + kk][4 * s2 + q][r];
+        } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) uc[m] = *reinterpret_cast<const double2 *>(ue + 64 * m + 8 * r + 2 * q);
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
             const int k = kb + kk;
@@ -977,6 +1012,7 @@ __global__ void __launch_bounds__(128, 3)
                     if ((wb >> (8 * q + r)) & 1u) ub[kk][s2] = 0.0;
                 }
             }
+        }
         }
         double2 acc[2];
 #pragma unroll
@@ -1060,10 +1096,18 @@ template <bool HELM>
 static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
                                 const uint32_t *mbits, double h1, double h2, double *w, int64_t grid, cudaStream_t s)
 {
-    ax_v5_kernel<HELM><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w, L.part,
-                                                       L.part_off, L.fin_total, L.dst, L.counter, L.done);
+    if (L.fused)
+        ax_v5_kernel<HELM, true><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
+                                                                 L.part, L.part_off, L.fin_total, L.dst, L.counter,
+                                                                 L.done, L.p, L.x, L.r, L.dinv, L.sc);
+    else
+        ax_v5_kernel<HELM, false><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
+                                                                  L.part, L.part_off, L.fin_total, L.dst, L.counter,
+                                                                  L.done, nullptr, nullptr, nullptr, nullptr, nullptr);
     return cudaGetLastError();
 }
+
+bool ax_has_fused(int variant, int N) { return variant == 0 && N == 7; }
 
 // variant (N = 7): 0 = default (v5, DMMA, k-slabs), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
 // 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups, 6 = v3 with 1 k-group, 7 = v4 (DMMA, j-slabs)
@@ -1208,57 +1252,64 @@ cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *o
 // vector (one dependent load level fewer).
 constexpr int GS_PAIRS_PER_THREAD = 4, GS_QUADS_PER_THREAD = 2;
 
+// Each warp takes a contiguous block of runs of one class and lane l handles
+// runs l, l+32, ... of it, so every warp-wide load touches consecutive runs
+// (first-touch order keeps their copies close in memory).
 __global__ void __launch_bounds__(256)
     gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
                       const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
                       const int32_t *__restrict__ og, double *__restrict__ v, const int *done)
 {
     if (done && *(volatile const int *)done) return;
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t w2 = (n2 + GS_PAIRS_PER_THREAD - 1) / GS_PAIRS_PER_THREAD;
-    const int64_t w4 = (n4 + GS_QUADS_PER_THREAD - 1) / GS_QUADS_PER_THREAD;
-    if (r < w2) {   // up to 4 face pairs: all index loads, then all value loads, then the stores
-        const int64_t r0 = r * GS_PAIRS_PER_THREAD;
-        const int cnt = (int)(n2 - r0 < GS_PAIRS_PER_THREAD ? n2 - r0 : GS_PAIRS_PER_THREAD);
+    int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t w2 = (n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD);
+    const int64_t w4 = (n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD);
+    const int64_t w8 = (n8 + 31) / 32;
+    if (wid < w2) {
+        const int64_t r0 = wid * 32 * GS_PAIRS_PER_THREAD + lane;
         int2 c[GS_PAIRS_PER_THREAD];
         double a[GS_PAIRS_PER_THREAD], b[GS_PAIRS_PER_THREAD];
 #pragma unroll
-        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (q < cnt) c[q] = p2[r0 + q];
-#pragma unroll
-        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (q < cnt) { a[q] = v[c[q].x]; b[q] = v[c[q].y]; }
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (r0 + 32 * q < n2) c[q] = p2[r0 + 32 * q];
 #pragma unroll
         for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
-            if (q < cnt) { const double s = a[q] + b[q]; v[c[q].x] = s; v[c[q].y] = s; }
+            if (r0 + 32 * q < n2) { a[q] = v[c[q].x]; b[q] = v[c[q].y]; }
+#pragma unroll
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
+            if (r0 + 32 * q < n2) { const double s = a[q] + b[q]; v[c[q].x] = s; v[c[q].y] = s; }
         return;
     }
-    r -= w2;
-    if (r < w4) {
-        const int64_t r0 = r * GS_QUADS_PER_THREAD;
-        const int cnt = (int)(n4 - r0 < GS_QUADS_PER_THREAD ? n4 - r0 : GS_QUADS_PER_THREAD);
+    wid -= w2;
+    if (wid < w4) {
+        const int64_t r0 = wid * 32 * GS_QUADS_PER_THREAD + lane;
         int4 c[GS_QUADS_PER_THREAD];
         double a[GS_QUADS_PER_THREAD][4];
 #pragma unroll
-        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (q < cnt) c[q] = p4[r0 + q];
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (r0 + 32 * q < n4) c[q] = p4[r0 + 32 * q];
 #pragma unroll
         for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
-            if (q < cnt) { a[q][0] = v[c[q].x]; a[q][1] = v[c[q].y]; a[q][2] = v[c[q].z]; a[q][3] = v[c[q].w]; }
+            if (r0 + 32 * q < n4) { a[q][0] = v[c[q].x]; a[q][1] = v[c[q].y]; a[q][2] = v[c[q].z]; a[q][3] = v[c[q].w]; }
 #pragma unroll
         for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
-            if (q < cnt) {
+            if (r0 + 32 * q < n4) {
                 const double s = ((a[q][0] + a[q][1]) + a[q][2]) + a[q][3];
                 v[c[q].x] = s; v[c[q].y] = s; v[c[q].z] = s; v[c[q].w] = s;
             }
         return;
     }
-    r -= w4;
-    if (r < n8) {
+    wid -= w4;
+    if (wid < w8) {
+        const int64_t r = wid * 32 + lane;
+        if (r >= n8) return;
         const int4 a = p8[2 * r], b = p8[2 * r + 1];
         const double s = ((((((v[a.x] + v[a.y]) + v[a.z]) + v[a.w]) + v[b.x]) + v[b.y]) + v[b.z]) + v[b.w];
         v[a.x] = s; v[a.y] = s; v[a.z] = s; v[a.w] = s;
         v[b.x] = s; v[b.y] = s; v[b.z] = s; v[b.w] = s;
         return;
     }
-    r -= n8;
+    wid -= w8;
+    const int64_t r = wid * 32 + lane;
     if (r < ng) {
         const int o0 = og[r], o1 = og[r + 1];
         double s = v[pg[o0]];
@@ -1269,11 +1320,12 @@ __global__ void __launch_bounds__(256)
 
 cudaError_t launch_gs_classes(const GsClasses &C, double *v, const int *done, cudaStream_t s)
 {
-    const int64_t tot = (C.n2 + GS_PAIRS_PER_THREAD - 1) / GS_PAIRS_PER_THREAD +
-                        (C.n4 + GS_QUADS_PER_THREAD - 1) / GS_QUADS_PER_THREAD + C.n8 + C.ng;
-    if (tot <= 0) return cudaSuccess;
-    gs_classes_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4,
-                                                                    C.n8, (const int4 *)C.p8, C.ng, C.pg, C.og, v, done);
+    const int64_t warps = (C.n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD) +
+                          (C.n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD) + (C.n8 + 31) / 32 +
+                          (C.ng + 31) / 32;
+    if (warps <= 0) return cudaSuccess;
+    gs_classes_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
+        C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8, (const int4 *)C.p8, C.ng, C.pg, C.og, v, done);
     return cudaGetLastError();
 }
 
@@ -1435,7 +1487,7 @@ __global__ void __launch_bounds__(VEC_THREADS)
     pcg_init_kernel(int64_t n, const uint32_t *__restrict__ mbits, const uint32_t *__restrict__ obits,
                     const double *__restrict__ b, const double *__restrict__ dinv, double *__restrict__ r,
                     double *__restrict__ p, double *__restrict__ x, double *__restrict__ part, double *dst,
-                    unsigned int *counter)
+                    unsigned int *counter, bool p_zero)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ int s_last;
@@ -1444,7 +1496,7 @@ __global__ void __launch_bounds__(VEC_THREADS)
         const double rv = bit_of(mbits, l) ? 0.0 : b[l];
         const double z = dinv[l] * rv;
         r[l] = rv;
-        p[l] = z;
+        p[l] = p_zero ? 0.0 : z;
         x[l] = 0.0;
         if (bit_of(obits, l)) { a0 = fma(rv, z, a0); a1 = fma(rv, rv, a1); }
     }
@@ -1456,9 +1508,9 @@ __global__ void __launch_bounds__(VEC_THREADS)
 
 cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *obits, const double *b,
                             const double *dinv, double *r, double *p, double *x, double *part, int nblk,
-                            double *dst, unsigned int *counter, cudaStream_t s)
+                            double *dst, unsigned int *counter, bool p_zero, cudaStream_t s)
 {
-    pcg_init_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, mbits, obits, b, dinv, r, p, x, part, dst, counter);
+    pcg_init_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, mbits, obits, b, dinv, r, p, x, part, dst, counter, p_zero);
     return cudaGetLastError();
 }
 
@@ -1472,6 +1524,8 @@ __global__ void pcg_init_fin_kernel(PcgScalars *sc, const double *red_all, int n
     sc->iter = 0;
     sc->status = NEK_MAXIT;
     sc->done = 0;
+    sc->alpha = 0.0;
+    sc->beta = 0.0;
     if (hist) hist[0] = rr > 0.0 ? 1.0 : 0.0;
     if (!(rr > 0.0)) { sc->done = 1; sc->status = NEK_OK; }              // b = 0 -> x = 0, 0 iterations
     else if (sc->tol >= 1.0) { sc->done = 1; sc->status = NEK_OK; }      // ||r0|| <= tol ||b||
@@ -1614,6 +1668,135 @@ cudaError_t launch_pcg_pupdate(int64_t n, const double *dinv, const double *r, d
                                cudaStream_t s)
 {
     pcg_pupdate_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, dinv, r, p, red_all, nranks, sc, hist, counter);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- fused PCG path
+// Iteration bookkeeping after <r, Dinv r> and <r, r> of the new residual are
+// known: history, convergence / maxit, the pending alpha for the deferred x
+// update and beta for the next direction.
+__device__ __forceinline__ void pcg_bookkeep(PcgScalars *sc, double rho1, double rr, double alpha, double *hist)
+{
+    const int it = sc->iter + 1;
+    sc->iter = it;
+    sc->rr = rr;
+    sc->alpha = alpha;
+    if (hist) hist[it] = sqrt(rr) / sc->bb;
+    sc->beta = rho1 / sc->rho;
+    sc->rho = rho1;
+    if (sqrt(rr) <= sc->tol * sc->bb) { sc->done = 1; sc->status = NEK_OK; }
+    else if (it >= sc->maxit) { sc->done = 1; sc->status = NEK_MAXIT; }
+    __threadfence();
+}
+
+__global__ void __launch_bounds__(VEC_THREADS, 4)
+    pcg_update_fused_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
+                            const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ red_all,
+                            int nranks, PcgScalars *sc, double *hist, double *__restrict__ part, double *dst,
+                            unsigned int *counter)
+{
+    __shared__ double sred[VEC_THREADS];
+    __shared__ int s_last;
+    if (*(volatile int *)&sc->done) return;
+    const double sigma = rank_sum(red_all, nranks, RED_SIGMA);
+    if (!(sigma > 0.0)) {                       // breakdown: <p, A p> <= 0
+        if (blockIdx.x == 0 && threadIdx.x == 0) { sc->status = NEK_ENOTSPD; sc->alpha = 0.0; sc->done = 1; }
+        return;
+    }
+    const double alpha = sc->rho / sigma;
+    double a0 = 0.0, a1 = 0.0;
+    const int64_t n2 = n >> 1;
+    const double2 *w2 = reinterpret_cast<const double2 *>(w), *d2 = reinterpret_cast<const double2 *>(dinv);
+    double2 *r2 = reinterpret_cast<double2 *>(r);
+    const int64_t tile = (int64_t)VEC_UNROLL * blockDim.x;
+    for (int64_t base = blockIdx.x * tile + threadIdx.x; base < n2; base += (int64_t)gridDim.x * tile) {
+        double2 wv[VEC_UNROLL], dv[VEC_UNROLL], rv[VEC_UNROLL];
+        uint32_t ow[VEC_UNROLL];
+#pragma unroll
+        for (int q = 0; q < VEC_UNROLL; ++q) {
+            const int64_t h = base + (int64_t)q * blockDim.x;
+            if (h < n2) {
+                wv[q] = w2[h]; dv[q] = d2[h]; rv[q] = r2[h];
+                ow[q] = __ldg(obits + ((2 * h) >> 5)) >> ((2 * h) & 31);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < VEC_UNROLL; ++q) {
+            const int64_t h = base + (int64_t)q * blockDim.x;
+            if (h < n2) {
+                rv[q].x = fma(-alpha, wv[q].x, rv[q].x); rv[q].y = fma(-alpha, wv[q].y, rv[q].y);
+                r2[h] = rv[q];
+                if (ow[q] & 1u) { a0 = fma(rv[q].x, dv[q].x * rv[q].x, a0); a1 = fma(rv[q].x, rv[q].x, a1); }
+                if (ow[q] & 2u) { a0 = fma(rv[q].y, dv[q].y * rv[q].y, a0); a1 = fma(rv[q].y, rv[q].y, a1); }
+            }
+        }
+    }
+    if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        const int64_t l = n - 1;
+        const double rv = fma(-alpha, w[l], r[l]);
+        r[l] = rv;
+        if (bit_of(obits, l)) { a0 = fma(rv, dinv[l] * rv, a0); a1 = fma(rv, rv, a1); }
+    }
+    a0 = block_sum(a0, sred);
+    a1 = block_sum(a1, sred);
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = a0; part[2 * blockIdx.x + 1] = a1; }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        double b0 = 0.0, b1 = 0.0;
+        for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
+            b0 += ((volatile double *)part)[2 * c];
+            b1 += ((volatile double *)part)[2 * c + 1];
+        }
+        b0 = block_sum(b0, sred);
+        b1 = block_sum(b1, sred);
+        if (threadIdx.x == 0) {
+            *counter = 0u;
+            if (nranks == 1) pcg_bookkeep(sc, b0, b1, alpha, hist);
+            else { dst[0] = b0; dst[1] = b1; }
+        }
+    }
+}
+
+cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
+                                    const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
+                                    int nblk, double *dst, unsigned int *counter, cudaStream_t s)
+{
+    pcg_update_fused_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist, part, dst,
+                                                         counter);
+    return cudaGetLastError();
+}
+
+__global__ void pcg_iter_fin_kernel(PcgScalars *sc, const double *red_all, int nranks, double *hist)
+{
+    if (sc->done) return;
+    const double sigma = rank_sum(red_all, nranks, RED_SIGMA);
+    const double alpha = sc->rho / sigma;
+    pcg_bookkeep(sc, rank_sum(red_all, nranks, RED_RHO), rank_sum(red_all, nranks, RED_RR), alpha, hist);
+}
+
+cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s)
+{
+    pcg_iter_fin_kernel<<<1, 1, 0, s>>>(sc, red_all, nranks, hist);
+    return cudaGetLastError();
+}
+
+// the deferred x += alpha p of the last iteration
+__global__ void pcg_xfinal_kernel(int64_t n, const PcgScalars *sc, const double *__restrict__ p, double *__restrict__ x)
+{
+    const double alpha = sc->alpha;
+    if (alpha == 0.0 || sc->status == NEK_ENOTSPD) return;
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x)
+        x[l] = fma(alpha, p[l], x[l]);
+}
+
+cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    pcg_xfinal_kernel<<<vec_blocks(), VEC_THREADS, 0, s>>>(n, sc, p, x);
     return cudaGetLastError();
 }
 

@@ -22,6 +22,8 @@ struct PcgScalars {
     int maxit;
     int done;          // 1 once converged / maxit / breakdown
     int status;        // NEK_OK, NEK_MAXIT, NEK_ENOTSPD
+    double alpha;      // alpha of the last update whose x += alpha p is still pending (fused path)
+    double beta;       // beta for the next direction update (fused path)
 };
 
 // Reduction slots (device): red_loc = this rank's partial sums, red_all = the
@@ -51,8 +53,14 @@ struct AxLaunch {
     double *part = nullptr;
     int64_t part_off = 0, fin_total = 0;
     double *dst = nullptr;
-    unsigned int *counter = nullptr;   // [0] pupdate, [1] Ax, [2] init/update
+    unsigned int *counter = nullptr;
     const int *done = nullptr;
+    // fused PCG prologue (Ax v5 only): p <- Dinv r + beta p, x <- x + alpha p on the
+    // element's points before the operator is applied to the new p (u == p then)
+    bool fused = false;
+    double *p = nullptr, *x = nullptr;
+    const double *r = nullptr, *dinv = nullptr;
+    const PcgScalars *sc = nullptr;
 };
 cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
                       const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch);
@@ -80,7 +88,15 @@ cudaError_t launch_dinv(int64_t n, const uint32_t *mbits, const double *d, doubl
 cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const double *src, double *dst, cudaStream_t s);
 cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *obits, const double *b,
                             const double *dinv, double *r, double *p, double *x, double *part, int nblk,
-                            double *dst, unsigned int *counter, cudaStream_t s);
+                            double *dst, unsigned int *counter, bool p_zero, cudaStream_t s);
+// fused path: r -= alpha w and the two dots; at nranks == 1 the last CTA also
+// does the iteration bookkeeping, at nranks > 1 pcg_iter_fin does it after the allgather
+cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
+                                    const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
+                                    int nblk, double *dst, unsigned int *counter, cudaStream_t s);
+cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
+cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s);
+bool ax_has_fused(int variant, int N);
 cudaError_t launch_pcg_init_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_update(int64_t n, const uint32_t *obits, const double *dinv, const double *p,
                               const double *w, double *x, double *r, const double *red_all, int nranks,

@@ -58,7 +58,7 @@ class nek_stats_t(ctypes.Structure):
     _fields_ = [("ax_ms", ctypes.c_double), ("gs_ms", ctypes.c_double), ("halo_ms", ctypes.c_double),
                 ("vec_ms", ctypes.c_double), ("ax_launches", ctypes.c_int64), ("gs_launches", ctypes.c_int64),
                 ("halo_launches", ctypes.c_int64), ("vec_launches", ctypes.c_int64), ("launches", ctypes.c_int64),
-                ("ax_elements", ctypes.c_int64)]
+                ("ax_elements", ctypes.c_int64), ("ax_bytes", ctypes.c_double)]
 
 
 _P, _I, _I64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
@@ -137,6 +137,23 @@ def comm_unique_id() -> bytes:
     buf = (ctypes.c_ubyte * 128)()
     _check(_lib.nek_comm_unique_id(buf))
     return bytes(buf)
+
+
+def comm_from_torch(device=None):
+    """A fresh (rank, nranks, nccl_id) triple for nek_setup: rank 0 creates a
+    new NCCL unique id, torch.distributed broadcasts it.  Every nek_setup needs
+    its own id (an id bootstraps exactly one communicator)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if world == 1:
+        return None
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    t = torch.zeros(128, dtype=torch.uint8, device=dev if dist.get_backend() == "nccl" else "cpu")
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(comm_unique_id()), dtype=torch.uint8))
+    dist.broadcast(t, 0)
+    return (rank, world, bytes(t.cpu().numpy().tobytes()))
 
 
 class Context:

@@ -28,11 +28,6 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-    if rank == 0:
-        idt.copy_(torch.frombuffer(bytearray(nek.comm_unique_id()), dtype=torch.uint8))
-    dist.broadcast(idt, 0)
-    comm = (rank, world, bytes(idt.cpu().numpy().tobytes()))
     results = {}
     ok = True
     cases = [("slab_N7", lambda: mg.box_mesh(4, 3, 2 * world, 7, deform="bubble"), "slab"),
@@ -50,7 +45,7 @@ def main():
             else:
                 parts = mg.block_partition(m, 2, 2, 2)
         sub = mg.submesh(m, parts[rank])
-        ctx = nek.setup(sub.E, sub.N, sub.xyz, sub.gid, sub.mask, comm=comm, device=local)
+        ctx = nek.setup(sub.E, sub.N, sub.xyz, sub.gid, sub.mask, comm=nek.comm_from_torch(dev), device=local)
         info = nek.get_info(ctx)
         P3 = m.Nq ** 3
         loc = (parts[rank][:, None] * P3 + np.arange(P3)).reshape(-1)
