@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--ez", type=int, default=EZ_PER_RANK, help="element layers per rank")
     ap.add_argument("--order", type=int, default=NORD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", type=int, default=0, help="Ax kernel variant (nek_set_variant; 0 = default)")
     ap.add_argument("--graph", action="store_true", help="time with the CUDA-graph PCG loop instead of "
                     "eager launches + per-kernel events (no roofline then)")
     return ap.parse_args()
@@ -189,6 +190,8 @@ def main():
     mesh = make_mesh(rank, world, args.ez, args.order)
     ctx = nek.setup(mesh.E, mesh.N, mesh.xyz, mesh.gid, mesh.mask, comm=comm, device=local)
     info = nek.get_info(ctx)
+    if args.variant:
+        nek.set_variant(ctx, args.variant)
     from workloads import meshgen as mg
     b = torch.from_numpy(mg.smooth_field(mesh, seed=1)).to(dev)
     x = torch.zeros_like(b)

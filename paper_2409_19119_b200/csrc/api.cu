@@ -550,7 +550,7 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
         {
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
-                                       ctx->sc, ctx->hist, ctx->part, vec_blocks(), ctx->red_loc + RED_RHO,
+                                       ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
                                        ctx->counter + 2, ctx->s_main));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }

@@ -33,8 +33,32 @@ __device__ __forceinline__ bool bit_of(const uint32_t *__restrict__ bits, int64_
     return (__ldg(bits + (l >> 5)) >> (l & 31)) & 1u;
 }
 
-// Fixed-order block sum of v (blockDim.x <= 1024); result valid in thread 0.
+// Fixed-order block sum of v (blockDim.x a multiple of 32, <= 1024): a
+// butterfly within each warp, then warp 0 folds the per-warp sums in warp
+// order.  Deterministic; result valid in thread 0.  sred needs 32 entries.
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 __device__ __forceinline__ double block_sum(double v, double *sred)
+{
+    const int t = threadIdx.x, nw = (int)(blockDim.x >> 5);
+    v = warp_sum(v);
+    if ((t & 31) == 0) sred[t >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (t < 32) {
+        r = t < nw ? sred[t] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+// Fixed-order block sum for any blockDim.x <= 1024 (smem tree); sred needs blockDim.x entries.
+__device__ __forceinline__ double block_sum_any(double v, double *sred)
 {
     const int t = threadIdx.x;
     sred[t] = v;
@@ -170,7 +194,7 @@ __global__ void __launch_bounds__(NQ *NQ)
         dot = fma(ru[k], v, dot);
     }
     if (part) {
-        double s = block_sum(dot, sred);
+        double s = block_sum_any(dot, sred);
         if (t == 0) part[pos] = s;
     }
 }
@@ -199,9 +223,10 @@ cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst
 __device__ __forceinline__ void last_block_finish(double *part, int64_t count, double *dst, unsigned int *counter,
                                                   double *sred, int *s_last)
 {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) *s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        *s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (*s_last) {
         __threadfence();
@@ -909,8 +934,8 @@ struct AxV5Smem {
     int last;
 };
 
-template <bool HELM, bool FUSED>
-__global__ void __launch_bounds__(128, 3)
+template <bool HELM, bool FUSED, int MINB>
+__global__ void __launch_bounds__(128, MINB)
     ax_v5_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *u,
                  const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
                  double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
@@ -1092,29 +1117,30 @@ __global__ void __launch_bounds__(128, 3)
     }
 }
 
-template <bool HELM>
+template <bool HELM, int MINB>
 static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
                                 const uint32_t *mbits, double h1, double h2, double *w, int64_t grid, cudaStream_t s)
 {
     if (L.fused)
-        ax_v5_kernel<HELM, true><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
+        ax_v5_kernel<HELM, true, MINB><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
                                                                  L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                  L.done, L.p, L.x, L.r, L.dinv, L.sc);
     else
-        ax_v5_kernel<HELM, false><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
+        ax_v5_kernel<HELM, false, MINB><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
                                                                   L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                   L.done, nullptr, nullptr, nullptr, nullptr, nullptr);
     return cudaGetLastError();
 }
 
-bool ax_has_fused(int variant, int N) { return variant == 0 && N == 7; }
+bool ax_has_fused(int variant, int N) { return (variant == 0 || variant == 8) && N == 7; }
 
-// variant (N = 7): 0 = default (v5, DMMA, k-slabs), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
+// variant (N = 7): 0 = default (v5, DMMA, k-slabs, 4 CTAs/SM), 8 = v5 at 3 CTAs/SM, 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
 // 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups, 6 = v3 with 1 k-group, 7 = v4 (DMMA, j-slabs)
 static int per_sm_of(int variant)
 {
     switch (variant) {
-    case 0: return 3;
+    case 0: return 4;
+    case 8: return 3;
     case 7: return 3;
     case 6: return 6;
     case 2: return 3;
@@ -1183,11 +1209,14 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         return h2 != 0.0 ? ax_v2_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                          : ax_v2_launch<false, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
     }
-    if (N == 7 && variant == 0) {
+    if (N == 7 && (variant == 0 || variant == 8)) {
         if (nlaunch) ++*nlaunch;
         const int64_t grid = ax_grid(variant, N, L.nelem);
-        return h2 != 0.0 ? ax_v5_launch<true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
-                         : ax_v5_launch<false>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+        if (variant == 0)
+            return h2 != 0.0 ? ax_v5_launch<true, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                             : ax_v5_launch<false, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+        return h2 != 0.0 ? ax_v5_launch<true, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                         : ax_v5_launch<false, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
     }
     if (N == 7 && variant == 7) {
         if (nlaunch) ++*nlaunch;
@@ -1250,7 +1279,7 @@ cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *o
 // ascending: the sum order of every run is unchanged (bit-exact with the
 // oracle) but fixed-length runs need no offsets and load their indices as one
 // vector (one dependent load level fewer).
-constexpr int GS_PAIRS_PER_THREAD = 4, GS_QUADS_PER_THREAD = 2;
+constexpr int GS_PAIRS_PER_THREAD = 8, GS_QUADS_PER_THREAD = 4;
 
 // Each warp takes a contiguous block of runs of one class and lane l handles
 // runs l, l+32, ... of it, so every warp-wide load touches consecutive runs
@@ -1466,9 +1495,10 @@ __device__ __forceinline__ double rank_sum(const double *red_all, int nranks, in
 __device__ __forceinline__ void last_block_finish2(double *part, int nblk, double *dst, unsigned int *counter,
                                                    double *sred, int *s_last)
 {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) *s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        *s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (*s_last) {
         __threadfence();
@@ -1645,9 +1675,11 @@ __global__ void __launch_bounds__(VEC_THREADS, 4)
         }
         if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) p[n - 1] = fma(beta, p[n - 1], dinv[n - 1] * r[n - 1]);
     }
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (last && threadIdx.x == 0) {
         *counter = 0u;
@@ -1689,7 +1721,7 @@ __device__ __forceinline__ void pcg_bookkeep(PcgScalars *sc, double rho1, double
     __threadfence();
 }
 
-__global__ void __launch_bounds__(VEC_THREADS, 4)
+__global__ void __launch_bounds__(VEC_THREADS, 2)
     pcg_update_fused_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                             const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ red_all,
                             int nranks, PcgScalars *sc, double *hist, double *__restrict__ part, double *dst,
@@ -1740,9 +1772,10 @@ __global__ void __launch_bounds__(VEC_THREADS, 4)
     a0 = block_sum(a0, sred);
     a1 = block_sum(a1, sred);
     if (threadIdx.x == 0) { part[2 * blockIdx.x] = a0; part[2 * blockIdx.x + 1] = a1; }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (s_last) {
         __threadfence();
