@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -145,6 +146,16 @@ static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w,
 
 static int halo_start(nek_ctx *ctx, const double *v, const int *done)
 {
+    if (ctx->p2p) {   // interface partials written straight into the neighbours' buffers over NVLink
+        Scope sc(ctx, CLS_HALO);
+        CK(launch_gs_pack_p2p(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots,
+                              ctx->send_run, ctx->d_slot_nbr, ctx->d_peer_recv, ctx->d_remote_off, ctx->d_send_offs,
+                              ctx->nslots, (int)ctx->neighbors.size(), ctx->rank, ctx->d_peer_hflags, ctx->epochs,
+                              ctx->counter + 3, done, ctx->s_main));
+        ctx->stats.launches += 1 + (ctx->nifc > 0);
+        ctx->stats.halo_launches += 1;
+        return NEK_OK;
+    }
     {
         Scope sc(ctx, CLS_HALO);
         CK(launch_gs_ifc_pack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots,
@@ -167,6 +178,15 @@ static int halo_start(nek_ctx *ctx, const double *v, const int *done)
 
 static int halo_finish(nek_ctx *ctx, double *v, const int *done)
 {
+    if (ctx->p2p) {
+        Scope sc(ctx, CLS_HALO);
+        CK(launch_gs_wait_p2p((int)ctx->neighbors.size(), ctx->d_nbr, ctx->hflags, ctx->epochs, ctx->p2p_err,
+                              ctx->s_main));
+        CK(launch_gs_ifc_unpack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, ctx->coffs, ctx->contrib, ctx->ifc_partial,
+                                ctx->recv2, v, done, ctx->s_main, ctx->epochs + 3, ctx->nslots));
+        ctx->stats.launches += 1 + (ctx->nifc > 0);
+        return NEK_OK;
+    }
     CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_join, 0));
     Scope sc(ctx, CLS_HALO);
     CK(launch_gs_ifc_unpack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, ctx->coffs, ctx->contrib, ctx->ifc_partial,
@@ -230,10 +250,18 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     return halo_finish(ctx, w, done);
 }
 
-// share this rank's reduction slots with every rank (rank-ordered; red_all == red_loc at one rank)
-static int exchange_slots(nek_ctx *ctx)
+// share this rank's reduction slots with every rank (rank-ordered; red_all == red_loc at one rank).
+// channel: 0 = after Ax (sigma), 1 = after the residual update (rho', rr)
+static int exchange_slots(nek_ctx *ctx, int channel)
 {
-    if (ctx->nranks > 1) NK(ncclAllGather(ctx->red_loc, ctx->red_all, RED_N, ncclDouble, ctx->nccl, ctx->s_main));
+    if (ctx->nranks == 1) return NEK_OK;
+    if (ctx->p2p) {
+        CK(launch_red_exchange(channel, ctx->rank, ctx->nranks, ctx->red_loc, ctx->red_all, ctx->mbox,
+                               ctx->d_peer_mbox, ctx->epochs, ctx->p2p_err, ctx->s_main));
+        ctx->stats.launches += 1;
+        return NEK_OK;
+    }
+    NK(ncclAllGather(ctx->red_loc, ctx->red_all, RED_N, ncclDouble, ctx->nccl, ctx->s_main));
     return NEK_OK;
 }
 
@@ -268,6 +296,103 @@ static int ensure_dinv(nek_ctx *ctx, double h1, double h2)
         cudaGraphExecDestroy(ctx->graph);
         ctx->graph = nullptr;
     }
+    return NEK_OK;
+}
+
+
+// Exchange CUDA IPC handles of the mailbox, the halo receive buffer and the halo
+// flags (one NCCL allgather), plus where each rank's data lands in each
+// neighbour's receive buffer, then open the peers' allocations.  Any failure
+// leaves ctx->p2p false (the NCCL path stays in use).
+static int setup_p2p(nek_ctx *ctx)
+{
+    const int P = ctx->nranks, me = ctx->rank;
+    const int nn = (int)ctx->neighbors.size();
+    CK(dalloc(ctx, &ctx->mbox, (int64_t)2 * 2 * P * 4));
+    CK(cudaMemset(ctx->mbox, 0, sizeof(double) * 2 * 2 * P * 4));
+    CK(dalloc(ctx, &ctx->hflags, P));
+    CK(cudaMemset(ctx->hflags, 0, sizeof(uint64_t) * P));
+    CK(dalloc(ctx, &ctx->recv2, 2 * std::max<int64_t>(ctx->nslots, 1)));
+    CK(dalloc(ctx, &ctx->epochs, 4));
+    CK(cudaMemset(ctx->epochs, 0, sizeof(uint64_t) * 4));
+    CK(dalloc(ctx, &ctx->p2p_err, 1));
+    CK(cudaMemset(ctx->p2p_err, 0, sizeof(int)));
+    // per-rank record: 3 IPC handles + offsets of my data in every rank's receive buffer (-1: not a neighbour)
+    struct Rec { cudaIpcMemHandle_t hm, hr, hf; int64_t off[1]; };
+    const size_t rec_bytes = sizeof(cudaIpcMemHandle_t) * 3 + sizeof(int64_t) * P;
+    std::vector<unsigned char> mine(rec_bytes, 0), all(rec_bytes * P, 0);
+    cudaIpcMemHandle_t h[3];
+    if (cudaIpcGetMemHandle(&h[0], ctx->mbox) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->recv2) != cudaSuccess ||
+        cudaIpcGetMemHandle(&h[2], ctx->hflags) != cudaSuccess) {
+        cudaGetLastError();
+        return NEK_OK;   // no IPC: stay on NCCL
+    }
+    std::memcpy(mine.data(), h, sizeof(h));
+    std::vector<int64_t> offs(P, -1);   // where neighbour q's data lands in MY receive buffer
+    for (int k = 0; k < nn; ++k) offs[ctx->neighbors[k]] = ctx->send_offs[k];
+    std::memcpy(mine.data() + sizeof(h), offs.data(), sizeof(int64_t) * P);
+    unsigned char *dbuf = nullptr;
+    CK(cudaMalloc(&dbuf, rec_bytes * (P + 1)));
+    CK(cudaMemcpy(dbuf + rec_bytes * P, mine.data(), rec_bytes, cudaMemcpyHostToDevice));
+    NK(ncclAllGather(dbuf + rec_bytes * P, dbuf, rec_bytes, ncclUint8, ctx->nccl, ctx->s_main));
+    CK(cudaStreamSynchronize(ctx->s_main));
+    CK(cudaMemcpy(all.data(), dbuf, rec_bytes * P, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    std::vector<double *> pm(P, nullptr), pr(P, nullptr);
+    std::vector<uint64_t *> pf(P, nullptr);
+    bool ok = true;
+    for (int q = 0; q < P && ok; ++q) {
+        if (q == me) { pm[q] = ctx->mbox; continue; }
+        cudaIpcMemHandle_t hq[3];
+        std::memcpy(hq, all.data() + rec_bytes * q, sizeof(hq));
+        void *p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, hq[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
+        ctx->ipc_opened.push_back(p); pm[q] = (double *)p;
+        bool nbr = std::find(ctx->neighbors.begin(), ctx->neighbors.end(), q) != ctx->neighbors.end();
+        if (!nbr) continue;
+        if (cudaIpcOpenMemHandle(&p, hq[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
+        ctx->ipc_opened.push_back(p); pr[q] = (double *)p;
+        if (cudaIpcOpenMemHandle(&p, hq[2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
+        ctx->ipc_opened.push_back(p); pf[q] = (uint64_t *)p;
+    }
+    // every rank must agree on the transport
+    int okv = ok ? 1 : 0;
+    int *dok = nullptr;
+    CK(cudaMalloc(&dok, sizeof(int)));
+    CK(cudaMemcpy(dok, &okv, sizeof(int), cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, ctx->nccl, ctx->s_main));
+    CK(cudaStreamSynchronize(ctx->s_main));
+    CK(cudaMemcpy(&okv, dok, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(dok);
+    if (!okv) {
+        cudaGetLastError();
+        for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+        ctx->ipc_opened.clear();
+        return NEK_OK;
+    }
+    // device-side tables
+    std::vector<double *> nrecv(nn);
+    std::vector<uint64_t *> nflag(nn);
+    std::vector<int64_t> roff(nn);
+    for (int k = 0; k < nn; ++k) {
+        const int q = ctx->neighbors[k];
+        nrecv[k] = pr[q];
+        nflag[k] = pf[q];
+        int64_t o;
+        std::memcpy(&o, all.data() + rec_bytes * q + sizeof(h) + sizeof(int64_t) * me, sizeof(int64_t));
+        roff[k] = o;
+    }
+    std::vector<int32_t> slot_nbr(ctx->nslots), nbr32(ctx->neighbors.begin(), ctx->neighbors.end());
+    for (int k = 0; k < nn; ++k)
+        for (int64_t s = ctx->send_offs[k]; s < ctx->send_offs[k + 1]; ++s) slot_nbr[s] = k;
+    CK(upload(ctx, &ctx->d_peer_mbox, pm));
+    CK(upload(ctx, &ctx->d_peer_recv, nrecv));
+    CK(upload(ctx, &ctx->d_peer_hflags, nflag));
+    CK(upload(ctx, &ctx->d_remote_off, roff));
+    CK(upload(ctx, &ctx->d_send_offs, ctx->send_offs));
+    CK(upload(ctx, &ctx->d_slot_nbr, slot_nbr));
+    CK(upload(ctx, &ctx->d_nbr, nbr32));
+    ctx->p2p = true;
     return NEK_OK;
 }
 
@@ -397,6 +522,15 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     ctx->n_masked = 0;
     for (auto m : p->mask) ctx->n_masked += m;
 
+    // NVLink peer-memory path: map the peers' mailbox / halo buffers (CUDA IPC)
+    if (ctx->nranks > 1) {
+        const char *env = getenv("NEK_P2P");
+        if (!env || std::strcmp(env, "0") != 0) {
+            st = setup_p2p(ctx);
+            if (st != NEK_OK) return st;
+        }
+    }
+
     // geometry
     const int64_t n = ctx->n;
     CK(dalloc(ctx, &ctx->G, 6 * n));
@@ -476,6 +610,11 @@ int nek_free(nek_ctx *ctx)
                     (void *)ctx->gs_p8, (void *)ctx->gs_pg, (void *)ctx->gs_og})
         if (p) cudaFree(p);
     if (ctx->red_all && ctx->red_all != ctx->red_loc) cudaFree(ctx->red_all);
+    for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+    for (void *p : {(void *)ctx->mbox, (void *)ctx->d_peer_mbox, (void *)ctx->epochs, (void *)ctx->p2p_err,
+                    (void *)ctx->recv2, (void *)ctx->d_peer_recv, (void *)ctx->d_remote_off, (void *)ctx->d_send_offs,
+                    (void *)ctx->d_slot_nbr, (void *)ctx->d_nbr, (void *)ctx->hflags, (void *)ctx->d_peer_hflags})
+        if (p) cudaFree(p);
     if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
     TimerPool &P = pool_of(ctx);
     for (auto &t : P.pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -546,7 +685,7 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
     if (use_fused(ctx)) {
         // Ax prologue: p = Dinv r + beta p, x += alpha p (deferred); then w = A p, sigma
         if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
-        if ((st = exchange_slots(ctx)) != NEK_OK) return st;
+        if ((st = exchange_slots(ctx, 0)) != NEK_OK) return st;
         {
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
@@ -555,14 +694,14 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
         if (ctx->nranks > 1) {
-            if ((st = exchange_slots(ctx)) != NEK_OK) return st;
+            if ((st = exchange_slots(ctx, 1)) != NEK_OK) return st;
             CK(launch_pcg_iter_fin(ctx->sc, ctx->red_all, ctx->nranks, ctx->hist, ctx->s_main));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
         return NEK_OK;
     }
     if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done)) != NEK_OK) return st;
-    if ((st = exchange_slots(ctx)) != NEK_OK) return st;
+    if ((st = exchange_slots(ctx, 0)) != NEK_OK) return st;
     {
         Scope sc(ctx, CLS_VEC);
         CK(launch_pcg_update(ctx->n, ctx->obits, ctx->vdinv, ctx->vp, ctx->vw, ctx->vx, ctx->vr, ctx->red_all,
@@ -570,7 +709,7 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
                              ctx->s_main));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
-    if ((st = exchange_slots(ctx)) != NEK_OK) return st;
+    if ((st = exchange_slots(ctx, 1)) != NEK_OK) return st;
     {
         Scope sc(ctx, CLS_VEC);
         CK(launch_pcg_pupdate(ctx->n, ctx->vdinv, ctx->vr, ctx->vp, ctx->red_all, ctx->nranks, ctx->sc, ctx->hist,
@@ -614,7 +753,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
                            ctx->red_loc + RED_RHO, ctx->counter + 2, use_fused(ctx), ctx->s_main));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
-    if ((st = exchange_slots(ctx)) != NEK_OK) return st;
+    if ((st = exchange_slots(ctx, 1)) != NEK_OK) return st;
     CK(launch_pcg_init_fin(ctx->sc, ctx->red_all, ctx->nranks, ctx->hist, ctx->s_main));
     ctx->stats.launches += 1;
 
@@ -677,6 +816,11 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     if (hist && H->iter >= 0)
         CK(cudaMemcpy(hist, ctx->hist, sizeof(double) * (H->iter + 1), cudaMemcpyDeviceToHost));
     if (ctx->timing) harvest_timers(ctx);
+    if (ctx->p2p) {
+        int perr = 0;
+        CK(cudaMemcpy(&perr, ctx->p2p_err, sizeof(int), cudaMemcpyDeviceToHost));
+        if (perr) return fail(ctx, NEK_ENCCL, "peer exchange timed out (a rank stopped participating)");
+    }
     if (iters) *iters = H->iter;
     if (relres) *relres = H->bb > 0 ? std::sqrt(H->rr) / H->bb : 0.0;
     leave(ctx, stream);

@@ -1392,9 +1392,10 @@ cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t 
 __global__ void gs_unpack_kernel(int64_t nifc, const int32_t *__restrict__ perm, const int32_t *__restrict__ offs,
                                  const int32_t *__restrict__ coffs, const int32_t *__restrict__ contrib,
                                  const double *__restrict__ partial, const double *__restrict__ recvbuf,
-                                 double *__restrict__ v, const int *done)
+                                 double *__restrict__ v, const int *done, const uint64_t *epoch, int64_t half)
 {
     if (done && *(volatile const int *)done) return;
+    if (epoch) recvbuf += (int64_t)(*epoch & 1) * half;   // P2P: double-buffered by epoch parity
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= nifc) return;
     const int c0 = coffs[r], c1 = coffs[r + 1];
@@ -1409,11 +1410,11 @@ __global__ void gs_unpack_kernel(int64_t nifc, const int32_t *__restrict__ perm,
 
 cudaError_t launch_gs_ifc_unpack(int64_t nifc, const int32_t *perm, const int32_t *offs, const int32_t *coffs,
                                  const int32_t *contrib, const double *partial, const double *recvbuf, double *v,
-                                 const int *done, cudaStream_t s)
+                                 const int *done, cudaStream_t s, const uint64_t *epoch, int64_t half)
 {
     if (nifc <= 0) return cudaSuccess;
     gs_unpack_kernel<<<(unsigned)((nifc + 255) / 256), 256, 0, s>>>(nifc, perm, offs, coffs, contrib, partial,
-                                                                    recvbuf, v, done);
+                                                                    recvbuf, v, done, epoch, half);
     return cudaGetLastError();
 }
 
@@ -1830,6 +1831,133 @@ cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, 
 {
     if (n == 0) return cudaSuccess;
     pcg_xfinal_kernel<<<vec_blocks(), VEC_THREADS, 0, s>>>(n, sc, p, x);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------ NVLink peer-memory exchange
+// One process per GPU; every rank maps its peers' mailbox / halo buffers
+// (CUDA IPC) and writes into them directly over NVLink.  A value block is
+// followed by a system-scope release store of a monotonically increasing
+// epoch; the reader acquires the epoch and then reads.  All ranks run the same
+// sequence of exchanges, so epochs agree.  Spins give up after ~2^26 polls and
+// raise *err (no hang if a peer died).
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p)
+{
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ bool wait_epoch(const uint64_t *flag, uint64_t e, int *err)
+{
+    for (long it = 0; it < (1l << 26); ++it) {
+        if (ld_acquire_sys(flag) >= e) return true;
+        if (it > 64) __nanosleep(32);
+    }
+    atomicExch(err, 1);
+    return false;
+}
+
+// mailbox layout: [channel][epoch parity][rank][4] doubles; slot 3 holds the epoch
+// (as u64).  The parity split means a slot is rewritten only two exchanges later,
+// by which time its reader has provably consumed it.
+__global__ void red_exchange_kernel(int channel, int me, int nranks, const double *__restrict__ red_loc,
+                                    double *__restrict__ red_all, double *mbox, double *const *peer_mbox,
+                                    uint64_t *epochs, int *err)
+{
+    __shared__ uint64_t s_e;
+    const int q = threadIdx.x;
+    if (q == 0) s_e = ++epochs[channel];
+    __syncthreads();
+    const uint64_t e = s_e;
+    const size_t base = ((size_t)channel * 2 + (e & 1)) * nranks;
+    if (q < nranks) {
+        double *dst = (q == me ? mbox : peer_mbox[q]) + (base + me) * 4;
+        dst[0] = red_loc[0]; dst[1] = red_loc[1]; dst[2] = red_loc[2];
+        __threadfence_system();
+        st_release_sys(reinterpret_cast<uint64_t *>(dst + 3), e);
+    }
+    if (q < nranks) {
+        const double *src = mbox + (base + q) * 4;
+        if (wait_epoch(reinterpret_cast<const uint64_t *>(src + 3), e, err)) {
+            red_all[q * RED_N + 0] = ((volatile const double *)src)[0];
+            red_all[q * RED_N + 1] = ((volatile const double *)src)[1];
+            red_all[q * RED_N + 2] = ((volatile const double *)src)[2];
+        }
+    }
+}
+
+cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *red_loc, double *red_all, double *mbox,
+                                double *const *peer_mbox, uint64_t *epochs, int *err, cudaStream_t s)
+{
+    red_exchange_kernel<<<1, 32, 0, s>>>(channel, me, nranks, red_loc, red_all, mbox, peer_mbox, epochs, err);
+    return cudaGetLastError();
+}
+
+// halo: interface partials straight into the neighbours' receive buffers
+// (double-buffered by epoch parity), then one flag per neighbour set by the
+// last CTA to finish.
+__global__ void gs_pack_p2p_kernel(int64_t nslots, const int32_t *__restrict__ send_run,
+                                   const int32_t *__restrict__ slot_nbr, const double *__restrict__ partial,
+                                   double *const *peer_recv, const int64_t *__restrict__ remote_off,
+                                   const int64_t *__restrict__ send_offs, int64_t recv_half, int nnbr, int me,
+                                   uint64_t *const *peer_hflags, uint64_t *epochs, unsigned int *counter,
+                                   const int *done)
+{
+    __shared__ int s_last;
+    const uint64_t e = epochs[2] + 1;           // this exchange's epoch (bumped by the last CTA)
+    const int64_t half = (int64_t)(e & 1) * recv_half;
+    if (!(done && *(volatile const int *)done)) {
+        for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < nslots;
+             sidx += (int64_t)gridDim.x * blockDim.x) {
+            const int k = slot_nbr[sidx];
+            peer_recv[k][half + remote_off[k] + (sidx - send_offs[k])] = partial[send_run[sidx]];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        *counter = 0u;
+        epochs[2] = e;
+        __threadfence_system();
+        for (int k = 0; k < nnbr; ++k) st_release_sys(peer_hflags[k] + me, e);
+    }
+}
+
+cudaError_t launch_gs_pack_p2p(int64_t nifc, const int32_t *perm, const int32_t *offs, const double *v,
+                               double *partial, int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
+                               double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
+                               int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags, uint64_t *epochs,
+                               unsigned int *counter, const int *done, cudaStream_t s)
+{
+    if (nifc > 0) gs_ifc_partial_kernel<<<(unsigned)((nifc + 255) / 256), 256, 0, s>>>(nifc, perm, offs, v, partial, done);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + 255) / 256, 148));
+    gs_pack_p2p_kernel<<<blocks, 256, 0, s>>>(nslots, send_run, slot_nbr, partial, peer_recv, remote_off, send_offs,
+                                              recv_half, nnbr, me, peer_hflags, epochs, counter, done);
+    return cudaGetLastError();
+}
+
+// wait until every neighbour's halo of this epoch has landed
+__global__ void gs_wait_p2p_kernel(int nnbr, const int32_t *__restrict__ nbr, const uint64_t *hflags, uint64_t *epochs,
+                                   int *err)
+{
+    __shared__ uint64_t s_e;
+    if (threadIdx.x == 0) s_e = ++epochs[3];
+    __syncthreads();
+    for (int k = threadIdx.x; k < nnbr; k += blockDim.x) wait_epoch(hflags + nbr[k], s_e, err);
+}
+
+cudaError_t launch_gs_wait_p2p(int nnbr, const int32_t *nbr, const uint64_t *hflags, uint64_t *epochs, int *err,
+                               cudaStream_t s)
+{
+    gs_wait_p2p_kernel<<<1, 32, 0, s>>>(nnbr, nbr, hflags, epochs, err);
     return cudaGetLastError();
 }
 

@@ -81,7 +81,8 @@ cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t 
                                const int *done, cudaStream_t s);
 cudaError_t launch_gs_ifc_unpack(int64_t nifc, const int32_t *perm, const int32_t *offs, const int32_t *coffs,
                                  const int32_t *contrib, const double *partial, const double *recvbuf, double *v,
-                                 const int *done, cudaStream_t s);
+                                 const int *done, cudaStream_t s, const uint64_t *epoch = nullptr,
+                                 int64_t half = 0);
 cudaError_t launch_diag(int N, int64_t E, const double *G, const double *wJ, double h1, double h2, double *d,
                         cudaStream_t s);
 cudaError_t launch_dinv(int64_t n, const uint32_t *mbits, const double *d, double *dinv, cudaStream_t s);
@@ -97,6 +98,16 @@ cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const doub
 cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s);
 bool ax_has_fused(int variant, int N);
+// NVLink peer-memory exchange (CUDA IPC mappings; see kernels.cu)
+cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *red_loc, double *red_all, double *mbox,
+                                double *const *peer_mbox, uint64_t *epochs, int *err, cudaStream_t s);
+cudaError_t launch_gs_pack_p2p(int64_t nifc, const int32_t *perm, const int32_t *offs, const double *v,
+                               double *partial, int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
+                               double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
+                               int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags, uint64_t *epochs,
+                               unsigned int *counter, const int *done, cudaStream_t s);
+cudaError_t launch_gs_wait_p2p(int nnbr, const int32_t *nbr, const uint64_t *hflags, uint64_t *epochs, int *err,
+                               cudaStream_t s);
 cudaError_t launch_pcg_init_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_update(int64_t n, const uint32_t *obits, const double *dinv, const double *p,
                               const double *w, double *x, double *r, const double *red_all, int nranks,
@@ -156,6 +167,19 @@ struct nek_ctx {
     int graph_iters = 0;
     double graph_h1 = 0, graph_h2 = 0;
     nek_stats_t graph_stats{};
+    // NVLink peer-memory path (nranks > 1, all peers mapped)
+    bool p2p = false;
+    double *mbox = nullptr;                 // [2 channels][2 parities][nranks][4]
+    double **d_peer_mbox = nullptr;         // [nranks]
+    uint64_t *epochs = nullptr;             // [4]: channel 0, channel 1, halo pack, halo wait
+    int *p2p_err = nullptr;
+    double *recv2 = nullptr;                // 2 x nslots halo receive buffer (P2P)
+    double **d_peer_recv = nullptr;         // [nnbr]
+    int64_t *d_remote_off = nullptr, *d_send_offs = nullptr;
+    int32_t *d_slot_nbr = nullptr, *d_nbr = nullptr;
+    uint64_t *hflags = nullptr;             // [nranks], written by neighbours
+    uint64_t **d_peer_hflags = nullptr;     // [nnbr]
+    std::vector<void *> ipc_opened;
     // stats
     bool timing = false;
     nek_stats_t stats{};
