@@ -34,6 +34,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# keep stdout to the one JSON line (NCCL prints a version banner at some debug levels)
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 METRIC = "FP64 Ax+gs GDOF/s and PCG iter/s at N=7, 1/2/4/8 B200, % of HBM roofline"
 ITERS = 100
@@ -187,7 +189,12 @@ def main():
         if dist:
             dist.barrier()
 
+    def log(msg):
+        if os.environ.get("NEK_BENCH_VERBOSE"):
+            print(f"[rank {rank}] {msg}", file=sys.stderr, flush=True)
+
     mesh = make_mesh(rank, world, args.ez, args.order)
+    log("setup")
     ctx = nek.setup(mesh.E, mesh.N, mesh.xyz, mesh.gid, mesh.mask, comm=comm, device=local)
     info = nek.get_info(ctx)
     if args.variant:
@@ -203,6 +210,7 @@ def main():
     clk = ClockSampler(local)
     clk.start()
     time.sleep(1.0)   # let nvidia-smi start sampling before the timed region
+    log(f"transport {info['transport']}; warm-up")
     # warm-up (also builds the Jacobi diagonal and, with --graph, the CUDA graph)
     for _ in range(args.warmup):
         nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, args.iters)
@@ -226,6 +234,7 @@ def main():
     t_ms = sum(a.elapsed_time(c) for a, c in evs)
     stats = nek.get_stats(ctx, reset=True)
 
+    log("timed PCG done")
     # ---- Ax+gs alone (nek_ax), same flush discipline
     u = torch.from_numpy(mg.smooth_field(mesh, seed=2)).to(dev)
     w = torch.empty_like(u)
@@ -245,6 +254,7 @@ def main():
     barrier()
     axstats = nek.get_stats(ctx, reset=True)
 
+    log("ax done")
     # ---- end to end through the public API with pinned host buffers
     bh = torch.empty(mesh.n_local, dtype=torch.float64, pin_memory=True)
     bh.copy_(b.cpu())
@@ -311,7 +321,8 @@ def main():
             "e2e": {"value": n_dof_total * args.iters / e2e_s / 1e9, "unit": "GDOF/s",
                     "h2d_bytes_per_step": mesh.n_local * 8, "d2h_bytes_per_step": mesh.n_local * 8},
             "roofline": roofline, "clocks": clocks,
-            "halo": {"doubles_per_gs": info["halo_doubles"], "neighbors": info["n_neighbors"]},
+            "halo": {"doubles_per_gs": info["halo_doubles"], "neighbors": info["n_neighbors"],
+                     "transport": {0: "none", 1: "nccl", 2: "nvlink-p2p"}[info["transport"]]},
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(mesh, 50)

@@ -166,6 +166,8 @@ typedef struct {
     int64_t n_boundary_elems;  /* elements holding at least one interface node     */
     int64_t device_bytes;      /* device memory held by the context                */
     double  geom_min_jac;      /* min J over local nodes                           */
+    int32_t transport;         /* 0 = single GPU, 1 = NCCL, 2 = NVLink peer memory (CUDA IPC) */
+    int32_t pad_;
 } nek_info_t;
 
 int nek_get_info(const nek_ctx *ctx, nek_info_t *info);

@@ -837,6 +837,7 @@ int nek_get_info(const nek_ctx *ctx, nek_info_t *info)
     info->n_runs = ctx->nruns; info->n_perm = ctx->nperm; info->n_ifc_runs = ctx->nifc; info->n_ifc_perm = ctx->nifc_perm;
     info->n_neighbors = (int64_t)ctx->neighbors.size(); info->halo_doubles = ctx->nslots;
     info->n_boundary_elems = ctx->n_boundary; info->device_bytes = ctx->device_bytes; info->geom_min_jac = ctx->min_jac;
+    info->transport = ctx->nranks == 1 ? 0 : (ctx->p2p ? 2 : 1);
     return NEK_OK;
 }
 

@@ -934,7 +934,7 @@ struct AxV5Smem {
     int last;
 };
 
-template <bool HELM, bool FUSED, int MINB>
+template <bool HELM, bool FUSED, int MINB, bool L2PF = false>
 __global__ void __launch_bounds__(128, MINB)
     ax_v5_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *u,
                  const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
@@ -968,6 +968,19 @@ __global__ void __launch_bounds__(128, MINB)
         const double *ue = u + e * P3;
         const double *Ge = G + e * 6 * (int64_t)P3;
         const int par = (int)(it & 1);
+        if (L2PF && t == 0 && it + 1 < nit) {    // next element's streams into L2 while this one computes
+            const int64_t pn = eoff + blockIdx.x + (it + 1) * (int64_t)gridDim.x;
+            const int64_t en = elist ? (int64_t)elist[pn] : pn;
+            tma::prefetch_l2(G + en * 6 * (int64_t)P3, 6 * P3 * 8);
+            if (FUSED) {
+                tma::prefetch_l2(pvec + en * P3, P3 * 8);
+                tma::prefetch_l2(rvec + en * P3, P3 * 8);
+                tma::prefetch_l2(dvec + en * P3, P3 * 8);
+                tma::prefetch_l2(xvec + en * P3, P3 * 8);
+            } else {
+                tma::prefetch_l2(u + en * P3, P3 * 8);
+            }
+        }
         uint32_t mword = 0u;
         if (mbits && lane < 16) mword = __ldg(mbits + e * 16 + lane);
         double2 uc[8];                           // own k-line
@@ -1117,30 +1130,32 @@ __global__ void __launch_bounds__(128, MINB)
     }
 }
 
-template <bool HELM, int MINB>
+template <bool HELM, int MINB, bool L2PF = false>
 static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
                                 const uint32_t *mbits, double h1, double h2, double *w, int64_t grid, cudaStream_t s)
 {
     if (L.fused)
-        ax_v5_kernel<HELM, true, MINB><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
+        ax_v5_kernel<HELM, true, MINB, L2PF><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
                                                                  L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                  L.done, L.p, L.x, L.r, L.dinv, L.sc);
     else
-        ax_v5_kernel<HELM, false, MINB><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
+        ax_v5_kernel<HELM, false, MINB, L2PF><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
                                                                   L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                   L.done, nullptr, nullptr, nullptr, nullptr, nullptr);
     return cudaGetLastError();
 }
 
-bool ax_has_fused(int variant, int N) { return (variant == 0 || variant == 8) && N == 7; }
+bool ax_has_fused(int variant, int N) { return (variant == 0 || variant == 8 || variant == 9) && N == 7; }
 
-// variant (N = 7): 0 = default (v5, DMMA, k-slabs, 4 CTAs/SM), 8 = v5 at 3 CTAs/SM, 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
+// variant (N = 7): 0 = default (v5, DMMA, k-slabs, 4 CTAs/SM), 8 = v5 at 3 CTAs/SM,
+// 9 = v5 + L2 bulk prefetch of the next element, 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
 // 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups, 6 = v3 with 1 k-group, 7 = v4 (DMMA, j-slabs)
 static int per_sm_of(int variant)
 {
     switch (variant) {
     case 0: return 4;
     case 8: return 3;
+    case 9: return 4;
     case 7: return 3;
     case 6: return 6;
     case 2: return 3;
@@ -1209,9 +1224,12 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         return h2 != 0.0 ? ax_v2_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                          : ax_v2_launch<false, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
     }
-    if (N == 7 && (variant == 0 || variant == 8)) {
+    if (N == 7 && (variant == 0 || variant == 8 || variant == 9)) {
         if (nlaunch) ++*nlaunch;
         const int64_t grid = ax_grid(variant, N, L.nelem);
+        if (variant == 9)
+            return h2 != 0.0 ? ax_v5_launch<true, 4, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                             : ax_v5_launch<false, 4, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
         if (variant == 0)
             return h2 != 0.0 ? ax_v5_launch<true, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
@@ -1853,9 +1871,9 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p)
 }
 __device__ __forceinline__ bool wait_epoch(const uint64_t *flag, uint64_t e, int *err)
 {
-    for (long it = 0; it < (1l << 26); ++it) {
+    for (long it = 0; it < (1l << 22); ++it) {   // ~0.5 s
         if (ld_acquire_sys(flag) >= e) return true;
-        if (it > 64) __nanosleep(32);
+        if (it > 64) __nanosleep(64);
     }
     atomicExch(err, 1);
     return false;

@@ -51,7 +51,7 @@ class nek_info_t(ctypes.Structure):
                 ("n_runs", ctypes.c_int64), ("n_perm", ctypes.c_int64), ("n_ifc_runs", ctypes.c_int64),
                 ("n_ifc_perm", ctypes.c_int64), ("n_neighbors", ctypes.c_int64), ("halo_doubles", ctypes.c_int64),
                 ("n_boundary_elems", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
-                ("geom_min_jac", ctypes.c_double)]
+                ("geom_min_jac", ctypes.c_double), ("transport", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class nek_stats_t(ctypes.Structure):

@@ -94,7 +94,8 @@ def main():
             results[name] = {"ax_err": ax_err, "gs_bitexact_vs_multirank_oracle": gs_bit, "gs_err_vs_1rank": gs_err,
                              "hist_ok": hist_ok, "x_err": x_err, "copies_identical": bool(same), "iters": ito,
                              "halo_doubles": [pl["info"]["halo_doubles"] for pl in gathered],
-                             "neighbors": [pl["info"]["n_neighbors"] for pl in gathered], "ok": case_ok}
+                             "neighbors": [pl["info"]["n_neighbors"] for pl in gathered],
+                             "transport": [pl["info"]["transport"] for pl in gathered], "ok": case_ok}
         nek.free(ctx)
     if rank == 0:
         print(json.dumps({"world": world, "ok": bool(ok), "cases": results}))
