@@ -144,15 +144,23 @@ static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w,
     return NEK_OK;
 }
 
+static P2PMail mail_of(const nek_ctx *ctx)
+{
+    P2PMail m;
+    m.mbox = ctx->mbox; m.peer_mbox = ctx->d_peer_mbox; m.epochs = ctx->epochs; m.err = ctx->p2p_err;
+    m.me = ctx->rank; m.nranks = ctx->nranks;
+    return m;
+}
+
 static int halo_start(nek_ctx *ctx, const double *v, const int *done)
 {
     if (ctx->p2p) {   // interface partials written straight into the neighbours' buffers over NVLink
         Scope sc(ctx, CLS_HALO);
-        CK(launch_gs_pack_p2p(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots,
-                              ctx->send_run, ctx->d_slot_nbr, ctx->d_peer_recv, ctx->d_remote_off, ctx->d_send_offs,
-                              ctx->nslots, (int)ctx->neighbors.size(), ctx->rank, ctx->d_peer_hflags, ctx->epochs,
-                              ctx->counter + 3, done, ctx->s_main));
-        ctx->stats.launches += 1 + (ctx->nifc > 0);
+        CK(launch_gs_pack_p2p_fused(ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots, ctx->send_run,
+                                    ctx->d_slot_nbr, ctx->d_peer_recv, ctx->d_remote_off, ctx->d_send_offs,
+                                    ctx->nslots, (int)ctx->neighbors.size(), ctx->rank, ctx->d_peer_hflags,
+                                    ctx->epochs, ctx->counter + 3, done, ctx->s_main));
+        ctx->stats.launches += 1;
         ctx->stats.halo_launches += 1;
         return NEK_OK;
     }
@@ -204,11 +212,27 @@ static int do_gs_local(nek_ctx *ctx, double *v, const int *done)
     return NEK_OK;
 }
 
+// P2P: the local runs and the halo unpack (which waits for the neighbours' data) in one launch
+static int gs_local_and_unpack_p2p(nek_ctx *ctx, double *v, const int *done)
+{
+    Scope sc(ctx, CLS_GS);
+    HaloUnpack U;
+    U.nifc = ctx->nifc; U.perm = ctx->ifc_perm; U.offs = ctx->ifc_offs; U.coffs = ctx->coffs;
+    U.contrib = ctx->contrib; U.nbr = ctx->d_nbr; U.partial = ctx->ifc_partial; U.recv = ctx->recv2;
+    U.half = ctx->nslots; U.hflags = ctx->hflags; U.epochs = ctx->epochs; U.nnbr = (int)ctx->neighbors.size();
+    U.err = ctx->p2p_err;
+    CK(launch_gs_classes_unpack(ctx->gsc, U, v, done, ctx->s_main));
+    ctx->stats.gs_launches += 1;
+    ctx->stats.launches += 1;
+    return NEK_OK;
+}
+
 // v <- QQ^T v (global)
 static int gs_full(nek_ctx *ctx, double *v, const int *done)
 {
     int st;
     if (ctx->nranks > 1 && (st = halo_start(ctx, v, done)) != NEK_OK) return st;
+    if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, v, done);
     if ((st = do_gs_local(ctx, v, done)) != NEK_OK) return st;
     if (ctx->nranks > 1 && (st = halo_finish(ctx, v, done)) != NEK_OK) return st;
     return NEK_OK;
@@ -237,15 +261,21 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     }
     const int64_t nb = ctx->n_boundary, ni = ctx->E - ctx->n_boundary;
     const int64_t g1 = ax_grid(ctx->variant, ctx->N, nb), g2 = ax_grid(ctx->variant, ctx->N, ni);
+    const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
     L.elist = ctx->elist;
     L.nelem = nb;
-    if (dot) { L.part = ctx->part; L.part_off = 0; L.fin_total = 0; }
+    if (dot) { L.part = ctx->part; L.part_off = 0; L.fin_total = ni > 0 ? 0 : g1; }
+    if (push && ni == 0) L.mail = mail_of(ctx);
     if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
     if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
-    L.nelem = ni;
-    L.eoff = nb;
-    if (dot) { L.part_off = g1; L.fin_total = g1 + g2; }
-    if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
+    if (ni > 0) {
+        L.nelem = ni;
+        L.eoff = nb;
+        if (dot) { L.part_off = g1; L.fin_total = g1 + g2; }
+        if (push) L.mail = mail_of(ctx);
+        if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
+    }
+    if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, w, done);
     if ((st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
     return halo_finish(ctx, w, done);
 }
@@ -682,6 +712,21 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
     int st;
     const int *done = &ctx->sc->done;
     const int nb = vec_blocks();
+    if (use_fused(ctx) && ctx->p2p) {
+        // sigma pushed by the Ax kernel, pulled by the update kernel; (rho', rr) pushed by the
+        // update kernel, pulled by the bookkeeping kernel: no separate exchange launches
+        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
+        const P2PMail m = mail_of(ctx);
+        {
+            Scope sc(ctx, CLS_VEC);
+            CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
+                                       ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
+                                       ctx->counter + 2, ctx->s_main, &m));
+            CK(launch_pcg_fin_p2p(ctx->sc, m, ctx->hist, ctx->s_main));
+            ctx->stats.launches += 2; ctx->stats.vec_launches += 2;
+        }
+        return NEK_OK;
+    }
     if (use_fused(ctx)) {
         // Ax prologue: p = Dinv r + beta p, x += alpha p (deferred); then w = A p, sigma
         if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;

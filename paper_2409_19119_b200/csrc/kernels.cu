@@ -57,6 +57,60 @@ __device__ __forceinline__ double block_sum(double v, double *sred)
     return r;
 }
 
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p)
+{
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ bool wait_epoch(const uint64_t *flag, uint64_t e, int *err)
+{
+    for (long it = 0; it < (1l << 22); ++it) {   // ~0.5 s
+        if (ld_acquire_sys(flag) >= e) return true;
+        if (it > 64) __nanosleep(64);
+    }
+    atomicExch(err, 1);
+    return false;
+}
+
+// single thread: publish up to 3 values on `channel` to every rank (self included)
+__device__ __forceinline__ void mail_push(const P2PMail &M, int channel, double v0, double v1, double v2)
+{
+    const uint64_t e = ++M.epochs[channel];
+    const size_t base = ((size_t)channel * 2 + (e & 1)) * M.nranks;
+    for (int q = 0; q < M.nranks; ++q) {
+        double *dst = (q == M.me ? M.mbox : M.peer_mbox[q]) + (base + M.me) * 4;
+        dst[0] = v0; dst[1] = v1; dst[2] = v2;
+    }
+    __threadfence_system();
+    for (int q = 0; q < M.nranks; ++q) {
+        double *dst = (q == M.me ? M.mbox : M.peer_mbox[q]) + (base + M.me) * 4;
+        st_release_sys(reinterpret_cast<uint64_t *>(dst + 3), e);
+    }
+}
+
+// single thread: wait for the current epoch of `channel` from every rank and
+// return the rank-ordered sums of the value slots
+__device__ __forceinline__ void mail_pull(const P2PMail &M, int channel, double *sum3)
+{
+    const uint64_t e = *(volatile uint64_t *)&M.epochs[channel];
+    const size_t base = ((size_t)channel * 2 + (e & 1)) * M.nranks;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int q = 0; q < M.nranks; ++q) {
+        const double *src = M.mbox + (base + q) * 4;
+        wait_epoch(reinterpret_cast<const uint64_t *>(src + 3), e, M.err);
+        const double b0 = ((volatile const double *)src)[0], b1 = ((volatile const double *)src)[1],
+                     b2 = ((volatile const double *)src)[2];
+        if (q == 0) { a0 = b0; a1 = b1; a2 = b2; }
+        else { a0 += b0; a1 += b1; a2 += b2; }
+    }
+    sum3[0] = a0; sum3[1] = a1; sum3[2] = a2;
+}
+
 // Fixed-order block sum for any blockDim.x <= 1024 (smem tree); sred needs blockDim.x entries.
 __device__ __forceinline__ double block_sum_any(double v, double *sred)
 {
@@ -221,7 +275,7 @@ cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst
 
 // Last CTA to finish sums part[0..count) (fixed order) into dst[0] and resets the counter.
 __device__ __forceinline__ void last_block_finish(double *part, int64_t count, double *dst, unsigned int *counter,
-                                                  double *sred, int *s_last)
+                                                  double *sred, int *s_last, const P2PMail *mail = nullptr)
 {
     if (threadIdx.x == 0) {
         __threadfence();
@@ -233,7 +287,11 @@ __device__ __forceinline__ void last_block_finish(double *part, int64_t count, d
         double a = 0.0;
         for (int64_t c = threadIdx.x; c < count; c += blockDim.x) a += ((volatile double *)part)[c];
         a = block_sum(a, sred);
-        if (threadIdx.x == 0) { dst[0] = a; *counter = 0u; }
+        if (threadIdx.x == 0) {
+            dst[0] = a;
+            *counter = 0u;
+            if (mail) mail_push(*mail, 0, a, 0.0, 0.0);   // sigma straight to every rank (channel 0)
+        }
     }
 }
 
@@ -941,7 +999,7 @@ __global__ void __launch_bounds__(128, MINB)
                  double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
                  int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done,
                  double *pvec, double *__restrict__ xvec, const double *__restrict__ rvec,
-                 const double *__restrict__ dvec, const PcgScalars *sc)
+                 const double *__restrict__ dvec, const PcgScalars *sc, P2PMail mail)
 {
     constexpr int P3 = 512, N = 7;
     if (done && *(volatile const int *)done) return;
@@ -1126,7 +1184,7 @@ __global__ void __launch_bounds__(128, MINB)
     if (part) {
         const double sum = block_sum(dot, S.sred);
         if (t == 0) part[part_off + blockIdx.x] = sum;
-        if (fin_total > 0) last_block_finish(part, fin_total, dst, counter, S.sred, &S.last);
+        if (fin_total > 0) last_block_finish(part, fin_total, dst, counter, S.sred, &S.last, mail.nranks > 1 ? &mail : nullptr);
     }
 }
 
@@ -1137,11 +1195,12 @@ static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double
     if (L.fused)
         ax_v5_kernel<HELM, true, MINB, L2PF><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
                                                                  L.part, L.part_off, L.fin_total, L.dst, L.counter,
-                                                                 L.done, L.p, L.x, L.r, L.dinv, L.sc);
+                                                                 L.done, L.p, L.x, L.r, L.dinv, L.sc, L.mail);
     else
         ax_v5_kernel<HELM, false, MINB, L2PF><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
                                                                   L.part, L.part_off, L.fin_total, L.dst, L.counter,
-                                                                  L.done, nullptr, nullptr, nullptr, nullptr, nullptr);
+                                                                  L.done, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                                  L.mail);
     return cudaGetLastError();
 }
 
@@ -1302,14 +1361,12 @@ constexpr int GS_PAIRS_PER_THREAD = 8, GS_QUADS_PER_THREAD = 4;
 // Each warp takes a contiguous block of runs of one class and lane l handles
 // runs l, l+32, ... of it, so every warp-wide load touches consecutive runs
 // (first-touch order keeps their copies close in memory).
-__global__ void __launch_bounds__(256)
-    gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
-                      const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
-                      const int32_t *__restrict__ og, double *__restrict__ v, const int *done)
+__device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n2, const int2 *__restrict__ p2,
+                                                int64_t n4, const int4 *__restrict__ p4, int64_t n8,
+                                                const int4 *__restrict__ p8, int64_t ng,
+                                                const int32_t *__restrict__ pg, const int32_t *__restrict__ og,
+                                                double *__restrict__ v)
 {
-    if (done && *(volatile const int *)done) return;
-    int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
     const int64_t w2 = (n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD);
     const int64_t w4 = (n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD);
     const int64_t w8 = (n8 + 31) / 32;
@@ -1365,11 +1422,70 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+__global__ void __launch_bounds__(256)
+    gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
+                      const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
+                      const int32_t *__restrict__ og, double *__restrict__ v, const int *done)
+{
+    if (done && *(volatile const int *)done) return;
+    gs_classes_body((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, n2, p2, n4, p4, n8, p8,
+                    ng, pg, og, v);
+}
+
+static int64_t gs_class_warps(const GsClasses &C)
+{
+    return (C.n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD) +
+           (C.n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD) + (C.n8 + 31) / 32 + (C.ng + 31) / 32;
+}
+
+// local runs (warps [0, cw)) and, after them, the halo unpack (warps [cw, ...)):
+// one lane per interface run waits for this epoch's halo of every neighbour,
+// folds the contributions in rank order and writes the total to the local copies.
+__global__ void __launch_bounds__(256)
+    gs_classes_unpack_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4,
+                             int64_t n8, const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
+                             const int32_t *__restrict__ og, int64_t cw, HaloUnpack U, double *__restrict__ v,
+                             const int *done)
+{
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const bool skip = done && *(volatile const int *)done;
+    if (wid < cw) {
+        if (!skip) gs_classes_body(wid, lane, n2, p2, n4, p4, n8, p8, ng, pg, og, v);
+        return;
+    }
+    const uint64_t e = *(volatile const uint64_t *)(U.epochs + 2);
+    if (lane == 0)
+        for (int k = 0; k < U.nnbr; ++k) wait_epoch(U.hflags + U.nbr[k], e, U.err);
+    __syncwarp();
+    if (skip) return;
+    const int64_t r = (wid - cw) * 32 + lane;
+    if (r >= U.nifc) return;
+    const double *recv = U.recv + (int64_t)(e & 1) * U.half;
+    const int c0 = U.coffs[r], c1 = U.coffs[r + 1];
+    int src = U.contrib[c0];
+    double s = src < 0 ? U.partial[r] : ((volatile const double *)recv)[src];
+    for (int c = c0 + 1; c < c1; ++c) {
+        src = U.contrib[c];
+        s += src < 0 ? U.partial[r] : ((volatile const double *)recv)[src];
+    }
+    for (int c = U.offs[r]; c < U.offs[r + 1]; ++c) v[U.perm[c]] = s;
+}
+
+cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, double *v, const int *done,
+                                     cudaStream_t s)
+{
+    const int64_t cw = gs_class_warps(C), uw = (U.nifc + 31) / 32;
+    const int64_t warps = cw + std::max<int64_t>(uw, 1);   // at least one waiting warp keeps epochs in step
+    gs_classes_unpack_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
+        C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8, (const int4 *)C.p8, C.ng, C.pg, C.og, cw, U, v,
+        done);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gs_classes(const GsClasses &C, double *v, const int *done, cudaStream_t s)
 {
-    const int64_t warps = (C.n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD) +
-                          (C.n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD) + (C.n8 + 31) / 32 +
-                          (C.ng + 31) / 32;
+    const int64_t warps = gs_class_warps(C);
     if (warps <= 0) return cudaSuccess;
     gs_classes_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
         C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8, (const int4 *)C.p8, C.ng, C.pg, C.og, v, done);
@@ -1744,12 +1860,21 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
     pcg_update_fused_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                             const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ red_all,
                             int nranks, PcgScalars *sc, double *hist, double *__restrict__ part, double *dst,
-                            unsigned int *counter)
+                            unsigned int *counter, P2PMail mail)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ int s_last;
+    __shared__ double s_sig[3];
     if (*(volatile int *)&sc->done) return;
-    const double sigma = rank_sum(red_all, nranks, RED_SIGMA);
+    double sigma;
+    if (mail.nranks > 1) {                       // sigma of every rank from the mailbox (channel 0)
+        if (threadIdx.x == 0) mail_pull(mail, 0, s_sig);
+        __syncthreads();
+        sigma = s_sig[0];
+        if (blockIdx.x == 0 && threadIdx.x == 0) sc->sigma = sigma;
+    } else {
+        sigma = rank_sum(red_all, nranks, RED_SIGMA);
+    }
     if (!(sigma > 0.0)) {                       // breakdown: <p, A p> <= 0
         if (blockIdx.x == 0 && threadIdx.x == 0) { sc->status = NEK_ENOTSPD; sc->alpha = 0.0; sc->done = 1; }
         return;
@@ -1808,6 +1933,7 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
         if (threadIdx.x == 0) {
             *counter = 0u;
             if (nranks == 1) pcg_bookkeep(sc, b0, b1, alpha, hist);
+            else if (mail.nranks > 1) mail_push(mail, 1, b0, b1, 0.0);   // to every rank (channel 1)
             else { dst[0] = b0; dst[1] = b1; }
         }
     }
@@ -1815,10 +1941,28 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
 
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
-                                    int nblk, double *dst, unsigned int *counter, cudaStream_t s)
+                                    int nblk, double *dst, unsigned int *counter, cudaStream_t s,
+                                    const P2PMail *mail)
 {
+    P2PMail m;
+    if (mail) m = *mail;
     pcg_update_fused_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist, part, dst,
-                                                         counter);
+                                                         counter, m);
+    return cudaGetLastError();
+}
+
+// P2P: pull <r, Dinv r> and <r, r> of every rank (channel 1) and do the bookkeeping
+__global__ void pcg_fin_p2p_kernel(PcgScalars *sc, P2PMail mail, double *hist)
+{
+    if (sc->done) return;
+    double v[3];
+    mail_pull(mail, 1, v);
+    pcg_bookkeep(sc, v[0], v[1], sc->rho / sc->sigma, hist);
+}
+
+cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s)
+{
+    pcg_fin_p2p_kernel<<<1, 1, 0, s>>>(sc, mail, hist);
     return cudaGetLastError();
 }
 
@@ -1859,26 +2003,6 @@ cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, 
 // epoch; the reader acquires the epoch and then reads.  All ranks run the same
 // sequence of exchanges, so epochs agree.  Spins give up after ~2^26 polls and
 // raise *err (no hang if a peer died).
-__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v)
-{
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p)
-{
-    uint64_t v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ bool wait_epoch(const uint64_t *flag, uint64_t e, int *err)
-{
-    for (long it = 0; it < (1l << 22); ++it) {   // ~0.5 s
-        if (ld_acquire_sys(flag) >= e) return true;
-        if (it > 64) __nanosleep(64);
-    }
-    atomicExch(err, 1);
-    return false;
-}
-
 // mailbox layout: [channel][epoch parity][rank][4] doubles; slot 3 holds the epoch
 // (as u64).  The parity split means a slot is rewritten only two exchanges later,
 // by which time its reader has provably consumed it.
@@ -1947,6 +2071,58 @@ __global__ void gs_pack_p2p_kernel(int64_t nslots, const int32_t *__restrict__ s
         __threadfence_system();
         for (int k = 0; k < nnbr; ++k) st_release_sys(peer_hflags[k] + me, e);
     }
+}
+
+// pack with the interface partials folded in (one thread per send slot; a run
+// shared with several neighbours is folded once per slot, same bits)
+__global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restrict__ perm,
+                                         const int32_t *__restrict__ offs, const double *__restrict__ v,
+                                         double *__restrict__ partial, const int32_t *__restrict__ send_run,
+                                         const int32_t *__restrict__ slot_nbr, double *const *peer_recv,
+                                         const int64_t *__restrict__ remote_off, const int64_t *__restrict__ send_offs,
+                                         int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags,
+                                         uint64_t *epochs, unsigned int *counter, const int *done)
+{
+    __shared__ int s_last;
+    const uint64_t e = epochs[2] + 1;
+    const int64_t half = (int64_t)(e & 1) * recv_half;
+    if (!(done && *(volatile const int *)done)) {
+        for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < nslots;
+             sidx += (int64_t)gridDim.x * blockDim.x) {
+            const int run = send_run[sidx];
+            const int o0 = offs[run], o1 = offs[run + 1];
+            double s = v[perm[o0]];
+            for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
+            partial[run] = s;
+            const int k = slot_nbr[sidx];
+            peer_recv[k][half + remote_off[k] + (sidx - send_offs[k])] = s;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        *counter = 0u;
+        epochs[2] = e;
+        __threadfence_system();
+        for (int k = 0; k < nnbr; ++k) st_release_sys(peer_hflags[k] + me, e);
+    }
+}
+
+cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const double *v, double *partial,
+                                     int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
+                                     double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
+                                     int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags,
+                                     uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s)
+{
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + 255) / 256, 296));
+    gs_pack_p2p_fused_kernel<<<blocks, 256, 0, s>>>(nslots, perm, offs, v, partial, send_run, slot_nbr, peer_recv,
+                                                    remote_off, send_offs, recv_half, nnbr, me, peer_hflags, epochs,
+                                                    counter, done);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_gs_pack_p2p(int64_t nifc, const int32_t *perm, const int32_t *offs, const double *v,

@@ -22,8 +22,18 @@ struct PcgScalars {
     int maxit;
     int done;          // 1 once converged / maxit / breakdown
     int status;        // NEK_OK, NEK_MAXIT, NEK_ENOTSPD
+    double sigma;      // global <p, A p> of the current iteration (P2P path)
     double alpha;      // alpha of the last update whose x += alpha p is still pending (fused path)
     double beta;       // beta for the next direction update (fused path)
+};
+
+// NVLink peer mailbox of a rank: [channel][epoch parity][rank][4] doubles, slot 3 = epoch.
+struct P2PMail {
+    double *mbox = nullptr;               // local mailbox
+    double *const *peer_mbox = nullptr;   // [nranks] (own entry = local)
+    uint64_t *epochs = nullptr;
+    int *err = nullptr;
+    int me = 0, nranks = 1;
 };
 
 // Reduction slots (device): red_loc = this rank's partial sums, red_all = the
@@ -58,6 +68,7 @@ struct AxLaunch {
     // fused PCG prologue (Ax v5 only): p <- Dinv r + beta p, x <- x + alpha p on the
     // element's points before the operator is applied to the new p (u == p then)
     bool fused = false;
+    P2PMail mail;                        // mail.nranks > 1: the finalising CTA pushes sigma to every rank
     double *p = nullptr, *x = nullptr;
     const double *r = nullptr, *dinv = nullptr;
     const PcgScalars *sc = nullptr;
@@ -94,7 +105,22 @@ cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *ob
 // does the iteration bookkeeping, at nranks > 1 pcg_iter_fin does it after the allgather
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
-                                    int nblk, double *dst, unsigned int *counter, cudaStream_t s);
+                                    int nblk, double *dst, unsigned int *counter, cudaStream_t s,
+                                    const P2PMail *mail = nullptr);
+cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
+// local gather-scatter and (P2P) the halo unpack in one launch
+struct HaloUnpack {
+    int64_t nifc = 0;
+    const int32_t *perm = nullptr, *offs = nullptr, *coffs = nullptr, *contrib = nullptr, *nbr = nullptr;
+    double *partial = nullptr;
+    const double *recv = nullptr;
+    int64_t half = 0;
+    const uint64_t *hflags = nullptr, *epochs = nullptr;
+    int nnbr = 0;
+    int *err = nullptr;
+};
+cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, double *v, const int *done,
+                                     cudaStream_t s);
 cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s);
 bool ax_has_fused(int variant, int N);
@@ -106,6 +132,11 @@ cudaError_t launch_gs_pack_p2p(int64_t nifc, const int32_t *perm, const int32_t 
                                double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
                                int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags, uint64_t *epochs,
                                unsigned int *counter, const int *done, cudaStream_t s);
+cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const double *v, double *partial,
+                                     int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
+                                     double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
+                                     int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags,
+                                     uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s);
 cudaError_t launch_gs_wait_p2p(int nnbr, const int32_t *nbr, const uint64_t *hflags, uint64_t *epochs, int *err,
                                cudaStream_t s);
 cudaError_t launch_pcg_init_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
