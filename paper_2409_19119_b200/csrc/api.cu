@@ -262,6 +262,24 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     const int64_t nb = ctx->n_boundary, ni = ctx->E - ctx->n_boundary;
     const int64_t g1 = ax_grid(ctx->variant, ctx->N, nb), g2 = ax_grid(ctx->variant, ctx->N, ni);
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
+    if (ctx->p2p && ax_has_halo_pack(ctx->variant, ctx->N)) {
+        // ONE Ax launch: boundary elements first; the CTA finishing the last boundary element
+        // sends the halo over NVLink while the other CTAs go on with interior elements
+        L.elist = ctx->elist;
+        L.nelem = ctx->E;
+        if (dot) { L.part = ctx->part; L.fin_total = ax_grid(ctx->variant, ctx->N, ctx->E); }
+        if (push) L.mail = mail_of(ctx);
+        HaloPack &H = L.halo;
+        H.nbnd = nb; H.bnd_counter = ctx->counter + 3;
+        H.perm = ctx->ifc_perm; H.offs = ctx->ifc_offs; H.send_run = ctx->send_run; H.slot_nbr = ctx->d_slot_nbr;
+        H.partial = ctx->ifc_partial; H.peer_recv = ctx->d_peer_recv; H.remote_off = ctx->d_remote_off;
+        H.send_offs = ctx->d_send_offs; H.nslots = ctx->nslots; H.half = ctx->nslots;
+        H.nnbr = (int)ctx->neighbors.size(); H.me = ctx->rank; H.peer_hflags = ctx->d_peer_hflags;
+        H.epochs = ctx->epochs;
+        if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
+        ctx->stats.halo_launches += 1;
+        return gs_local_and_unpack_p2p(ctx, w, done);
+    }
     L.elist = ctx->elist;
     L.nelem = nb;
     if (dot) { L.part = ctx->part; L.part_off = 0; L.fin_total = ni > 0 ? 0 : g1; }
