@@ -101,14 +101,14 @@ static cudaEvent_t take_event(nek_ctx *ctx)
 }
 enum { CLS_AX = 0, CLS_GS = 1, CLS_HALO = 2, CLS_VEC = 3 };
 struct Scope {
-    nek_ctx *ctx; int cls; cudaEvent_t a = nullptr;
-    Scope(nek_ctx *c, int k) : ctx(c), cls(k) {
-        if (ctx->timing) { a = take_event(ctx); cudaEventRecord(a, ctx->s_main); }
+    nek_ctx *ctx; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
+    Scope(nek_ctx *c, int k, cudaStream_t st = nullptr) : ctx(c), cls(k), s(st ? st : c->s_main) {
+        if (ctx->timing) { a = take_event(ctx); cudaEventRecord(a, s); }
     }
     ~Scope() {
         if (ctx->timing) {
             cudaEvent_t b = take_event(ctx);
-            cudaEventRecord(b, ctx->s_main);
+            cudaEventRecord(b, s);
             pool_of(ctx).pending.push_back({cls, a, b});
         }
     }
@@ -129,11 +129,13 @@ static void harvest_timers(nek_ctx *ctx)
 }
 
 // ------------------------------------------------------------ building blocks
-static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, const AxLaunch &L)
+static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, const AxLaunch &L,
+                 cudaStream_t strm = nullptr)
 {
-    Scope sc(ctx, CLS_AX);
+    if (!strm) strm = ctx->s_main;
+    Scope sc(ctx, CLS_AX, strm);
     int nl = 0;
-    CK(launch_ax(ctx->variant, ctx->N, L, u, ctx->G, ctx->wJ, ctx->mbits, h1, h2, w, ctx->s_main, &nl));
+    CK(launch_ax(ctx->variant, ctx->N, L, u, ctx->G, ctx->wJ, ctx->mbits, h1, h2, w, strm, &nl));
     ctx->stats.ax_launches += L.nelem > 0;
     ctx->stats.launches += nl;
     ctx->stats.ax_elements += L.nelem;
@@ -152,26 +154,27 @@ static P2PMail mail_of(const nek_ctx *ctx)
     return m;
 }
 
-static int halo_start(nek_ctx *ctx, const double *v, const int *done)
+static int halo_start(nek_ctx *ctx, const double *v, const int *done, cudaStream_t strm = nullptr)
 {
+    if (!strm) strm = ctx->s_main;
     if (ctx->p2p) {   // interface partials written straight into the neighbours' buffers over NVLink
-        Scope sc(ctx, CLS_HALO);
+        Scope sc(ctx, CLS_HALO, strm);
         CK(launch_gs_pack_p2p_fused(ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots, ctx->send_run,
                                     ctx->d_slot_nbr, ctx->d_peer_recv, ctx->d_remote_off, ctx->d_send_offs,
                                     ctx->nslots, (int)ctx->neighbors.size(), ctx->rank, ctx->d_peer_hflags,
-                                    ctx->epochs, ctx->counter + 3, done, ctx->s_main));
+                                    ctx->epochs, ctx->counter + 3, done, strm));
         ctx->stats.launches += 1;
         ctx->stats.halo_launches += 1;
         return NEK_OK;
     }
     {
-        Scope sc(ctx, CLS_HALO);
+        Scope sc(ctx, CLS_HALO, strm);
         CK(launch_gs_ifc_pack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots,
-                              ctx->send_run, ctx->sendbuf, done, ctx->s_main));
+                              ctx->send_run, ctx->sendbuf, done, strm));
         ctx->stats.launches += (ctx->nifc > 0) + (ctx->nslots > 0);
         ctx->stats.halo_launches += 1;
     }
-    CK(cudaEventRecord(ctx->ev_fork, ctx->s_main));
+    CK(cudaEventRecord(ctx->ev_fork, strm));
     CK(cudaStreamWaitEvent(ctx->s_comm, ctx->ev_fork, 0));
     NK(ncclGroupStart());
     for (size_t k = 0; k < ctx->neighbors.size(); ++k) {
@@ -262,36 +265,34 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     const int64_t nb = ctx->n_boundary, ni = ctx->E - ctx->n_boundary;
     const int64_t g1 = ax_grid(ctx->variant, ctx->N, nb), g2 = ax_grid(ctx->variant, ctx->N, ni);
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
-    if (ctx->p2p && ax_has_halo_pack(ctx->variant, ctx->N)) {
-        // ONE Ax launch: boundary elements first; the CTA finishing the last boundary element
-        // sends the halo over NVLink while the other CTAs go on with interior elements
-        L.elist = ctx->elist;
-        L.nelem = ctx->E;
-        if (dot) { L.part = ctx->part; L.fin_total = ax_grid(ctx->variant, ctx->N, ctx->E); }
-        if (push) L.mail = mail_of(ctx);
-        HaloPack &H = L.halo;
-        H.nbnd = nb; H.bnd_counter = ctx->counter + 3;
-        H.perm = ctx->ifc_perm; H.offs = ctx->ifc_offs; H.send_run = ctx->send_run; H.slot_nbr = ctx->d_slot_nbr;
-        H.partial = ctx->ifc_partial; H.peer_recv = ctx->d_peer_recv; H.remote_off = ctx->d_remote_off;
-        H.send_offs = ctx->d_send_offs; H.nslots = ctx->nslots; H.half = ctx->nslots;
-        H.nnbr = (int)ctx->neighbors.size(); H.me = ctx->rank; H.peer_hflags = ctx->d_peer_hflags;
-        H.epochs = ctx->epochs;
-        if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
-        ctx->stats.halo_launches += 1;
-        return gs_local_and_unpack_p2p(ctx, w, done);
-    }
     L.elist = ctx->elist;
-    L.nelem = nb;
-    if (dot) { L.part = ctx->part; L.part_off = 0; L.fin_total = ni > 0 ? 0 : g1; }
-    if (push && ni == 0) L.mail = mail_of(ctx);
-    if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
-    if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
-    if (ni > 0) {
-        L.nelem = ni;
-        L.eoff = nb;
-        if (dot) { L.part_off = g1; L.fin_total = g1 + g2; }
+    if (ax_has_fused(ctx->variant, ctx->N)) {
+        // Boundary elements and the halo send on the high-priority stream, interior elements on
+        // the main stream, concurrently; the last CTA of either launch finalises sigma.
+        CK(cudaEventRecord(ctx->ev_fork2, ctx->s_main));
+        CK(cudaStreamWaitEvent(ctx->s_hi, ctx->ev_fork2, 0));
+        if (dot) { L.part = ctx->part; L.fin_total = g1 + g2; L.ctas_total = (unsigned)(g1 + g2); }
         if (push) L.mail = mail_of(ctx);
+        L.nelem = nb; L.eoff = 0; L.part_off = 0;
+        if ((st = do_ax(ctx, h1, h2, u, w, L, ctx->s_hi)) != NEK_OK) return st;
+        if ((st = halo_start(ctx, w, done, ctx->s_hi)) != NEK_OK) return st;
+        CK(cudaEventRecord(ctx->ev_bnd, ctx->s_hi));
+        L.nelem = ni; L.eoff = nb; L.part_off = g1;
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
+        CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_bnd, 0));
+    } else {
+        L.nelem = nb;
+        if (dot) { L.part = ctx->part; L.part_off = 0; L.fin_total = ni > 0 ? 0 : g1; }
+        if (push && ni == 0) L.mail = mail_of(ctx);
+        if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
+        if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
+        if (ni > 0) {
+            L.nelem = ni;
+            L.eoff = nb;
+            if (dot) { L.part_off = g1; L.fin_total = g1 + g2; }
+            if (push) L.mail = mail_of(ctx);
+            if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
+        }
     }
     if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, w, done);
     if ((st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
@@ -490,7 +491,12 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
 
     CK(cudaStreamCreateWithFlags(&ctx->s_main, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ctx->s_comm, cudaStreamNonBlocking));
-    for (cudaEvent_t *e : {&ctx->ev_in, &ctx->ev_out, &ctx->ev_fork, &ctx->ev_join})
+    {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi));
+    }
+    for (cudaEvent_t *e : {&ctx->ev_in, &ctx->ev_out, &ctx->ev_fork, &ctx->ev_join, &ctx->ev_fork2, &ctx->ev_bnd})
         CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     enter(ctx, stream);
 
@@ -668,10 +674,12 @@ int nek_free(nek_ctx *ctx)
     for (auto &t : P.pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : P.free_ev) cudaEventDestroy(e);
     P.pending.clear(); P.free_ev.clear();
-    for (cudaEvent_t e : {ctx->ev_in, ctx->ev_out, ctx->ev_fork, ctx->ev_join}) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {ctx->ev_in, ctx->ev_out, ctx->ev_fork, ctx->ev_join, ctx->ev_fork2, ctx->ev_bnd})
+        if (e) cudaEventDestroy(e);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
     if (ctx->s_comm) cudaStreamDestroy(ctx->s_comm);
+    if (ctx->s_hi) cudaStreamDestroy(ctx->s_hi);
     nek_plan_free(ctx->plan);
     delete ctx;
     return NEK_OK;

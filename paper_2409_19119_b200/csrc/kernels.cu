@@ -274,12 +274,14 @@ cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst
 }
 
 // Last CTA to finish sums part[0..count) (fixed order) into dst[0] and resets the counter.
+// ctas_total: CTAs (over one or several concurrent launches) that share `counter`.
 __device__ __forceinline__ void last_block_finish(double *part, int64_t count, double *dst, unsigned int *counter,
-                                                  double *sred, int *s_last, const P2PMail *mail = nullptr)
+                                                  double *sred, int *s_last, const P2PMail *mail = nullptr,
+                                                  unsigned int ctas_total = 0)
 {
     if (threadIdx.x == 0) {
         __threadfence();
-        *s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        *s_last = atomicAdd(counter, 1u) == (ctas_total ? ctas_total : gridDim.x) - 1;
     }
     __syncthreads();
     if (*s_last) {
@@ -977,34 +979,6 @@ static cudaError_t ax_v4_launch(const AxLaunch &L, const double *u, const double
     return cudaGetLastError();
 }
 
-// ------------------------------------------------- in-kernel halo pack (P2P)
-// All threads of one CTA: fold every send slot's interface run (local copies
-// in ascending order), keep the partial for the unpack, store it into the
-// neighbour's receive buffer (NVLink), then raise each neighbour's flag with
-// this exchange's epoch.
-__device__ __noinline__ void halo_pack_cta(const HaloPack &H, const double *w, bool with_data)
-{
-    const uint64_t e = *(volatile uint64_t *)(H.epochs + 2) + 1;
-    const int64_t half = (int64_t)(e & 1) * H.half;
-    if (with_data) {
-        for (int64_t sidx = threadIdx.x; sidx < H.nslots; sidx += blockDim.x) {
-            const int run = H.send_run[sidx];
-            const int o0 = H.offs[run], o1 = H.offs[run + 1];
-            double s = __ldcg(w + H.perm[o0]);
-            for (int c = o0 + 1; c < o1; ++c) s += __ldcg(w + H.perm[c]);
-            H.partial[run] = s;
-            const int k = H.slot_nbr[sidx];
-            H.peer_recv[k][half + H.remote_off[k] + (sidx - H.send_offs[k])] = s;
-        }
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        H.epochs[2] = e;
-        for (int k = 0; k < H.nnbr; ++k) st_release_sys(H.peer_hflags[k] + H.me, e);
-    }
-}
-
 // ------------------------------------------------------------------- Ax v5
 // v4 with the roles of j and k exchanged: a warp owns the k-slabs {2w, 2w+1},
 // lane (q, r) the points (i = 2q + v, j = r, k).  Every per-slab load or store
@@ -1027,15 +1001,11 @@ __global__ void __launch_bounds__(128, MINB)
                  double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
                  int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done,
                  double *pvec, double *__restrict__ xvec, const double *__restrict__ rvec,
-                 const double *__restrict__ dvec, const PcgScalars *sc, P2PMail mail, HaloPack H)
+                 const double *__restrict__ dvec, const PcgScalars *sc, P2PMail mail, unsigned int ctas_total)
 {
     constexpr int P3 = 512, N = 7;
-    if (done && *(volatile const int *)done) {
-        if (H.nbnd >= 0 && blockIdx.x == 0) halo_pack_cta(H, w, false);   // keep the exchange epochs in step
-        return;
-    }
+    if (done && *(volatile const int *)done) return;
     __shared__ AxV5Smem S;
-    if (H.nbnd == 0 && blockIdx.x == 0) halo_pack_cta(H, w, true);    // no boundary elements on this rank
     double beta = 0.0, alpha = 0.0;
     if (FUSED) { beta = sc->beta; alpha = sc->alpha; }
     const int t = threadIdx.x, lane = t & 31, wq = t >> 5, q = lane & 3, r = lane >> 2;
@@ -1212,22 +1182,13 @@ __global__ void __launch_bounds__(128, MINB)
             dot = fma(uk[kk].x, v0, dot);
             dot = fma(uk[kk].y, v1, dot);
         }
-        if (H.nbnd > 0 && pos < H.nbnd) {         // a partition-boundary element is complete
-            __threadfence();
-            __syncthreads();
-            if (t == 0) S.last = atomicAdd(H.bnd_counter, 1u) == (unsigned int)(H.nbnd - 1);
-            __syncthreads();
-            if (S.last) {                          // the last one: this CTA sends the halo now
-                __threadfence();
-                halo_pack_cta(H, w, true);
-                if (t == 0) *H.bnd_counter = 0u;
-            }
-        }
     }
     if (part) {
         const double sum = block_sum(dot, S.sred);
         if (t == 0) part[part_off + blockIdx.x] = sum;
-        if (fin_total > 0) last_block_finish(part, fin_total, dst, counter, S.sred, &S.last, mail.nranks > 1 ? &mail : nullptr);
+        if (fin_total > 0)
+            last_block_finish(part, fin_total, dst, counter, S.sred, &S.last, mail.nranks > 1 ? &mail : nullptr,
+                              ctas_total);
     }
 }
 
@@ -1238,17 +1199,17 @@ static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double
     if (L.fused)
         ax_v5_kernel<HELM, true, MINB, L2PF><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
                                                                  L.part, L.part_off, L.fin_total, L.dst, L.counter,
-                                                                 L.done, L.p, L.x, L.r, L.dinv, L.sc, L.mail, L.halo);
+                                                                 L.done, L.p, L.x, L.r, L.dinv, L.sc, L.mail,
+                                                                 L.ctas_total ? L.ctas_total : (unsigned)grid);
     else
         ax_v5_kernel<HELM, false, MINB, L2PF><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
                                                                   L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                   L.done, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                                                  L.mail, L.halo);
+                                                                  L.mail, L.ctas_total ? L.ctas_total : (unsigned)grid);
     return cudaGetLastError();
 }
 
 bool ax_has_fused(int variant, int N) { return (variant == 0 || variant == 8 || variant == 9) && N == 7; }
-bool ax_has_halo_pack(int variant, int N) { return ax_has_fused(variant, N); }
 
 // variant (N = 7): 0 = default (v5, DMMA, k-slabs, 4 CTAs/SM), 8 = v5 at 3 CTAs/SM,
 // 9 = v5 + L2 bulk prefetch of the next element, 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,

@@ -36,22 +36,6 @@ struct P2PMail {
     int me = 0, nranks = 1;
 };
 
-// Halo pack done inside the Ax kernel (P2P): the CTA that completes the last
-// partition-boundary element folds the interface partials and writes them into
-// the neighbours' receive buffers, then raises their flags.
-struct HaloPack {
-    int64_t nbnd = -1;                    // boundary elements = first nbnd positions of elist; < 0: off
-    unsigned int *bnd_counter = nullptr;
-    const int32_t *perm = nullptr, *offs = nullptr, *send_run = nullptr, *slot_nbr = nullptr;
-    double *partial = nullptr;
-    double *const *peer_recv = nullptr;
-    const int64_t *remote_off = nullptr, *send_offs = nullptr;
-    int64_t nslots = 0, half = 0;
-    int nnbr = 0, me = 0;
-    uint64_t *const *peer_hflags = nullptr;
-    uint64_t *epochs = nullptr;
-};
-
 // Reduction slots (device): red_loc = this rank's partial sums, red_all = the
 // nranks partials gathered in rank order (equal to red_loc at nranks == 1).
 enum { RED_SIGMA = 0, RED_RHO = 1, RED_RR = 2, RED_N = 3 };
@@ -85,7 +69,7 @@ struct AxLaunch {
     // element's points before the operator is applied to the new p (u == p then)
     bool fused = false;
     P2PMail mail;                        // mail.nranks > 1: the finalising CTA pushes sigma to every rank
-    HaloPack halo;                       // halo.nbnd >= 0: in-kernel halo pack (Ax v5 only)
+    unsigned int ctas_total = 0;         // > 0: CTAs of all concurrent launches sharing the finalise counter
     double *p = nullptr, *x = nullptr;
     const double *r = nullptr, *dinv = nullptr;
     const PcgScalars *sc = nullptr;
@@ -141,7 +125,6 @@ cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, do
 cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s);
 bool ax_has_fused(int variant, int N);
-bool ax_has_halo_pack(int variant, int N);
 // NVLink peer-memory exchange (CUDA IPC mappings; see kernels.cu)
 cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *red_loc, double *red_all, double *mbox,
                                 double *const *peer_mbox, uint64_t *epochs, int *err, cudaStream_t s);
@@ -177,8 +160,9 @@ struct nek_ctx {
     int64_t n = 0;
     int rank = 0, nranks = 1;
     ncclComm_t nccl = nullptr;
-    cudaStream_t s_main = nullptr, s_comm = nullptr;
+    cudaStream_t s_main = nullptr, s_comm = nullptr, s_hi = nullptr;   // s_hi: high priority (boundary work)
     cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork2 = nullptr, ev_bnd = nullptr;
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
     nek_plan *plan = nullptr;
     int variant = 0;
