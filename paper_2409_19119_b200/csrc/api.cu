@@ -216,7 +216,7 @@ static int do_gs_local(nek_ctx *ctx, double *v, const int *done)
 }
 
 // P2P: the local runs and the halo unpack (which waits for the neighbours' data) in one launch
-static int gs_local_and_unpack_p2p(nek_ctx *ctx, double *v, const int *done)
+static int gs_local_and_unpack_p2p(nek_ctx *ctx, double *v, const int *done, bool skip_local = false)
 {
     Scope sc(ctx, CLS_GS);
     HaloUnpack U;
@@ -224,7 +224,7 @@ static int gs_local_and_unpack_p2p(nek_ctx *ctx, double *v, const int *done)
     U.contrib = ctx->contrib; U.nbr = ctx->d_nbr; U.partial = ctx->ifc_partial; U.recv = ctx->recv2;
     U.half = ctx->nslots; U.hflags = ctx->hflags; U.epochs = ctx->epochs; U.nnbr = (int)ctx->neighbors.size();
     U.err = ctx->p2p_err;
-    CK(launch_gs_classes_unpack(ctx->gsc, U, v, done, ctx->s_main));
+    CK(launch_gs_classes_unpack(skip_local ? GsClasses() : ctx->gsc, U, v, done, ctx->s_main));
     ctx->stats.gs_launches += 1;
     ctx->stats.launches += 1;
     return NEK_OK;
@@ -245,7 +245,7 @@ static int gs_full(nek_ctx *ctx, double *v, const int *done)
 // red_loc[RED_SIGMA] (then allgathered across ranks into red_all).  fused: the
 // PCG direction / deferred x update is applied in the Ax prologue (u == vp).
 static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, bool dot, const int *done,
-                    bool fused = false)
+                    bool fused = false, bool skip_local_gs = false)
 {
     int st;
     AxLaunch L;
@@ -260,7 +260,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         L.nelem = ctx->E;
         if (dot) { L.part = ctx->part; L.fin_total = ax_grid(ctx->variant, ctx->N, ctx->E); }
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
-        return do_gs_local(ctx, w, done);
+        return skip_local_gs ? NEK_OK : do_gs_local(ctx, w, done);
     }
     const int64_t nb = ctx->n_boundary, ni = ctx->E - ctx->n_boundary;
     const int64_t g1 = ax_grid(ctx->variant, ctx->N, nb), g2 = ax_grid(ctx->variant, ctx->N, ni);
@@ -294,8 +294,8 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
             if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         }
     }
-    if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, w, done);
-    if ((st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
+    if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, w, done, skip_local_gs);
+    if (!skip_local_gs && (st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
     return halo_finish(ctx, w, done);
 }
 
@@ -556,6 +556,22 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         ctx->gsc.ng = (int64_t)og.size() - 1;
         ctx->gsc.p2 = ctx->gs_p2; ctx->gsc.p4 = ctx->gs_p4; ctx->gsc.p8 = ctx->gs_p8;
         ctx->gsc.pg = ctx->gs_pg; ctx->gsc.og = ctx->gs_og;
+        // inline tables for the residual update: pair partner, or a generic run id
+        std::vector<int32_t> idx(ctx->n, -1), gp, go(1, 0);
+        for (int64_t r = 0; r < ctx->nruns; ++r) {
+            const int64_t a0 = p->offs[r], len = p->offs[r + 1] - a0;
+            if (len == 2) {
+                idx[p->perm[a0]] = p->perm[a0 + 1];
+                idx[p->perm[a0 + 1]] = p->perm[a0];
+            } else {
+                const int32_t gr = (int32_t)go.size() - 1;
+                for (int64_t c = 0; c < len; ++c) { gp.push_back(p->perm[a0 + c]); idx[p->perm[a0 + c]] = -(gr + 2); }
+                go.push_back((int32_t)gp.size());
+            }
+        }
+        CK(upload(ctx, &ctx->gsi_idx, idx)); CK(upload(ctx, &ctx->gsi_perm, gp)); CK(upload(ctx, &ctx->gsi_offs, go));
+        const char *genv = getenv("NEK_GS_INLINE");
+        ctx->gs_inline = !(genv && std::strcmp(genv, "0") == 0);
     }
     ctx->nifc = (int64_t)p->ifc_offs.size() - 1; ctx->nifc_perm = (int64_t)p->ifc_perm.size();
     CK(upload(ctx, &ctx->ifc_perm, p->ifc_perm));
@@ -661,7 +677,8 @@ int nek_free(nek_ctx *ctx)
                     (void *)ctx->vx, (void *)ctx->vdinv, (void *)ctx->vtmp, (void *)ctx->stage_in,
                     (void *)ctx->stage_out, (void *)ctx->part, (void *)ctx->red_loc, (void *)ctx->sc,
                     (void *)ctx->counter, (void *)ctx->hist, (void *)ctx->gs_p2, (void *)ctx->gs_p4,
-                    (void *)ctx->gs_p8, (void *)ctx->gs_pg, (void *)ctx->gs_og})
+                    (void *)ctx->gs_p8, (void *)ctx->gs_pg, (void *)ctx->gs_og, (void *)ctx->gsi_idx,
+                    (void *)ctx->gsi_perm, (void *)ctx->gsi_offs})
         if (p) cudaFree(p);
     if (ctx->red_all && ctx->red_all != ctx->red_loc) cudaFree(ctx->red_all);
     for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -738,30 +755,34 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
     int st;
     const int *done = &ctx->sc->done;
     const int nb = vec_blocks();
+    GsInline gi;
+    if (ctx->gs_inline) { gi.idx = ctx->gsi_idx; gi.perm = ctx->gsi_perm; gi.offs = ctx->gsi_offs; }
+    const GsInline *gip = ctx->gs_inline ? &gi : nullptr;
     if (use_fused(ctx) && ctx->p2p) {
         // sigma pushed by the Ax kernel, pulled by the update kernel; (rho', rr) pushed by the
         // update kernel, pulled by the bookkeeping kernel: no separate exchange launches
-        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
+        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true, ctx->gs_inline)) != NEK_OK) return st;
         const P2PMail m = mail_of(ctx);
         {
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, &m));
+                                       ctx->counter + 2, ctx->s_main, &m, gip));
             CK(launch_pcg_fin_p2p(ctx->sc, m, ctx->hist, ctx->s_main));
             ctx->stats.launches += 2; ctx->stats.vec_launches += 2;
         }
         return NEK_OK;
     }
     if (use_fused(ctx)) {
-        // Ax prologue: p = Dinv r + beta p, x += alpha p (deferred); then w = A p, sigma
-        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
+        // Ax prologue: p = Dinv r + beta p, x += alpha p (deferred); then w = A p, sigma; the local
+        // gather-scatter of w happens inside the residual update
+        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true, ctx->gs_inline)) != NEK_OK) return st;
         if ((st = exchange_slots(ctx, 0)) != NEK_OK) return st;
         {
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main));
+                                       ctx->counter + 2, ctx->s_main, nullptr, gip));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
         if (ctx->nranks > 1) {

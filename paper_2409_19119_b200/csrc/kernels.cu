@@ -1844,6 +1844,22 @@ cudaError_t launch_pcg_pupdate(int64_t n, const double *dinv, const double *r, d
 }
 
 // ---------------------------------------------------------- fused PCG path
+// QQ^T w at one local point from the unassembled w (gather-scatter folded into the
+// residual update).  id = -1: not in a local run (unshared, or an interface copy
+// whose total the halo unpack already wrote); id >= 0: the other copy of a pair
+// run (a + b == b + a exactly, so both copies get the canonical bits); id <= -2:
+// run -(id+2) of the generic list, folded in canonical order.
+__device__ __forceinline__ double w_assembled(int32_t id, double wl, const double *__restrict__ w, const GsInline &gi)
+{
+    if (id == -1) return wl;
+    if (id >= 0) return wl + __ldg(w + id);
+    const int run = -id - 2;
+    const int o0 = gi.offs[run], o1 = gi.offs[run + 1];
+    double s = __ldg(w + gi.perm[o0]);
+    for (int c = o0 + 1; c < o1; ++c) s += __ldg(w + gi.perm[c]);
+    return s;
+}
+
 // Iteration bookkeeping after <r, Dinv r> and <r, r> of the new residual are
 // known: history, convergence / maxit, the pending alpha for the deferred x
 // update and beta for the next direction.
@@ -1865,7 +1881,7 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
     pcg_update_fused_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                             const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ red_all,
                             int nranks, PcgScalars *sc, double *hist, double *__restrict__ part, double *dst,
-                            unsigned int *counter, P2PMail mail)
+                            unsigned int *counter, P2PMail mail, GsInline gi)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ int s_last;
@@ -1889,16 +1905,29 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
     const int64_t n2 = n >> 1;
     const double2 *w2 = reinterpret_cast<const double2 *>(w), *d2 = reinterpret_cast<const double2 *>(dinv);
     double2 *r2 = reinterpret_cast<double2 *>(r);
+    const int2 *i2 = reinterpret_cast<const int2 *>(gi.idx);
     const int64_t tile = (int64_t)VEC_UNROLL * blockDim.x;
     for (int64_t base = blockIdx.x * tile + threadIdx.x; base < n2; base += (int64_t)gridDim.x * tile) {
         double2 wv[VEC_UNROLL], dv[VEC_UNROLL], rv[VEC_UNROLL];
         uint32_t ow[VEC_UNROLL];
+        int2 id[VEC_UNROLL];
 #pragma unroll
         for (int q = 0; q < VEC_UNROLL; ++q) {
             const int64_t h = base + (int64_t)q * blockDim.x;
             if (h < n2) {
                 wv[q] = w2[h]; dv[q] = d2[h]; rv[q] = r2[h];
                 ow[q] = __ldg(obits + ((2 * h) >> 5)) >> ((2 * h) & 31);
+                if (gi.idx) id[q] = i2[h];
+            }
+        }
+        if (gi.idx) {   // the gather-scatter QQ^T of w, on the fly (canonical order, bit-exact)
+#pragma unroll
+            for (int q = 0; q < VEC_UNROLL; ++q) {
+                const int64_t h = base + (int64_t)q * blockDim.x;
+                if (h < n2) {
+                    wv[q].x = w_assembled(id[q].x, wv[q].x, w, gi);
+                    wv[q].y = w_assembled(id[q].y, wv[q].y, w, gi);
+                }
             }
         }
 #pragma unroll
@@ -1914,7 +1943,8 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
     }
     if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
         const int64_t l = n - 1;
-        const double rv = fma(-alpha, w[l], r[l]);
+        const double wl = gi.idx ? w_assembled(gi.idx[l], w[l], w, gi) : w[l];
+        const double rv = fma(-alpha, wl, r[l]);
         r[l] = rv;
         if (bit_of(obits, l)) { a0 = fma(rv, dinv[l] * rv, a0); a1 = fma(rv, rv, a1); }
     }
@@ -1947,12 +1977,14 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail)
+                                    const P2PMail *mail, const GsInline *gi)
 {
     P2PMail m;
     if (mail) m = *mail;
+    GsInline g;
+    if (gi) g = *gi;
     pcg_update_fused_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist, part, dst,
-                                                         counter, m);
+                                                         counter, m, g);
     return cudaGetLastError();
 }
 

@@ -36,6 +36,14 @@ struct P2PMail {
     int me = 0, nranks = 1;
 };
 
+// Gather-scatter folded into the residual update: per local point an index
+// (-1: take w as is; >= 0: partner copy of a pair run; <= -2: generic run -(id+2)
+// in perm/offs, the non-pair local runs in canonical order).
+struct GsInline {
+    const int32_t *idx = nullptr;
+    const int32_t *perm = nullptr, *offs = nullptr;
+};
+
 // Reduction slots (device): red_loc = this rank's partial sums, red_all = the
 // nranks partials gathered in rank order (equal to red_loc at nranks == 1).
 enum { RED_SIGMA = 0, RED_RHO = 1, RED_RR = 2, RED_N = 3 };
@@ -107,7 +115,7 @@ cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *ob
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail = nullptr);
+                                    const P2PMail *mail = nullptr, const GsInline *gi = nullptr);
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
 // local gather-scatter and (P2P) the halo unpack in one launch
 struct HaloUnpack {
@@ -121,7 +129,7 @@ struct HaloUnpack {
     int *err = nullptr;
 };
 cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, double *v, const int *done,
-                                     cudaStream_t s);
+                                     cudaStream_t s);   // C empty: halo unpack only
 cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s);
 bool ax_has_fused(int variant, int N);
@@ -173,6 +181,8 @@ struct nek_ctx {
     int32_t *perm = nullptr, *offs = nullptr;
     int64_t nruns = 0, nperm = 0;
     int32_t *gs_p2 = nullptr, *gs_p4 = nullptr, *gs_p8 = nullptr, *gs_pg = nullptr, *gs_og = nullptr;
+    int32_t *gsi_idx = nullptr, *gsi_perm = nullptr, *gsi_offs = nullptr;   // GsInline tables
+    bool gs_inline = false;
     nekb200::GsClasses gsc;
     int32_t *ifc_perm = nullptr, *ifc_offs = nullptr, *send_run = nullptr, *coffs = nullptr, *contrib = nullptr;
     int64_t nifc = 0, nifc_perm = 0, nslots = 0;
