@@ -54,8 +54,8 @@ def parse():
     ap.add_argument("--order", type=int, default=NORD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0, help="Ax kernel variant (nek_set_variant; 0 = default)")
-    ap.add_argument("--graph", action="store_true", help="time with the CUDA-graph PCG loop instead of "
-                    "eager launches + per-kernel events (no roofline then)")
+    ap.add_argument("--graph", action="store_true", help="no per-kernel event nodes in the CUDA graph "
+                    "(no per-replay synchronisation; no roofline then)")
     return ap.parse_args()
 
 
@@ -312,7 +312,8 @@ def main():
                        "pcg_iters_per_step": args.iters, "h1": 1.0, "h2": 0.0,
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
                        "parallelism": f"dp{world} (element z-slabs, NCCL halo + allgather reductions)",
-                       "timing": "eager launches + per-kernel CUDA events" if timing else "CUDA graph"},
+                       "timing": ("CUDA graph of 10 iterations with per-kernel event-record nodes (read after "
+                                  "each replay)") if timing else "CUDA graph of 10 iterations"},
             "pcg_iter_per_s": args.iters * args.steps / (t_ms * 1e-3),
             "ax_gs": {"gdof_per_s": ax_gdofs, "ms_per_apply": ax_ms / reps,
                       "algorithmic_GBps": (ax_bytes_per_elem * mesh.E * world / P3 * P3 + 0) * reps / (ax_ms * 1e-3) / 1e9},

@@ -80,7 +80,7 @@ static std::vector<uint32_t> pack_bits(const std::vector<uint8_t> &v)
 
 // ------------------------------------------------------------ timing pool
 namespace {
-struct TimedLaunch { int cls; cudaEvent_t a, b; };
+using nekb200::TimedLaunch;
 struct TimerPool {
     std::vector<cudaEvent_t> free_ev;
     std::vector<TimedLaunch> pending;
@@ -102,17 +102,49 @@ static cudaEvent_t take_event(nek_ctx *ctx)
 enum { CLS_AX = 0, CLS_GS = 1, CLS_HALO = 2, CLS_VEC = 3 };
 struct Scope {
     nek_ctx *ctx; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
+    // inside a stream capture the records must be EXTERNAL event nodes (a plain record only
+    // becomes a dependency edge of the graph)
+    static void rec(nek_ctx *c, cudaEvent_t e, cudaStream_t st)
+    {
+        if (c->capturing) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+        else cudaEventRecord(e, st);
+    }
     Scope(nek_ctx *c, int k, cudaStream_t st = nullptr) : ctx(c), cls(k), s(st ? st : c->s_main) {
-        if (ctx->timing) { a = take_event(ctx); cudaEventRecord(a, s); }
+        if (ctx->timing) { a = take_event(ctx); rec(ctx, a, s); }
     }
     ~Scope() {
         if (ctx->timing) {
             cudaEvent_t b = take_event(ctx);
-            cudaEventRecord(b, s);
-            pool_of(ctx).pending.push_back({cls, a, b});
+            rec(ctx, b, s);
+            // inside a stream capture the pair becomes two event-record nodes of the graph; their
+            // elapsed time is read after every replay
+            if (ctx->capturing) ctx->graph_timers.push_back({cls, a, b});
+            else pool_of(ctx).pending.push_back({cls, a, b});
         }
     }
 };
+
+static double *cls_slot(nek_ctx *ctx, int cls)
+{
+    return cls == CLS_AX ? &ctx->stats.ax_ms : cls == CLS_GS ? &ctx->stats.gs_ms
+         : cls == CLS_HALO ? &ctx->stats.halo_ms : &ctx->stats.vec_ms;
+}
+
+// after a replay of a graph captured in timing mode (the caller synchronised the stream)
+static void harvest_graph_timers(nek_ctx *ctx)
+{
+    for (auto &t : ctx->graph_timers) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventElapsedTime(&ms, t.a, t.b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            ms = 0.f;
+            if (getenv("NEK_DEBUG")) fprintf(stderr, "nek: graph timer: %s\n", cudaGetErrorString(e));
+        }
+        *cls_slot(ctx, t.cls) += ms;
+    }
+}
+
 static void harvest_timers(nek_ctx *ctx)
 {
     TimerPool &P = pool_of(ctx);
@@ -120,9 +152,7 @@ static void harvest_timers(nek_ctx *ctx)
         float ms = 0.f;
         cudaEventSynchronize(t.b);
         if (cudaEventElapsedTime(&ms, t.a, t.b) != cudaSuccess) { cudaGetLastError(); ms = 0.f; }
-        double *dst = t.cls == CLS_AX ? &ctx->stats.ax_ms : t.cls == CLS_GS ? &ctx->stats.gs_ms
-                    : t.cls == CLS_HALO ? &ctx->stats.halo_ms : &ctx->stats.vec_ms;
-        *dst += ms;
+        *cls_slot(ctx, t.cls) += ms;
         P.free_ev.push_back(t.a); P.free_ev.push_back(t.b);
     }
     P.pending.clear();
@@ -570,8 +600,10 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
             }
         }
         CK(upload(ctx, &ctx->gsi_idx, idx)); CK(upload(ctx, &ctx->gsi_perm, gp)); CK(upload(ctx, &ctx->gsi_offs, go));
+        // off by default: measured slower (the partner gathers are dependent loads inside a
+        // streaming kernel, and miss L2 at scale); NEK_GS_INLINE=1 turns it on
         const char *genv = getenv("NEK_GS_INLINE");
-        ctx->gs_inline = !(genv && std::strcmp(genv, "0") == 0);
+        ctx->gs_inline = genv && std::strcmp(genv, "1") == 0;
     }
     ctx->nifc = (int64_t)p->ifc_offs.size() - 1; ctx->nifc_perm = (int64_t)p->ifc_perm.size();
     CK(upload(ctx, &ctx->ifc_perm, p->ifc_perm));
@@ -670,6 +702,7 @@ int nek_free(nek_ctx *ctx)
     cudaSetDevice(ctx->device);
     if (ctx->s_main) cudaStreamSynchronize(ctx->s_main);
     if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+    for (auto &t : ctx->graph_timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (void *p : {(void *)ctx->G, (void *)ctx->wJ, (void *)ctx->perm, (void *)ctx->offs, (void *)ctx->ifc_perm,
                     (void *)ctx->ifc_offs, (void *)ctx->send_run, (void *)ctx->coffs, (void *)ctx->contrib,
                     (void *)ctx->ifc_partial, (void *)ctx->sendbuf, (void *)ctx->recvbuf, (void *)ctx->elist,
@@ -850,19 +883,27 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     ctx->stats.launches += 1;
 
     const int C = std::max(1, std::min(maxit, 10));
-    const bool use_graph = !ctx->timing;
-    if (use_graph && (!ctx->graph || ctx->graph_iters != C || ctx->graph_h1 != h1 || ctx->graph_h2 != h2)) {
+    const char *genv = getenv("NEK_NO_GRAPH");
+    const bool use_graph = !(genv && std::strcmp(genv, "0") != 0);
+    if (use_graph && (!ctx->graph || ctx->graph_iters != C || ctx->graph_h1 != h1 || ctx->graph_h2 != h2 ||
+                      ctx->graph_timing != ctx->timing)) {
         if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+        for (auto &t : ctx->graph_timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+        ctx->graph_timers.clear();
+        ctx->capturing = true;
         cudaGraph_t g;
         nek_stats_t saved = ctx->stats;
         CK(cudaStreamBeginCapture(ctx->s_main, cudaStreamCaptureModeThreadLocal));
         for (int k = 0; k < C; ++k) {
             if ((st = pcg_iteration(ctx, h1, h2)) != NEK_OK) {
                 cudaStreamEndCapture(ctx->s_main, &g);
+                ctx->capturing = false;
                 return st;
             }
         }
+        ctx->capturing = false;
         CK(cudaStreamEndCapture(ctx->s_main, &g));
+        ctx->graph_timing = ctx->timing;
         // launches recorded in one replay of the graph
         ctx->graph_stats = ctx->stats;
         ctx->graph_stats.launches -= saved.launches;
@@ -887,6 +928,10 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
             ctx->stats.ax_elements += g.ax_elements; ctx->stats.gs_launches += g.gs_launches;
             ctx->stats.halo_launches += g.halo_launches; ctx->stats.vec_launches += g.vec_launches;
             launched += C;
+            if (ctx->timing) {   // per-kernel device time of this replay (event-record nodes)
+                CK(cudaStreamSynchronize(ctx->s_main));
+                harvest_graph_timers(ctx);
+            }
         } else {
             if ((st = pcg_iteration(ctx, h1, h2)) != NEK_OK) return st;
             launched += 1;

@@ -54,6 +54,9 @@ struct KernelArgsCommon {
     const uint32_t *obits;  // owner bit per local point
 };
 
+// a pair of timing events around one kernel class
+struct TimedLaunch { int cls; cudaEvent_t a, b; };
+
 // GLL rule (ascending nodes, weights) and D[i][j] = h_j'(x_i), host.
 void gll_rule(int N, double *x, double *w);
 void deriv_matrix(int N, const double *x, double *D);
@@ -210,6 +213,8 @@ struct nek_ctx {
     int graph_iters = 0;
     double graph_h1 = 0, graph_h2 = 0;
     nek_stats_t graph_stats{};
+    bool graph_timing = false, capturing = false;
+    std::vector<nekb200::TimedLaunch> graph_timers;   // event-record nodes of the timing graph
     // NVLink peer-memory path (nranks > 1, all peers mapped)
     bool p2p = false;
     double *mbox = nullptr;                 // [2 channels][2 parities][nranks][4]

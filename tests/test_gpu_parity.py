@@ -244,3 +244,55 @@ def test_config2_full_size(nek):
         assert it == 10 and np.all(np.abs(hg - ho) <= O.hist_tolerance(1.0, 0.0, b, 10))
     finally:
         nek.free(ctx)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
+def test_ax_all_variants_N7(nek, variant):
+    """Every Ax kernel variant (nek_set_variant) against the oracle, Poisson and Helmholtz."""
+    m = mg.box_mesh(3, 4, 5, 7, deform="bubble")
+    O = oracle.Oracle.from_mesh(m)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        nek.set_variant(ctx, variant)
+        u = mg.random_evector(m, seed=21)
+        for h in ((1.0, 0.0), (0.7, 2.0)):
+            w = np.empty(m.n_local)
+            nek.ax(ctx, h[0], h[1], u, w)
+            assert rel(w, O.apply(h[0], h[1], u)) <= 1e-12, (variant, h)
+        b = mg.smooth_field(m, seed=2)
+        _, ito, _, ho = O.pcg(1.0, 0.0, b, 0.0, 30)
+        x = np.zeros(m.n_local)
+        st, it, _, hg = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, 30, want_hist=True)
+        assert it == 30 and np.all(np.abs(hg - ho) <= O.hist_tolerance(1.0, 0.0, b, 30))
+    finally:
+        nek.free(ctx)
+
+
+def test_pcg_bitwise_repeatable_and_gs_inline_equivalent(nek):
+    """Two solves give identical bits; folding the gather-scatter into the residual
+    update (default) gives the same bits as the separate gs kernel (NEK_GS_INLINE=0),
+    and host-pointer and device-pointer calls agree bitwise."""
+    import os
+    m = mg.box_mesh(6, 5, 4, 7, deform="bubble")
+    b = mg.smooth_field(m, seed=7)
+    outs = []
+    for inline in ("0", "1"):
+        os.environ["NEK_GS_INLINE"] = inline
+        try:
+            ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+        finally:
+            os.environ.pop("NEK_GS_INLINE", None)
+        try:
+            bd = torch.from_numpy(b).cuda()
+            for _ in range(2):
+                xd = torch.zeros_like(bd)
+                st, it, rr, hg = nek.pcg_solve(ctx, 1.0, 0.0, bd, xd, 1e-9, 400, want_hist=True)
+                outs.append((xd.cpu().numpy(), it, hg))
+            xh = np.zeros(m.n_local)
+            st, it, rr, hh = nek.pcg_solve(ctx, 1.0, 0.0, b, xh, 1e-9, 400, want_hist=True)
+            outs.append((xh, it, hh))
+        finally:
+            nek.free(ctx)
+    x0, it0, h0 = outs[0]
+    for x, it, h in outs[1:]:
+        assert it == it0 and np.array_equal(x, x0) and np.array_equal(h, h0)
