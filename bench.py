@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--order", type=int, default=NORD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0, help="Ax kernel variant (nek_set_variant; 0 = default)")
+    ap.add_argument("--mesh", default="box", choices=["box", "rod"],
+                    help="box: 16x16xez elements per GPU (config 2 at ez=16); rod: 17x17-pin rod bundle, "
+                         "--rod-layers element layers per GPU (config 4 at 3 layers)")
+    ap.add_argument("--rod-layers", type=int, default=3)
+    ap.add_argument("--h2", type=float, default=0.0, help="Helmholtz mass coefficient (0 = Poisson)")
     ap.add_argument("--graph", action="store_true", help="no per-kernel event nodes in the CUDA graph "
                     "(no per-replay synchronisation; no roofline then)")
     return ap.parse_args()
@@ -63,14 +68,23 @@ def rank_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def make_mesh(rank, world, ez, N):
+def make_mesh(rank, world, ez, N, args=None):
     from workloads import meshgen as mg
+    if args is not None and args.mesh == "rod":
+        L = args.rod_layers
+        return mg.rod_bundle(17, 17, L, N, dirichlet="pins_walls" if args.h2 != 0.0 else "outlet",
+                             z0_layer=rank * L, nlayers_total=L * world)
     return mg.box_mesh(EX, EY, ez * world, N, deform="bubble", eps=0.05, dirichlet="all",
                        zlayers=(rank * ez, (rank + 1) * ez))
 
 
 def workload_name(args, world):
-    return (f"SEM Poisson Jacobi-PCG, {args.iters} iters/step; {EX}x{EY}x{args.ez} elements per GPU "
+    kind = "Helmholtz (h1,h2)=(1,%g)" % args.h2 if args.h2 != 0.0 else "Poisson"
+    if args.mesh == "rod":
+        return (f"SEM {kind} Jacobi-PCG, {args.iters} iters/step; 17x17-pin rod bundle, 27744 curved elements per "
+                f"layer, {args.rod_layers} layers per GPU ({args.rod_layers * world} total, z-slabs), N={args.order}, "
+                + ("Dirichlet on pins, walls, inlet" if args.h2 != 0.0 else "Dirichlet on the outlet plane"))
+    return (f"SEM {kind} Jacobi-PCG, {args.iters} iters/step; {EX}x{EY}x{args.ez} elements per GPU "
             f"(box {EX}x{EY}x{args.ez * world}, z-slabs), N={args.order}, bubble-deformed, Dirichlet all faces")
 
 
@@ -123,15 +137,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(mesh, iters):
+def cpu_baseline(mesh, iters, h2=0.0):
     """The oracle as it stands, single-threaded C, on a bounded sample."""
     import oracle
     from workloads import meshgen as mg
+    iters = max(2, int(iters * 2097152 / mesh.n_local))     # ~10-30 s of CPU work
     O = oracle.Oracle.from_mesh(mesh)
     b = mg.smooth_field(mesh, seed=1)
-    d = O.dinv(1.0, 0.0)
+    d = O.dinv(1.0, h2)
     t0 = time.perf_counter()
-    O.pcg(1.0, 0.0, b, 0.0, iters, dinv=d)
+    O.pcg(1.0, h2, b, 0.0, iters, dinv=d)
     dt = time.perf_counter() - t0
     return {"value": mesh.n_dof * iters / dt / 1e9, "unit": "GDOF/s", "cores": 1, "kind": "oracle",
             "sample": f"{iters} Jacobi-PCG iterations (incl. init) on the N=1 workload mesh, plain C oracle, 1 thread"}
@@ -141,18 +156,18 @@ def run_reference(args):
     rank, world, _ = rank_env()
     if rank != 0:
         return 0
-    mesh = make_mesh(0, 1, args.ez, args.order)
+    mesh = make_mesh(0, 1, args.ez, args.order, args)
     import oracle
     from workloads import meshgen as mg
     O = oracle.Oracle.from_mesh(mesh)
     b = mg.smooth_field(mesh, seed=1)
-    d = O.dinv(1.0, 0.0)
-    it_per_step = 10
+    d = O.dinv(1.0, args.h2)
+    it_per_step = max(1, int(10 * 2097152 / mesh.n_local))
     for _ in range(args.warmup):
-        O.pcg(1.0, 0.0, b, 0.0, it_per_step, dinv=d)
+        O.pcg(1.0, args.h2, b, 0.0, it_per_step, dinv=d)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        O.pcg(1.0, 0.0, b, 0.0, it_per_step, dinv=d)
+        O.pcg(1.0, args.h2, b, 0.0, it_per_step, dinv=d)
     dt = time.perf_counter() - t0
     val = mesh.n_dof * it_per_step * args.steps / dt / 1e9
     sample = f"{it_per_step} Jacobi-PCG iterations per step on the N=1 workload mesh, plain C oracle, 1 thread"
@@ -193,7 +208,7 @@ def main():
         if os.environ.get("NEK_BENCH_VERBOSE"):
             print(f"[rank {rank}] {msg}", file=sys.stderr, flush=True)
 
-    mesh = make_mesh(rank, world, args.ez, args.order)
+    mesh = make_mesh(rank, world, args.ez, args.order, args)
     log("setup")
     ctx = nek.setup(mesh.E, mesh.N, mesh.xyz, mesh.gid, mesh.mask, comm=comm, device=local)
     info = nek.get_info(ctx)
@@ -213,7 +228,7 @@ def main():
     log(f"transport {info['transport']}; warm-up")
     # warm-up (also builds the Jacobi diagonal and, with --graph, the CUDA graph)
     for _ in range(args.warmup):
-        nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, args.iters)
+        nek.pcg_solve(ctx, 1.0, args.h2, b, x, 0.0, args.iters)
     torch.cuda.synchronize()
     nek.get_stats(ctx, reset=True)
 
@@ -225,7 +240,7 @@ def main():
         flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        st, it, rr, _ = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, args.iters)
+        st, it, rr, _ = nek.pcg_solve(ctx, 1.0, args.h2, b, x, 0.0, args.iters)
         e1.record(stream)
         evs.append((e0, e1))
         assert it == args.iters, (st, it)
@@ -242,7 +257,7 @@ def main():
     kt_steps = 0
     if timing:
         nek.set_timing(ctx, True)
-        nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, args.iters)          # capture the timing graph
+        nek.pcg_solve(ctx, 1.0, args.h2, b, x, 0.0, args.iters)          # capture the timing graph
         nek.get_stats(ctx, reset=True)
         kt_steps = max(1, min(args.steps, 5))
         barrier(); torch.cuda.synchronize()
@@ -251,7 +266,7 @@ def main():
         for _ in range(kt_steps):
             flush.fill_(1)
             ev0.record(stream)
-            nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, args.iters)
+            nek.pcg_solve(ctx, 1.0, args.h2, b, x, 0.0, args.iters)
             ev1.record(stream)
             ev1.synchronize()
             kt_ms += ev0.elapsed_time(ev1)
@@ -264,7 +279,7 @@ def main():
     u = torch.from_numpy(mg.smooth_field(mesh, seed=2)).to(dev)
     w = torch.empty_like(u)
     for _ in range(3):
-        nek.ax(ctx, 1.0, 0.0, u, w)
+        nek.ax(ctx, 1.0, args.h2, u, w)
     reps = 20
     barrier(); torch.cuda.synchronize()
     ax_ms = 0.0
@@ -272,7 +287,7 @@ def main():
         flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        nek.ax(ctx, 1.0, 0.0, u, w)
+        nek.ax(ctx, 1.0, args.h2, u, w)
         e1.record(stream)
         e1.synchronize()
         ax_ms += e0.elapsed_time(e1)
@@ -285,12 +300,12 @@ def main():
     bh.copy_(b.cpu())
     xh = torch.empty(mesh.n_local, dtype=torch.float64, pin_memory=True)
     nek.set_timing(ctx, False)
-    nek.pcg_solve(ctx, 1.0, 0.0, bh, xh, 0.0, args.iters)
+    nek.pcg_solve(ctx, 1.0, args.h2, bh, xh, 0.0, args.iters)
     e2e_steps = max(1, min(args.steps, 5))
     barrier(); torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        nek.pcg_solve(ctx, 1.0, 0.0, bh, xh, 0.0, args.iters)
+        nek.pcg_solve(ctx, 1.0, args.h2, bh, xh, 0.0, args.iters)
     torch.cuda.synchronize(); barrier()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
 
@@ -337,7 +352,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args, world), "E_per_gpu": mesh.E, "N": mesh.N,
                        "n_dof_per_gpu": mesh.n_dof, "n_local_per_gpu": mesh.n_local,
-                       "pcg_iters_per_step": args.iters, "h1": 1.0, "h2": 0.0,
+                       "pcg_iters_per_step": args.iters, "h1": 1.0, "h2": args.h2,
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
                        "parallelism": f"dp{world} (element z-slabs, NCCL halo + allgather reductions)",
                        "timing": "CUDA graph of 10 PCG iterations per replay, device time by CUDA events"},
@@ -354,7 +369,7 @@ def main():
                      "transport": {0: "none", 1: "nccl", 2: "nvlink-p2p"}[info["transport"]]},
         }
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(mesh, 50)
+            out["cpu_baseline"] = cpu_baseline(mesh, 50, args.h2)
         print(json.dumps(out), flush=True)
     nek.free(ctx)
     if dist:

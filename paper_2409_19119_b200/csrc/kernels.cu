@@ -994,7 +994,9 @@ struct AxV5Smem {
     int last;
 };
 
-template <bool HELM, bool FUSED, int MINB, bool L2PF = false>
+// TMAG: the 24 KB metric block of the element two ahead is brought into a 2-stage
+// shared-memory ring by one TMA bulk copy while this element computes (dynamic smem).
+template <bool HELM, bool FUSED, int MINB, bool L2PF = false, bool TMAG = false>
 __global__ void __launch_bounds__(128, MINB)
     ax_v5_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *u,
                  const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
@@ -1006,6 +1008,8 @@ __global__ void __launch_bounds__(128, MINB)
     constexpr int P3 = 512, N = 7;
     if (done && *(volatile const int *)done) return;
     __shared__ AxV5Smem S;
+    extern __shared__ __align__(128) double gstage[];          // TMAG: [2][6 * 512]
+    __shared__ uint64_t gfull[2];
     double beta = 0.0, alpha = 0.0;
     if (FUSED) { beta = sc->beta; alpha = sc->alpha; }
     const int t = threadIdx.x, lane = t & 31, wq = t >> 5, q = lane & 3, r = lane >> 2;
@@ -1019,6 +1023,28 @@ __global__ void __launch_bounds__(128, MINB)
         As[s2] = S.sD[r * 8 + 4 * s2 + q];       // s fwd   A(r, K=(s,q))   = D(j_out=r, m=4s+q)
         Bt[s2] = S.sD[(2 * q + s2) * 8 + r];     // r trans B(K=(s,q), n=r) = D(i=2q+s, i'=r)
         Ast[s2] = S.sD[(4 * s2 + q) * 8 + r];    // s trans A(r, K=(s,q))   = D(j=4s+q, j'=r)
+    }
+    auto elem_at = [&](int64_t it) -> int64_t {
+        const int64_t pos = eoff + blockIdx.x + it * (int64_t)gridDim.x;
+        return elist ? (int64_t)elist[pos] : pos;
+    };
+    auto g_issue = [&](int64_t it, int st) {
+        tma::fence_proxy_async();
+        tma::mbar_arrive_expect_tx(&gfull[st], 6 * P3 * 8);
+        tma::bulk_g2s(gstage + st * 6 * P3, G + elem_at(it) * 6 * (int64_t)P3, 6 * P3 * 8, &gfull[st],
+                      tma::policy_evict_first());
+    };
+    if (TMAG) {
+        if (t == 0) {
+            tma::mbar_init(&gfull[0], 1);
+            tma::mbar_init(&gfull[1], 1);
+            tma::fence_mbar_init();
+        }
+        __syncthreads();
+        if (t == 0) {
+            if (nit > 0) g_issue(0, 0);
+            if (nit > 1) g_issue(1, 1);
+        }
     }
     const int kb = 2 * wq;                       // this warp's first k-slab
     double dot = 0.0;
@@ -1065,9 +1091,11 @@ __global__ void __launch_bounds__(128, MINB)
                 *reinterpret_cast<double2 *>(xvec + l) = xv;
                 *reinterpret_cast<double2 *>(&S.sU[par][kb + kk][r][2 * q]) = pn;
                 uk[kk] = pn;
+                if (!TMAG) {
 #pragma unroll
-                for (int a = 0; a < 6; ++a)
-                    Gv[kk][a] = *reinterpret_cast<const double2 *>(Ge + a * P3 + 64 * (kb + kk) + 8 * r + 2 * q);
+                    for (int a = 0; a < 6; ++a)
+                        Gv[kk][a] = *reinterpret_cast<const double2 *>(Ge + a * P3 + 64 * (kb + kk) + 8 * r + 2 * q);
+                }
             }
             __syncthreads();
 #pragma unroll
@@ -1085,9 +1113,11 @@ __global__ void __launch_bounds__(128, MINB)
             uk[kk] = *reinterpret_cast<const double2 *>(ue + 64 * k + 8 * r + 2 * q);
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) ub[kk][s2] = ue[64 * k + 8 * (4 * s2 + q) + r];
+            if (!TMAG) {
 #pragma unroll
-            for (int a = 0; a < 6; ++a)
-                Gv[kk][a] = *reinterpret_cast<const double2 *>(Ge + a * P3 + 64 * k + 8 * r + 2 * q);
+                for (int a = 0; a < 6; ++a)
+                    Gv[kk][a] = *reinterpret_cast<const double2 *>(Ge + a * P3 + 64 * k + 8 * r + 2 * q);
+            }
         }
         if (mbits) {
             // own point (i=2q+v, j=r, k): word 2k + (r >> 2), bit 8 (r & 3) + 2q + v
@@ -1111,6 +1141,16 @@ __global__ void __launch_bounds__(128, MINB)
                 }
             }
         }
+        }
+        if (TMAG) {
+            const int st = (int)(it & 1);
+            tma::mbar_wait(&gfull[st], (uint32_t)((it >> 1) & 1));
+            const double *sg = gstage + st * 6 * P3;
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                for (int a = 0; a < 6; ++a)
+                    Gv[kk][a] = *reinterpret_cast<const double2 *>(sg + a * P3 + 64 * (kb + kk) + 8 * r + 2 * q);
         }
         double2 acc[2];
 #pragma unroll
@@ -1152,7 +1192,8 @@ __global__ void __launch_bounds__(128, MINB)
             acc[kk].x += ws0;
             acc[kk].y += ws1;
         }
-        __syncthreads();                         // sGT[par] complete
+        __syncthreads();                         // sGT[par] complete (and every G read of this element done)
+        if (TMAG && t == 0 && it + 2 < nit) g_issue(it + 2, (int)(it & 1));
         double2 gtl[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) gtl[m] = *reinterpret_cast<const double2 *>(&S.sGT[par][m][r][2 * q]);
@@ -1192,27 +1233,38 @@ __global__ void __launch_bounds__(128, MINB)
     }
 }
 
-template <bool HELM, int MINB, bool L2PF = false>
+template <bool HELM, int MINB, bool L2PF = false, bool TMAG = false>
 static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
                                 const uint32_t *mbits, double h1, double h2, double *w, int64_t grid, cudaStream_t s)
 {
+    const size_t dsm = TMAG ? 2 * 6 * 512 * sizeof(double) : 0;
+    if (TMAG) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(ax_v5_kernel<HELM, true, MINB, L2PF, TMAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dsm);
+            cudaFuncSetAttribute(ax_v5_kernel<HELM, false, MINB, L2PF, TMAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dsm);
+            attr = true;
+        }
+    }
     if (L.fused)
-        ax_v5_kernel<HELM, true, MINB, L2PF><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
+        ax_v5_kernel<HELM, true, MINB, L2PF, TMAG><<<(unsigned)grid, 128, dsm, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
                                                                  L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                  L.done, L.p, L.x, L.r, L.dinv, L.sc, L.mail,
                                                                  L.ctas_total ? L.ctas_total : (unsigned)grid);
     else
-        ax_v5_kernel<HELM, false, MINB, L2PF><<<(unsigned)grid, 128, 0, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
+        ax_v5_kernel<HELM, false, MINB, L2PF, TMAG><<<(unsigned)grid, 128, dsm, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
                                                                   L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                   L.done, nullptr, nullptr, nullptr, nullptr, nullptr,
                                                                   L.mail, L.ctas_total ? L.ctas_total : (unsigned)grid);
     return cudaGetLastError();
 }
 
-bool ax_has_fused(int variant, int N) { return (variant == 0 || variant == 8 || variant == 9) && N == 7; }
+bool ax_has_fused(int variant, int N) { return (variant == 0 || variant == 8 || variant == 9 || variant == 10) && N == 7; }
 
 // variant (N = 7): 0 = default (v5, DMMA, k-slabs, 4 CTAs/SM), 8 = v5 at 3 CTAs/SM,
-// 9 = v5 + L2 bulk prefetch of the next element, 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
+// 9 = v5 + L2 bulk prefetch of the next element, 10 = v5 + TMA ring for G (3 CTAs/SM), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
 // 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups, 6 = v3 with 1 k-group, 7 = v4 (DMMA, j-slabs)
 static int per_sm_of(int variant)
 {
@@ -1220,6 +1272,7 @@ static int per_sm_of(int variant)
     case 0: return 4;
     case 8: return 3;
     case 9: return 4;
+    case 10: return 3;
     case 7: return 3;
     case 6: return 6;
     case 2: return 3;
@@ -1288,12 +1341,15 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         return h2 != 0.0 ? ax_v2_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                          : ax_v2_launch<false, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
     }
-    if (N == 7 && (variant == 0 || variant == 8 || variant == 9)) {
+    if (N == 7 && (variant == 0 || variant == 8 || variant == 9 || variant == 10)) {
         if (nlaunch) ++*nlaunch;
         const int64_t grid = ax_grid(variant, N, L.nelem);
         if (variant == 9)
             return h2 != 0.0 ? ax_v5_launch<true, 4, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 4, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+        if (variant == 10)
+            return h2 != 0.0 ? ax_v5_launch<true, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                             : ax_v5_launch<false, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
         if (variant == 0)
             return h2 != 0.0 ? ax_v5_launch<true, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s);

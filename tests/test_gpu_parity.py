@@ -246,7 +246,7 @@ def test_config2_full_size(nek):
         nek.free(ctx)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10])
 def test_ax_all_variants_N7(nek, variant):
     """Every Ax kernel variant (nek_set_variant) against the oracle, Poisson and Helmholtz."""
     m = mg.box_mesh(3, 4, 5, 7, deform="bubble")
@@ -296,3 +296,35 @@ def test_pcg_bitwise_repeatable_and_gs_inline_equivalent(nek):
     x0, it0, h0 = outs[0]
     for x, it, h in outs[1:]:
         assert it == it0 and np.array_equal(x, x0) and np.array_equal(h, h0)
+
+
+@pytest.mark.parametrize("N,dirichlet", [(7, "pins_walls"), (5, "outlet"), (3, "pins_walls")])
+def test_rod_bundle_parity(nek, N, dirichlet):
+    """Curved rod-bundle mesh (config 4 shape, 2x2 pins): multiplicities up to 16."""
+    m = mg.rod_bundle(2, 2, 2, N, dirichlet=dirichlet)
+    O = oracle.Oracle.from_mesh(m)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        perm, offs = nek.get_gs_map(ctx)
+        assert np.array_equal(perm, O.gs.perm) and np.array_equal(offs, O.gs.offs)
+        G, wJ = nek.get_geom(ctx)
+        assert rel(G, O.G) <= 1e-12 and rel(wJ, O.wJ) <= 1e-12
+        u = mg.random_evector(m, seed=4)
+        v = u.copy()
+        nek.gs(ctx, v)
+        assert np.array_equal(v, O.gs_apply(u))
+        for h in ((1.0, 0.0), (1.0, 100.0)):
+            w = np.empty(m.n_local)
+            nek.ax(ctx, h[0], h[1], u, w)
+            assert rel(w, O.apply(h[0], h[1], u)) <= 1e-12
+        h = (1.0, 100.0) if dirichlet == "pins_walls" else (1.0, 0.0)
+        b = mg.smooth_field(m, seed=5)
+        _, kconv, _, _ = O.pcg(h[0], h[1], b, 1e-11, 100)
+        win = min(60, kconv)
+        xo, ito, _, ho = O.pcg(h[0], h[1], b, 0.0, win)
+        x = np.zeros(m.n_local)
+        st, it, _, hg = nek.pcg_solve(ctx, h[0], h[1], b, x, 0.0, win, want_hist=True)
+        assert it == ito and np.all(np.abs(hg - ho) <= O.hist_tolerance(h[0], h[1], b, win))
+        assert rel(x, xo) <= 1e-9
+    finally:
+        nek.free(ctx)

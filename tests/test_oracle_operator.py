@@ -255,3 +255,23 @@ def test_gs_multi_rank_equals_single(parts):
     for e, o in zip(P, outi):
         fulli[(e[:, None] * 64 + np.arange(64)).reshape(-1)] = o
     assert np.array_equal(fulli, oracle.Oracle.from_mesh(m).gs_apply(iv))
+
+
+def test_rod_bundle_mesh_and_operator():
+    """Config-4-like curved rod-bundle mesh (reading 13): conforming (copies share coordinates),
+    positive Jacobians, volume = cell squares minus pins up to the isoparametric circle error,
+    multiplicities up to 16, A.1 = 0 and symmetry on curved elements."""
+    m = mg.rod_bundle(2, 2, 2, 4)
+    O = oracle.Oracle.from_mesh(m)
+    mult = np.bincount(oracle.multiplicity(m.gid))
+    assert mult.size == 17 and mult[16] > 0
+    exact = 4 * 1.26 ** 2 * 2 * 1.26 - 4 * np.pi * 0.475 ** 2 * 2 * 1.26
+    assert abs(O.wJ.sum() - exact) < 1e-5 * exact and O.wJ.min() > 0
+    one = np.ones(m.n_local)
+    scale = np.abs(O.ax_local(1.0, 0.0, mg.smooth_field(m, 3, masked=False))).max()
+    assert np.abs(O.gs_apply(O.ax_local(1.0, 0.0, one))).max() <= 1e-13 * scale
+    x, y = mg.smooth_field(m, 1), mg.smooth_field(m, 2)
+    assert abs(O.dot(y, O.apply(1.0, 2.0, x)) - O.dot(x, O.apply(1.0, 2.0, y))) <= 1e-12 * abs(O.dot(x, O.apply(1.0, 2.0, x)))
+    # slabs of layers generate the same ids as the whole column
+    top = mg.rod_bundle(2, 2, 1, 4, z0_layer=1, nlayers_total=2)
+    assert np.isin(top.gid, m.gid).all()

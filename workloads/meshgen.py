@@ -257,3 +257,89 @@ def config_mesh(cfg: int, **kw) -> Mesh:
     if cfg == 3:   # 32x64x64, N=7
         return box_mesh(32, 64, 64, 7, deform="bubble", eps=0.05, dirichlet="all", **kw)
     raise ValueError(cfg)
+
+
+# ------------------------------------------------------------- rod bundle
+def rod_bundle(npx: int = 17, npy: int = 17, nlayers: int = 3, N: int = 7, pitch: float = 1.26,
+               radius: float = 0.475, ntheta: int = 4, nrad: int = 6, dz: float = None,
+               dirichlet: str = "pins_walls", z0_layer: int = 0, nlayers_total: int = None) -> Mesh:
+    """Rod-bundle-like curved hex mesh (BASELINE config 4, reading 13): npx x npy pin
+    cells of side `pitch`, each an O-grid of 4 side blocks x (ntheta x nrad) elements between the
+    pin circle of `radius` and the cell square, blended radially; extruded in z by `nlayers`
+    element layers (layers z0_layer .. z0_layer+nlayers-1 of nlayers_total).  GLL nodes are placed
+    through the analytic map (curved elements); node ids come from coordinate hashing and every
+    copy of a node gets the coordinates of its first occurrence (bit-identical copies).
+
+    dirichlet: "pins_walls" (pin surfaces, outer walls, inlet z = 0: velocity-shaped),
+               "outlet" (top plane only: pressure-shaped), "none"."""
+    if dz is None:
+        dz = pitch
+    if nlayers_total is None:
+        nlayers_total = z0_layer + nlayers
+    Nq = N + 1
+    xi = gll_points(N)
+    h = 0.5 * pitch
+    dth = 0.5 * np.pi / ntheta
+    R, S = np.meshgrid(xi, xi, indexing="xy")          # R[j, i] = xi_i, S[j, i] = xi_j
+    # all cross-section elements at once, ordered (cy, cx, blk, c, a)
+    cyv, cxv, bv, cv, av = np.meshgrid(np.arange(npy), np.arange(npx), np.arange(4), np.arange(nrad),
+                                       np.arange(ntheta), indexing="ij")
+    cyv, cxv, bv, cv, av = (v.reshape(-1, 1, 1) for v in (cyv, cxv, bv, cv, av))
+    ox, oy = (cxv + 0.5) * pitch, (cyv + 0.5) * pitch
+    th0 = -0.25 * np.pi + bv * 0.5 * np.pi
+    # i (r) runs outward from the pin, j (s) counter-clockwise: right-handed with z
+    th = th0 + (av + 0.5 * (S[None] + 1.0)) * dth
+    srad = (cv + 0.5 * (R[None] + 1.0)) / nrad
+    cth, sth = np.cos(th), np.sin(th)
+    mm = np.maximum(np.abs(cth), np.abs(sth))
+    PX = ox + (1.0 - srad) * radius * cth + srad * h * cth / mm
+    PY = oy + (1.0 - srad) * radius * sth + srad * h * sth / mm
+    els_xyz = [(PX[e], PY[e]) for e in range(PX.shape[0])]
+    nE2 = len(els_xyz)
+    E = nE2 * nlayers
+    P3 = Nq ** 3
+    # cross-section ids by coordinate hashing (tolerance far below the node spacing, far above
+    # rounding); every rank builds the same cross-section, so the ids agree across ranks
+    pts2 = np.stack([PX.reshape(PX.shape[0], -1), PY.reshape(PY.shape[0], -1)], 1)   # (nE2, 2, Nq^2)
+    flat = pts2.transpose(1, 0, 2).reshape(2, -1)
+    tol = 1e-7 * pitch
+    key = np.round(flat / tol).astype(np.int64)
+    _, first, inv = np.unique(key.T, axis=0, return_index=True, return_inverse=True)
+    inv = inv.reshape(-1)
+    flat = flat[:, first[inv]]                                              # bit-identical copies
+    xy_id = inv.reshape(nE2, Nq * Nq)
+    pts2 = flat.reshape(2, nE2, Nq * Nq)
+    NZ = nlayers_total * N + 1
+    xyz = np.empty((3, E * P3))
+    gid = np.empty(E * P3, np.int64)
+    zt = 0.5 * (xi + 1.0)
+    for L in range(nlayers):
+        Lg = z0_layer + L
+        zl = (Lg + zt) * dz
+        sl = slice(L * nE2 * P3, (L + 1) * nE2 * P3)
+        xyz[0, sl] = np.broadcast_to(pts2[0][:, None, :], (nE2, Nq, Nq * Nq)).reshape(-1)
+        xyz[1, sl] = np.broadcast_to(pts2[1][:, None, :], (nE2, Nq, Nq * Nq)).reshape(-1)
+        xyz[2, sl] = np.broadcast_to(zl[None, :, None], (nE2, Nq, Nq * Nq)).reshape(-1)
+        K = Lg * N + np.arange(Nq)
+        gid[sl] = (xy_id[:, None, :].astype(np.int64) * NZ + K[None, :, None]).reshape(-1)
+    x, y, zz = xyz
+    ccx = np.clip(np.floor(x / pitch), 0, npx - 1)
+    ccy = np.clip(np.floor(y / pitch), 0, npy - 1)
+    on_pin = np.abs(np.hypot(x - (ccx + 0.5) * pitch, y - (ccy + 0.5) * pitch) - radius) < 1e-9
+    walls = (np.abs(x) < 1e-9) | (np.abs(x - npx * pitch) < 1e-9) | (np.abs(y) < 1e-9) | \
+        (np.abs(y - npy * pitch) < 1e-9)
+    inlet = np.abs(zz) < 1e-9
+    outlet = np.abs(zz - nlayers_total * dz) < 1e-9
+    if dirichlet == "pins_walls":
+        mask = on_pin | walls | inlet
+    elif dirichlet == "outlet":
+        mask = outlet
+    elif dirichlet == "none":
+        mask = np.zeros(E * P3, bool)
+    else:
+        raise ValueError(dirichlet)
+    elem = np.zeros((E, 3), np.int64)
+    elem[:, 2] = np.repeat(np.arange(nlayers) + z0_layer, nE2)
+    Lx, Ly, Lz = npx * pitch, npy * pitch, nlayers_total * dz
+    return Mesh(E=E, N=N, xyz=xyz, gid=gid, mask=mask.astype(np.uint8), elem=elem, shape=(npx, npy, nlayers_total),
+                extent=(Lx, Ly, Lz), deform="rod", eps=0.0)
