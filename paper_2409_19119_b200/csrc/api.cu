@@ -191,7 +191,7 @@ static int halo_start(nek_ctx *ctx, const double *v, const int *done, cudaStream
         Scope sc(ctx, CLS_HALO, strm);
         CK(launch_gs_pack_p2p_fused(ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots, ctx->send_run,
                                     ctx->d_slot_nbr, ctx->d_peer_recv, ctx->d_remote_off, ctx->d_send_offs,
-                                    ctx->nslots, (int)ctx->neighbors.size(), ctx->rank, ctx->d_peer_hflags,
+                                    ctx->d_remote_half, (int)ctx->neighbors.size(), ctx->rank, ctx->d_peer_hflags,
                                     ctx->epochs, ctx->counter + 3, done, strm));
         ctx->stats.launches += 1;
         ctx->stats.halo_launches += 1;
@@ -219,15 +219,6 @@ static int halo_start(nek_ctx *ctx, const double *v, const int *done, cudaStream
 
 static int halo_finish(nek_ctx *ctx, double *v, const int *done)
 {
-    if (ctx->p2p) {
-        Scope sc(ctx, CLS_HALO);
-        CK(launch_gs_wait_p2p((int)ctx->neighbors.size(), ctx->d_nbr, ctx->hflags, ctx->epochs, ctx->p2p_err,
-                              ctx->s_main));
-        CK(launch_gs_ifc_unpack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, ctx->coffs, ctx->contrib, ctx->ifc_partial,
-                                ctx->recv2, v, done, ctx->s_main, ctx->epochs + 3, ctx->nslots));
-        ctx->stats.launches += 1 + (ctx->nifc > 0);
-        return NEK_OK;
-    }
     CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_join, 0));
     Scope sc(ctx, CLS_HALO);
     CK(launch_gs_ifc_unpack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, ctx->coffs, ctx->contrib, ctx->ifc_partial,
@@ -252,7 +243,7 @@ static int gs_local_and_unpack_p2p(nek_ctx *ctx, double *v, const int *done, boo
     HaloUnpack U;
     U.nifc = ctx->nifc; U.perm = ctx->ifc_perm; U.offs = ctx->ifc_offs; U.coffs = ctx->coffs;
     U.contrib = ctx->contrib; U.nbr = ctx->d_nbr; U.partial = ctx->ifc_partial; U.recv = ctx->recv2;
-    U.half = ctx->nslots; U.hflags = ctx->hflags; U.epochs = ctx->epochs; U.nnbr = (int)ctx->neighbors.size();
+    U.half = std::max<int64_t>(ctx->nslots, 1); U.hflags = ctx->hflags; U.epochs = ctx->epochs; U.nnbr = (int)ctx->neighbors.size();
     U.err = ctx->p2p_err;
     CK(launch_gs_classes_unpack(skip_local ? GsClasses() : ctx->gsc, U, v, done, ctx->s_main));
     ctx->stats.gs_launches += 1;
@@ -396,9 +387,9 @@ static int setup_p2p(nek_ctx *ctx)
     CK(cudaMemset(ctx->epochs, 0, sizeof(uint64_t) * 4));
     CK(dalloc(ctx, &ctx->p2p_err, 1));
     CK(cudaMemset(ctx->p2p_err, 0, sizeof(int)));
-    // per-rank record: 3 IPC handles + offsets of my data in every rank's receive buffer (-1: not a neighbour)
-    struct Rec { cudaIpcMemHandle_t hm, hr, hf; int64_t off[1]; };
-    const size_t rec_bytes = sizeof(cudaIpcMemHandle_t) * 3 + sizeof(int64_t) * P;
+    // per-rank record: 3 IPC handles, offsets of every rank's data in MY receive buffer (-1: not a
+    // neighbour), and my receive-buffer half size (the buffer is double-buffered by epoch parity)
+    const size_t rec_bytes = sizeof(cudaIpcMemHandle_t) * 3 + sizeof(int64_t) * (P + 1);
     std::vector<unsigned char> mine(rec_bytes, 0), all(rec_bytes * P, 0);
     cudaIpcMemHandle_t h[3];
     if (cudaIpcGetMemHandle(&h[0], ctx->mbox) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->recv2) != cudaSuccess ||
@@ -410,6 +401,8 @@ static int setup_p2p(nek_ctx *ctx)
     std::vector<int64_t> offs(P, -1);   // where neighbour q's data lands in MY receive buffer
     for (int k = 0; k < nn; ++k) offs[ctx->neighbors[k]] = ctx->send_offs[k];
     std::memcpy(mine.data() + sizeof(h), offs.data(), sizeof(int64_t) * P);
+    const int64_t my_half = std::max<int64_t>(ctx->nslots, 1);
+    std::memcpy(mine.data() + sizeof(h) + sizeof(int64_t) * P, &my_half, sizeof(int64_t));
     unsigned char *dbuf = nullptr;
     CK(cudaMalloc(&dbuf, rec_bytes * (P + 1)));
     CK(cudaMemcpy(dbuf + rec_bytes * P, mine.data(), rec_bytes, cudaMemcpyHostToDevice));
@@ -452,14 +445,16 @@ static int setup_p2p(nek_ctx *ctx)
     // device-side tables
     std::vector<double *> nrecv(nn);
     std::vector<uint64_t *> nflag(nn);
-    std::vector<int64_t> roff(nn);
+    std::vector<int64_t> roff(nn), rhalf(nn);
     for (int k = 0; k < nn; ++k) {
         const int q = ctx->neighbors[k];
         nrecv[k] = pr[q];
         nflag[k] = pf[q];
-        int64_t o;
+        int64_t o, hq;
         std::memcpy(&o, all.data() + rec_bytes * q + sizeof(h) + sizeof(int64_t) * me, sizeof(int64_t));
+        std::memcpy(&hq, all.data() + rec_bytes * q + sizeof(h) + sizeof(int64_t) * P, sizeof(int64_t));
         roff[k] = o;
+        rhalf[k] = hq;   // the neighbour's half size, not ours
     }
     std::vector<int32_t> slot_nbr(ctx->nslots), nbr32(ctx->neighbors.begin(), ctx->neighbors.end());
     for (int k = 0; k < nn; ++k)
@@ -468,6 +463,7 @@ static int setup_p2p(nek_ctx *ctx)
     CK(upload(ctx, &ctx->d_peer_recv, nrecv));
     CK(upload(ctx, &ctx->d_peer_hflags, nflag));
     CK(upload(ctx, &ctx->d_remote_off, roff));
+    CK(upload(ctx, &ctx->d_remote_half, rhalf));
     CK(upload(ctx, &ctx->d_send_offs, ctx->send_offs));
     CK(upload(ctx, &ctx->d_slot_nbr, slot_nbr));
     CK(upload(ctx, &ctx->d_nbr, nbr32));
@@ -717,6 +713,7 @@ int nek_free(nek_ctx *ctx)
     for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     for (void *p : {(void *)ctx->mbox, (void *)ctx->d_peer_mbox, (void *)ctx->epochs, (void *)ctx->p2p_err,
                     (void *)ctx->recv2, (void *)ctx->d_peer_recv, (void *)ctx->d_remote_off, (void *)ctx->d_send_offs,
+                    (void *)ctx->d_remote_half,
                     (void *)ctx->d_slot_nbr, (void *)ctx->d_nbr, (void *)ctx->hflags, (void *)ctx->d_peer_hflags})
         if (p) cudaFree(p);
     if (ctx->sc_host) cudaFreeHost(ctx->sc_host);

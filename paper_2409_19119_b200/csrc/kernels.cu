@@ -2132,40 +2132,6 @@ cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *r
     return cudaGetLastError();
 }
 
-// halo: interface partials straight into the neighbours' receive buffers
-// (double-buffered by epoch parity), then one flag per neighbour set by the
-// last CTA to finish.
-__global__ void gs_pack_p2p_kernel(int64_t nslots, const int32_t *__restrict__ send_run,
-                                   const int32_t *__restrict__ slot_nbr, const double *__restrict__ partial,
-                                   double *const *peer_recv, const int64_t *__restrict__ remote_off,
-                                   const int64_t *__restrict__ send_offs, int64_t recv_half, int nnbr, int me,
-                                   uint64_t *const *peer_hflags, uint64_t *epochs, unsigned int *counter,
-                                   const int *done)
-{
-    __shared__ int s_last;
-    const uint64_t e = epochs[2] + 1;           // this exchange's epoch (bumped by the last CTA)
-    const int64_t half = (int64_t)(e & 1) * recv_half;
-    if (!(done && *(volatile const int *)done)) {
-        for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < nslots;
-             sidx += (int64_t)gridDim.x * blockDim.x) {
-            const int k = slot_nbr[sidx];
-            peer_recv[k][half + remote_off[k] + (sidx - send_offs[k])] = partial[send_run[sidx]];
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        *counter = 0u;
-        epochs[2] = e;
-        __threadfence_system();
-        for (int k = 0; k < nnbr; ++k) st_release_sys(peer_hflags[k] + me, e);
-    }
-}
-
 // pack with the interface partials folded in (one thread per send slot; a run
 // shared with several neighbours is folded once per slot, same bits)
 __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restrict__ perm,
@@ -2173,12 +2139,13 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
                                          double *__restrict__ partial, const int32_t *__restrict__ send_run,
                                          const int32_t *__restrict__ slot_nbr, double *const *peer_recv,
                                          const int64_t *__restrict__ remote_off, const int64_t *__restrict__ send_offs,
-                                         int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags,
-                                         uint64_t *epochs, unsigned int *counter, const int *done)
+                                         const int64_t *__restrict__ remote_half, int nnbr, int me,
+                                         uint64_t *const *peer_hflags, uint64_t *epochs, unsigned int *counter,
+                                         const int *done)
 {
     __shared__ int s_last;
     const uint64_t e = epochs[2] + 1;
-    const int64_t half = (int64_t)(e & 1) * recv_half;
+    const int64_t par = (int64_t)(e & 1);   // receive half by epoch parity, in units of the NEIGHBOUR's half size
     if (!(done && *(volatile const int *)done)) {
         for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < nslots;
              sidx += (int64_t)gridDim.x * blockDim.x) {
@@ -2188,7 +2155,7 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
             for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
             partial[run] = s;
             const int k = slot_nbr[sidx];
-            peer_recv[k][half + remote_off[k] + (sidx - send_offs[k])] = s;
+            peer_recv[k][par * remote_half[k] + remote_off[k] + (sidx - send_offs[k])] = s;
         }
     }
     __syncthreads();
@@ -2208,44 +2175,15 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
 cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const double *v, double *partial,
                                      int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
                                      double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
-                                     int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags,
+                                     const int64_t *remote_half, int nnbr, int me, uint64_t *const *peer_hflags,
                                      uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s)
 {
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + 255) / 256, 296));
     gs_pack_p2p_fused_kernel<<<blocks, 256, 0, s>>>(nslots, perm, offs, v, partial, send_run, slot_nbr, peer_recv,
-                                                    remote_off, send_offs, recv_half, nnbr, me, peer_hflags, epochs,
+                                                    remote_off, send_offs, remote_half, nnbr, me, peer_hflags, epochs,
                                                     counter, done);
     return cudaGetLastError();
 }
 
-cudaError_t launch_gs_pack_p2p(int64_t nifc, const int32_t *perm, const int32_t *offs, const double *v,
-                               double *partial, int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
-                               double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
-                               int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags, uint64_t *epochs,
-                               unsigned int *counter, const int *done, cudaStream_t s)
-{
-    if (nifc > 0) gs_ifc_partial_kernel<<<(unsigned)((nifc + 255) / 256), 256, 0, s>>>(nifc, perm, offs, v, partial, done);
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + 255) / 256, 148));
-    gs_pack_p2p_kernel<<<blocks, 256, 0, s>>>(nslots, send_run, slot_nbr, partial, peer_recv, remote_off, send_offs,
-                                              recv_half, nnbr, me, peer_hflags, epochs, counter, done);
-    return cudaGetLastError();
-}
-
-// wait until every neighbour's halo of this epoch has landed
-__global__ void gs_wait_p2p_kernel(int nnbr, const int32_t *__restrict__ nbr, const uint64_t *hflags, uint64_t *epochs,
-                                   int *err)
-{
-    __shared__ uint64_t s_e;
-    if (threadIdx.x == 0) s_e = ++epochs[3];
-    __syncthreads();
-    for (int k = threadIdx.x; k < nnbr; k += blockDim.x) wait_epoch(hflags + nbr[k], s_e, err);
-}
-
-cudaError_t launch_gs_wait_p2p(int nnbr, const int32_t *nbr, const uint64_t *hflags, uint64_t *epochs, int *err,
-                               cudaStream_t s)
-{
-    gs_wait_p2p_kernel<<<1, 32, 0, s>>>(nnbr, nbr, hflags, epochs, err);
-    return cudaGetLastError();
-}
 
 }  // namespace nekb200

@@ -139,18 +139,12 @@ bool ax_has_fused(int variant, int N);
 // NVLink peer-memory exchange (CUDA IPC mappings; see kernels.cu)
 cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *red_loc, double *red_all, double *mbox,
                                 double *const *peer_mbox, uint64_t *epochs, int *err, cudaStream_t s);
-cudaError_t launch_gs_pack_p2p(int64_t nifc, const int32_t *perm, const int32_t *offs, const double *v,
-                               double *partial, int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
-                               double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
-                               int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags, uint64_t *epochs,
-                               unsigned int *counter, const int *done, cudaStream_t s);
 cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const double *v, double *partial,
                                      int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
                                      double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
-                                     int64_t recv_half, int nnbr, int me, uint64_t *const *peer_hflags,
+                                     const int64_t *remote_half, int nnbr, int me, uint64_t *const *peer_hflags,
                                      uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s);
-cudaError_t launch_gs_wait_p2p(int nnbr, const int32_t *nbr, const uint64_t *hflags, uint64_t *epochs, int *err,
-                               cudaStream_t s);
+
 cudaError_t launch_pcg_init_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_update(int64_t n, const uint32_t *obits, const double *dinv, const double *p,
                               const double *w, double *x, double *r, const double *red_all, int nranks,
@@ -223,7 +217,7 @@ struct nek_ctx {
     int *p2p_err = nullptr;
     double *recv2 = nullptr;                // 2 x nslots halo receive buffer (P2P)
     double **d_peer_recv = nullptr;         // [nnbr]
-    int64_t *d_remote_off = nullptr, *d_send_offs = nullptr;
+    int64_t *d_remote_off = nullptr, *d_send_offs = nullptr, *d_remote_half = nullptr;
     int32_t *d_slot_nbr = nullptr, *d_nbr = nullptr;
     uint64_t *hflags = nullptr;             // [nranks], written by neighbours
     uint64_t **d_peer_hflags = nullptr;     // [nnbr]
