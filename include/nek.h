@@ -149,6 +149,30 @@ int nek_free(nek_ctx *ctx);
 /* Message of the context's last failure ("" if none).  Valid until the next call. */
 const char *nek_errmsg(const nek_ctx *ctx);
 
+/* ------------------------------------------------ projection initial guess */
+/*
+ * Fischer's projection onto prior solutions (P:513-519
+ * "generate an initial guess ... by projecting onto the space of prior
+ * solutions", "increasing the number of prior solutions from 8 to 30";
+ * S:344-347).  A space holds up to max_vectors (<= 32)
+ * A-orthonormal vectors x_i and their images A x_i (2 * max_vectors E-vectors
+ * of device memory).  nek_proj_solve(b):
+ *   alpha_i = <x_i, M b>; xbar = sum alpha_i x_i; db = M b - sum alpha_i A x_i;
+ *   Jacobi-PCG on A dx = db to ||r|| <= tol ||M b||; x = xbar + dx;
+ *   then dx is A-orthonormalised against the space (classical Gram-Schmidt,
+ *   twice) and appended; when the space is full it restarts from x alone.
+ * The space is reset when (h1, h2) changes.  iters = PCG iterations on db;
+ * relres = ||r|| / ||M b||.  Collective for nranks > 1.  Status as
+ * nek_pcg_solve.  max_vectors = 0 gives plain PCG.
+ */
+typedef struct nek_proj nek_proj;
+int nek_proj_create(nek_ctx *ctx, int max_vectors, nek_proj **out);
+int nek_proj_solve(nek_proj *proj, double h1, double h2, const double *b, double *x, double tol, int maxit,
+                   int *iters, double *relres, void *stream);
+int nek_proj_size(const nek_proj *proj);      /* vectors currently in the space */
+int nek_proj_reset(nek_proj *proj);
+int nek_proj_free(nek_proj *proj);
+
 /* ----------------------------------------------------------- introspection */
 typedef struct {
     int64_t E;                 /* local elements                                   */

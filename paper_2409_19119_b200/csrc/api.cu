@@ -1037,3 +1037,184 @@ int nek_set_variant(nek_ctx *ctx, int v)
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ projection
+struct nek_proj {
+    nek_ctx *ctx = nullptr;
+    int L = 0, l = 0;
+    bool hvalid = false;
+    double h1 = 0, h2 = 0;
+    double *X = nullptr, *B = nullptr;          // [L][n]
+    double *xbar = nullptr, *db = nullptr, *dx = nullptr, *v = nullptr, *av = nullptr, *bm = nullptr;
+    double *coef = nullptr, *part = nullptr, *gath = nullptr;
+    int nblk = 296;
+};
+
+// global owner-copy dot products <V_i, y> for i < l, returned on the host (rank-ordered across ranks)
+static int proj_dots(nek_proj *P, int l, const double *V, const double *y, double *out)
+{
+    nek_ctx *ctx = P->ctx;
+    if (l <= 0) return NEK_OK;
+    CK(launch_multidot(ctx->n, l, V, y, ctx->obits, P->part, P->nblk, ctx->s_main));
+    ctx->stats.launches += 1;
+    std::vector<double> hp((size_t)P->nblk * l);
+    CK(cudaMemcpyAsync(hp.data(), P->part, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, ctx->s_main));
+    CK(cudaStreamSynchronize(ctx->s_main));
+    for (int i = 0; i < l; ++i) {
+        double s = 0.0;
+        for (int b = 0; b < P->nblk; ++b) s += hp[(size_t)b * l + i];
+        out[i] = s;
+    }
+    if (ctx->nranks > 1) {
+        CK(cudaMemcpyAsync(P->gath + (size_t)ctx->nranks * PROJ_MAX_VECTORS, out, sizeof(double) * l,
+                           cudaMemcpyHostToDevice, ctx->s_main));
+        NK(ncclAllGather(P->gath + (size_t)ctx->nranks * PROJ_MAX_VECTORS, P->gath, (size_t)l, ncclDouble, ctx->nccl,
+                         ctx->s_main));
+        std::vector<double> all((size_t)ctx->nranks * l);
+        CK(cudaMemcpyAsync(all.data(), P->gath, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, ctx->s_main));
+        CK(cudaStreamSynchronize(ctx->s_main));
+        for (int i = 0; i < l; ++i) {
+            double s = all[i];
+            for (int q = 1; q < ctx->nranks; ++q) s += all[(size_t)q * l + i];
+            out[i] = s;
+        }
+    }
+    return NEK_OK;
+}
+
+extern "C" int nek_proj_create(nek_ctx *ctx, int max_vectors, nek_proj **out)
+{
+    if (!ctx || !out || max_vectors < 0 || max_vectors > PROJ_MAX_VECTORS)
+        return fail(ctx, NEK_EINVAL, "max_vectors must be in [0, 32]");
+    *out = nullptr;
+    CK(cudaSetDevice(ctx->device));
+    nek_proj *P = new (std::nothrow) nek_proj();
+    if (!P) return fail(ctx, NEK_ENOMEM, "host allocation failed");
+    P->ctx = ctx; P->L = max_vectors;
+    const int64_t n = std::max<int64_t>(ctx->n, 1);
+    int st = NEK_OK;
+    auto al = [&](double **p, int64_t cnt) {
+        if (st != NEK_OK) return;
+        if (cudaMalloc(p, sizeof(double) * std::max<int64_t>(cnt, 1)) != cudaSuccess) {
+            cudaGetLastError();
+            st = fail(ctx, NEK_ENOMEM, "projection space allocation failed");
+        }
+    };
+    al(&P->X, (int64_t)P->L * n); al(&P->B, (int64_t)P->L * n);
+    for (double **p : {&P->xbar, &P->db, &P->dx, &P->v, &P->av, &P->bm}) al(p, n);
+    al(&P->coef, PROJ_MAX_VECTORS); al(&P->part, (int64_t)P->nblk * PROJ_MAX_VECTORS);
+    al(&P->gath, (int64_t)(ctx->nranks + 1) * PROJ_MAX_VECTORS);
+    if (st != NEK_OK) { nek_proj_free(P); return st; }
+    *out = P;
+    return NEK_OK;
+}
+
+extern "C" int nek_proj_free(nek_proj *P)
+{
+    if (!P) return NEK_OK;
+    cudaSetDevice(P->ctx->device);
+    cudaStreamSynchronize(P->ctx->s_main);
+    for (double *p : {P->X, P->B, P->xbar, P->db, P->dx, P->v, P->av, P->bm, P->coef, P->part, P->gath})
+        if (p) cudaFree(p);
+    delete P;
+    return NEK_OK;
+}
+
+extern "C" int nek_proj_size(const nek_proj *P) { return P ? P->l : -1; }
+
+extern "C" int nek_proj_reset(nek_proj *P)
+{
+    if (!P) return NEK_EINVAL;
+    P->l = 0;
+    return NEK_OK;
+}
+
+extern "C" int nek_proj_solve(nek_proj *P, double h1, double h2, const double *b, double *x, double tol, int maxit,
+                              int *iters, double *relres, void *stream)
+{
+    if (!P) return fail(nullptr, NEK_EINVAL, "null projection");
+    nek_ctx *ctx = P->ctx;
+    if (!b || !x || maxit < 0 || !(tol >= 0.0)) return fail(ctx, NEK_EINVAL, "bad b/x/maxit/tol");
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n = ctx->n;
+    int st;
+    enter(ctx, stream);
+    if (!P->hvalid || P->h1 != h1 || P->h2 != h2) { P->l = 0; P->hvalid = true; P->h1 = h1; P->h2 = h2; }
+    // M b (b may live on the host)
+    const double *bsrc = b;
+    if (!is_device_ptr(b)) {
+        if ((st = ensure_stage(ctx)) != NEK_OK) return st;
+        CK(cudaMemcpyAsync(ctx->stage_in, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s_main));
+        bsrc = ctx->stage_in;
+    }
+    CK(launch_copy_mask(n, ctx->mbits, bsrc, P->bm, ctx->s_main));
+    double alpha[PROJ_MAX_VECTORS];
+    if (P->l > 0) {
+        if ((st = proj_dots(P, P->l, P->X, P->bm, alpha)) != NEK_OK) return st;
+        CK(cudaMemcpyAsync(P->coef, alpha, sizeof(double) * P->l, cudaMemcpyHostToDevice, ctx->s_main));
+        CK(launch_multiaxpy(n, P->l, 0.0, P->xbar, P->X, P->coef, ctx->s_main));
+        CK(launch_multiaxpy(n, P->l, 0.0, P->v, P->B, P->coef, ctx->s_main));
+        CK(launch_axpby(n, 1.0, P->bm, -1.0, P->v, P->db, ctx->s_main));
+        ctx->stats.launches += 3;
+    } else {
+        CK(cudaMemsetAsync(P->xbar, 0, sizeof(double) * n, ctx->s_main));
+        CK(cudaMemcpyAsync(P->db, P->bm, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s_main));
+    }
+    double bn2 = 0.0, dn2 = 0.0;
+    if ((st = proj_dots(P, 1, P->bm, P->bm, &bn2)) != NEK_OK) return st;
+    if ((st = proj_dots(P, 1, P->db, P->db, &dn2)) != NEK_OK) return st;
+    const double bn = std::sqrt(bn2), dn = std::sqrt(dn2);
+    double rel = 1.0;
+    if (bn > 0.0 && dn > 0.0) rel = std::min(1.0, tol * bn / dn);
+    int it = 0;
+    double rr = 0.0;
+    int pst = nek_pcg_solve(ctx, h1, h2, P->db, P->dx, rel, maxit, &it, &rr, nullptr, ctx->s_main);
+    if (pst < 0) return pst;
+    CK(launch_axpby(n, 1.0, P->xbar, 1.0, P->dx, P->v, ctx->s_main));   // x = xbar + dx (in v)
+    ctx->stats.launches += 1;
+    if (is_device_ptr(x)) CK(cudaMemcpyAsync(x, P->v, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s_main));
+    else CK(cudaMemcpyAsync(x, P->v, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s_main));
+    // update the space
+    if (P->L > 0 && bn > 0.0) {
+        if (P->l < P->L) {
+            CK(cudaMemcpyAsync(P->v, P->dx, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s_main));
+            if ((st = apply_op(ctx, h1, h2, P->v, P->av, false, nullptr)) != NEK_OK) return st;
+            double c[PROJ_MAX_VECTORS];
+            for (int pass = 0; pass < 2 && P->l > 0; ++pass) {
+                if ((st = proj_dots(P, P->l, P->B, P->v, c)) != NEK_OK) return st;
+                for (int i = 0; i < P->l; ++i) c[i] = -c[i];
+                CK(cudaMemcpyAsync(P->coef, c, sizeof(double) * P->l, cudaMemcpyHostToDevice, ctx->s_main));
+                CK(launch_multiaxpy(n, P->l, 1.0, P->v, P->X, P->coef, ctx->s_main));
+                CK(launch_multiaxpy(n, P->l, 1.0, P->av, P->B, P->coef, ctx->s_main));
+                ctx->stats.launches += 2;
+            }
+            double nrm2 = 0.0;
+            if ((st = proj_dots(P, 1, P->v, P->av, &nrm2)) != NEK_OK) return st;
+            if (nrm2 > 0.0) {
+                const double inv = 1.0 / std::sqrt(nrm2);
+                CK(launch_axpby(n, inv, P->v, 0.0, P->v, P->X + (int64_t)P->l * n, ctx->s_main));
+                CK(launch_axpby(n, inv, P->av, 0.0, P->av, P->B + (int64_t)P->l * n, ctx->s_main));
+                ctx->stats.launches += 2;
+                P->l += 1;
+            }
+        } else {   // full: restart from the current solution
+            if ((st = apply_op(ctx, h1, h2, P->v, P->av, false, nullptr)) != NEK_OK) return st;
+            double nrm2 = 0.0;
+            if ((st = proj_dots(P, 1, P->v, P->av, &nrm2)) != NEK_OK) return st;
+            if (nrm2 > 0.0) {
+                const double inv = 1.0 / std::sqrt(nrm2);
+                CK(launch_axpby(n, inv, P->v, 0.0, P->v, P->X, ctx->s_main));
+                CK(launch_axpby(n, inv, P->av, 0.0, P->av, P->B, ctx->s_main));
+                ctx->stats.launches += 2;
+                P->l = 1;
+            } else {
+                P->l = 0;
+            }
+        }
+    }
+    CK(cudaStreamSynchronize(ctx->s_main));
+    if (iters) *iters = it;
+    if (relres) *relres = bn > 0.0 ? rr * dn / bn : 0.0;
+    leave(ctx, stream);
+    return pst;
+}

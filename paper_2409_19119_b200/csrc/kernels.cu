@@ -176,61 +176,71 @@ cudaError_t launch_geom(int N, int64_t E, const double *xyz, double *G, double *
 }
 
 // ------------------------------------------------------------------- Ax v0
-// One element per CTA, (N+1)^2 threads (i fastest), the k-column of u and of
-// the result in registers, one (i,j) slice in shared memory at a time.
+// Any order N.  EPB elements per CTA (threadIdx.y), (N+1)^2 threads per element
+// (threadIdx.x, i fastest), the k-column of u and of the result in registers,
+// one (i,j) slice per element in shared memory at a time.  One <u, w> partial
+// per CTA.
+constexpr int v0_epb(int NQ) { return NQ * NQ >= 256 ? 1 : 256 / (NQ * NQ); }
+
 template <int NQ>
-__global__ void __launch_bounds__(NQ *NQ)
-    ax_v0_kernel(int64_t eoff, const int32_t *__restrict__ elist, const double *__restrict__ u,
+__global__ void __launch_bounds__(NQ *NQ *v0_epb(NQ))
+    ax_v0_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *__restrict__ u,
                  const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
                  double h1, double h2, double *__restrict__ w, double *__restrict__ part, const int *__restrict__ done)
 {
-    constexpr int P2 = NQ * NQ, P3 = P2 * NQ, N = NQ - 1;
+    constexpr int P2 = NQ * NQ, P3 = P2 * NQ, N = NQ - 1, EPB = v0_epb(NQ);
     if (done && *(volatile const int *)done) return;
     __shared__ double sD[NQ * NQ];
-    __shared__ double sa[P2], sb[P2];
-    __shared__ double sred[P2];
-    const int t = threadIdx.x, i = t % NQ, j = t / NQ;
-    const int64_t pos = eoff + blockIdx.x;
+    __shared__ double sa[EPB][P2], sb[EPB][P2];
+    __shared__ double sred[P2 * EPB];
+    const int t = threadIdx.x, g = threadIdx.y, i = t % NQ, j = t / NQ;
+    const int64_t rel = (int64_t)blockIdx.x * EPB + g;
+    const bool valid = rel < nelem;
+    const int64_t pos = eoff + (valid ? rel : 0);
     const int64_t e = elist ? (int64_t)elist[pos] : pos;
-    for (int q = t; q < NQ * NQ; q += P2) sD[q] = c_D[N][q];
+    for (int q = t + P2 * g; q < NQ * NQ; q += P2 * EPB) sD[q] = c_D[N][q];
     const double *ue = u + e * P3;
     const double *Ge = G + e * 6 * (int64_t)P3;
     double ru[NQ], rw[NQ];
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
         const int64_t l = e * P3 + k * P2 + t;
-        double v = ue[k * P2 + t];
-        if (mbits && bit_of(mbits, l)) v = 0.0;
+        double v = valid ? ue[k * P2 + t] : 0.0;
+        if (valid && mbits && bit_of(mbits, l)) v = 0.0;
         ru[k] = v;
         rw[k] = 0.0;
     }
     __syncthreads();
+    double *sag = sa[g], *sbg = sb[g];
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
-        sa[t] = ru[k];
+        sag[t] = ru[k];
         __syncthreads();
         double ur = 0, us = 0, ut = 0;
 #pragma unroll
         for (int m = 0; m < NQ; ++m) {
-            ur = fma(sD[i * NQ + m], sa[j * NQ + m], ur);
-            us = fma(sD[j * NQ + m], sa[m * NQ + i], us);
+            ur = fma(sD[i * NQ + m], sag[j * NQ + m], ur);
+            us = fma(sD[j * NQ + m], sag[m * NQ + i], us);
             ut = fma(sD[k * NQ + m], ru[m], ut);
         }
         const int q = k * P2 + t;
-        const double Grr = Ge[q], Grs = Ge[P3 + q], Grt = Ge[2 * P3 + q];
-        const double Gss = Ge[3 * P3 + q], Gst = Ge[4 * P3 + q], Gtt = Ge[5 * P3 + q];
+        double Grr = 0, Grs = 0, Grt = 0, Gss = 0, Gst = 0, Gtt = 0;
+        if (valid) {
+            Grr = Ge[q]; Grs = Ge[P3 + q]; Grt = Ge[2 * P3 + q];
+            Gss = Ge[3 * P3 + q]; Gst = Ge[4 * P3 + q]; Gtt = Ge[5 * P3 + q];
+        }
         const double gr = Grr * ur + Grs * us + Grt * ut;
         const double gs = Grs * ur + Gss * us + Gst * ut;
         const double gt = Grt * ur + Gst * us + Gtt * ut;
         __syncthreads();
-        sa[t] = gr;
-        sb[t] = gs;
+        sag[t] = gr;
+        sbg[t] = gs;
         __syncthreads();
         double acc = 0;
 #pragma unroll
         for (int m = 0; m < NQ; ++m) {
-            acc = fma(sD[m * NQ + i], sa[j * NQ + m], acc);
-            acc = fma(sD[m * NQ + j], sb[m * NQ + i], acc);
+            acc = fma(sD[m * NQ + i], sag[j * NQ + m], acc);
+            acc = fma(sD[m * NQ + j], sbg[m * NQ + i], acc);
         }
         rw[k] += acc;
 #pragma unroll
@@ -238,18 +248,27 @@ __global__ void __launch_bounds__(NQ *NQ)
         __syncthreads();
     }
     double dot = 0.0;
+    if (valid) {
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) {
-        const int64_t l = e * P3 + k * P2 + t;
-        double v = h1 * rw[k];
-        if (h2 != 0.0) v = fma(h2 * wJ[l], ru[k], v);
-        if (mbits && bit_of(mbits, l)) v = 0.0;
-        w[l] = v;
-        dot = fma(ru[k], v, dot);
+        for (int k = 0; k < NQ; ++k) {
+            const int64_t l = e * P3 + k * P2 + t;
+            double v = h1 * rw[k];
+            if (h2 != 0.0) v = fma(h2 * wJ[l], ru[k], v);
+            if (mbits && bit_of(mbits, l)) v = 0.0;
+            w[l] = v;
+            dot = fma(ru[k], v, dot);
+        }
     }
     if (part) {
-        double s = block_sum_any(dot, sred);
-        if (t == 0) part[pos] = s;
+        // fixed-order CTA sum over the linear thread index
+        const int lt = t + P2 * g, nt = P2 * EPB;
+        sred[lt] = dot;
+        __syncthreads();
+        for (int s2 = 512; s2 > 0; s2 >>= 1) {
+            if (s2 < nt && lt < s2 && lt + s2 < nt) sred[lt] += sred[lt + s2];
+            __syncthreads();
+        }
+        if (lt == 0) part[blockIdx.x] = sred[0];
     }
 }
 
@@ -1266,6 +1285,7 @@ bool ax_has_fused(int variant, int N) { return (variant == 0 || variant == 8 || 
 // variant (N = 7): 0 = default (v5, DMMA, k-slabs, 4 CTAs/SM), 8 = v5 at 3 CTAs/SM,
 // 9 = v5 + L2 bulk prefetch of the next element, 10 = v5 + TMA ring for G (3 CTAs/SM), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
 // 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups, 6 = v3 with 1 k-group, 7 = v4 (DMMA, j-slabs)
+constexpr int V5_SMALL_ELEMS_PER_CTA = 16;
 static int per_sm_of(int variant)
 {
     switch (variant) {
@@ -1285,8 +1305,11 @@ static int per_sm_of(int variant)
 int64_t ax_grid(int variant, int N, int64_t nelem)
 {
     if (nelem <= 0) return 0;
+    if (N == 7 && variant == 0 && nelem <= (int64_t)V5_SMALL_ELEMS_PER_CTA * 4 * 148)
+        return std::min<int64_t>(nelem, 3 * 148);   // auto: the TMA-staged configuration (see launch_ax)
     if (N == 7 && per_sm_of(variant) > 0) return std::min<int64_t>(nelem, (int64_t)per_sm_of(variant) * 148);
-    return nelem;
+    const int epb = v0_epb(N + 1);
+    return (nelem + epb - 1) / epb;
 }
 
 int ax_partials_needed(int variant, int N, int64_t E) { return (int)std::max<int64_t>(2 * ax_grid(variant, N, E), E); }
@@ -1314,7 +1337,9 @@ static void ax_v0_launch(int64_t nelem, int64_t eoff, const int32_t *elist, cons
                          const double *wJ, const uint32_t *mbits, double h1, double h2, double *w, double *part,
                          const int *done, cudaStream_t s)
 {
-    ax_v0_kernel<NQ><<<(unsigned)nelem, NQ * NQ, 0, s>>>(eoff, elist, u, G, wJ, mbits, h1, h2, w, part, done);
+    constexpr int EPB = v0_epb(NQ);
+    ax_v0_kernel<NQ><<<(unsigned)((nelem + EPB - 1) / EPB), dim3(NQ * NQ, EPB), 0, s>>>(
+        nelem, eoff, elist, u, G, wJ, mbits, h1, h2, w, part, done);
 }
 
 cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
@@ -1350,9 +1375,15 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         if (variant == 10)
             return h2 != 0.0 ? ax_v5_launch<true, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
-        if (variant == 0)
+        if (variant == 0) {
+            // few elements per CTA (the pipeline never fills): TMA-staged metric prefetch at 3 CTAs/SM;
+            // otherwise register streaming at 4 CTAs/SM (measured 98% of the copy peak at scale)
+            if (L.nelem <= (int64_t)V5_SMALL_ELEMS_PER_CTA * 4 * 148)
+                return h2 != 0.0 ? ax_v5_launch<true, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                                 : ax_v5_launch<false, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
             return h2 != 0.0 ? ax_v5_launch<true, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+        }
         return h2 != 0.0 ? ax_v5_launch<true, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                          : ax_v5_launch<false, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
     }
@@ -1371,7 +1402,7 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         return h2 != 0.0 ? ax_v3_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                          : ax_v3_launch<false, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
     }
-    double *part = L.part ? L.part + L.part_off - L.eoff : nullptr;   // v0 writes part[eoff + block]
+    double *part = L.part ? L.part + L.part_off : nullptr;   // v0: one partial per CTA
     switch (N) {
 #define NEK_CASE(NN) \
     case NN: ax_v0_launch<NN + 1>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w, part, L.done, s); break;
@@ -2185,5 +2216,75 @@ cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, c
     return cudaGetLastError();
 }
 
+
+// ------------------------------------------------ projection (NEXT #2)
+// out_part[block][i] = block partial of <V_i, y>_owner for i < l (V is [l][n] row-major);
+// the caller reduces the partials in block order.  l <= PROJ_MAXV.
+constexpr int PROJ_MAXV = 32;
+
+__global__ void __launch_bounds__(256)
+    multidot_kernel(int64_t n, int l, const double *__restrict__ V, const double *__restrict__ y,
+                    const uint32_t *__restrict__ obits, double *__restrict__ out_part)
+{
+    __shared__ double sred[32];
+    double acc[PROJ_MAXV];
+#pragma unroll
+    for (int i = 0; i < PROJ_MAXV; ++i) acc[i] = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        if (!bit_of(obits, p)) continue;
+        const double yv = y[p];
+#pragma unroll
+        for (int i = 0; i < PROJ_MAXV; ++i)
+            if (i < l) acc[i] = fma(V[(int64_t)i * n + p], yv, acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < PROJ_MAXV; ++i) {
+        if (i >= l) break;
+        const double s2 = block_sum(acc[i], sred);
+        if (threadIdx.x == 0) out_part[(int64_t)blockIdx.x * l + i] = s2;
+    }
+}
+
+cudaError_t launch_multidot(int64_t n, int l, const double *V, const double *y, const uint32_t *obits,
+                            double *out_part, int nblk, cudaStream_t s)
+{
+    if (l <= 0) return cudaSuccess;
+    multidot_kernel<<<nblk, 256, 0, s>>>(n, l, V, y, obits, out_part);
+    return cudaGetLastError();
+}
+
+// y = a * y + sum_{i<l} c[i] * V_i  (c on the device)
+__global__ void multiaxpy_kernel(int64_t n, int l, double a, double *__restrict__ y, const double *__restrict__ V,
+                                 const double *__restrict__ c)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        double v = a == 0.0 ? 0.0 : a * y[p];
+        for (int i = 0; i < l; ++i) v = fma(c[i], V[(int64_t)i * n + p], v);
+        y[p] = v;
+    }
+}
+
+cudaError_t launch_multiaxpy(int64_t n, int l, double a, double *y, const double *V, const double *c, cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    multiaxpy_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(n, l, a, y, V, c);
+    return cudaGetLastError();
+}
+
+// z = alpha * x + beta * y
+__global__ void axpby_kernel(int64_t n, double alpha, const double *__restrict__ x, double beta,
+                             const double *__restrict__ y, double *__restrict__ z)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        z[p] = fma(alpha, x[p], beta * y[p]);
+}
+
+cudaError_t launch_axpby(int64_t n, double alpha, const double *x, double beta, const double *y, double *z,
+                         cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    axpby_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(n, alpha, x, beta, y, z);
+    return cudaGetLastError();
+}
 
 }  // namespace nekb200

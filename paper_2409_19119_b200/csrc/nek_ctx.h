@@ -136,6 +136,13 @@ cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, do
 cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s);
 bool ax_has_fused(int variant, int N);
+// projection space (NEXT #2)
+constexpr int PROJ_MAX_VECTORS = 32;
+cudaError_t launch_multidot(int64_t n, int l, const double *V, const double *y, const uint32_t *obits,
+                            double *out_part, int nblk, cudaStream_t s);
+cudaError_t launch_multiaxpy(int64_t n, int l, double a, double *y, const double *V, const double *c, cudaStream_t s);
+cudaError_t launch_axpby(int64_t n, double alpha, const double *x, double beta, const double *y, double *z,
+                         cudaStream_t s);
 // NVLink peer-memory exchange (CUDA IPC mappings; see kernels.cu)
 cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *red_loc, double *red_all, double *mbox,
                                 double *const *peer_mbox, uint64_t *epochs, int *err, cudaStream_t s);

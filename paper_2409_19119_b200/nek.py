@@ -79,6 +79,11 @@ _sig = {
     "nek_set_timing": ([_P, _I], _I),
     "nek_get_stats": ([_P, ctypes.POINTER(nek_stats_t), _I], _I),
     "nek_set_variant": ([_P, _I], _I),
+    "nek_proj_create": ([_P, _I, ctypes.POINTER(_P)], _I),
+    "nek_proj_solve": ([_P, _D, _D, _P, _P, _D, _I, ctypes.POINTER(_I), ctypes.POINTER(_D), _P], _I),
+    "nek_proj_size": ([_P], _I),
+    "nek_proj_reset": ([_P], _I),
+    "nek_proj_free": ([_P], _I),
     "nek_plan_create": ([ctypes.POINTER(_P), _I64, _I, _P, _P, _P], _I),
     "nek_plan_surface_gids": ([_P, _P], _I64),
     "nek_plan_set_ranks": ([_P, _I, _I, _P, _P], _I),
@@ -280,6 +285,45 @@ def get_stats(ctx: Context, reset=False) -> dict:
 
 def set_variant(ctx: Context, v: int):
     _check(_lib.nek_set_variant(ctx.handle, int(v)), ctx.handle)
+
+
+class Projection:
+    """nek_proj_*: projection of the initial guess onto up to max_vectors prior solutions
+    (Fischer; P:513-519)."""
+
+    def __init__(self, ctx: Context, max_vectors: int):
+        self.ctx = ctx
+        h = ctypes.c_void_p()
+        _check(_lib.nek_proj_create(ctx.handle, int(max_vectors), ctypes.byref(h)), ctx.handle)
+        self._h = h
+
+    def solve(self, h1, h2, b, x, tol, maxit):
+        """-> (status, iters, relres)"""
+        pb, sb = _field_ptr(b, self.ctx.n, "b")
+        px, sx = _field_ptr(x, self.ctx.n, "x", writable=True)
+        it = ctypes.c_int(0)
+        rr = ctypes.c_double(0.0)
+        st = _lib.nek_proj_solve(self._h, float(h1), float(h2), pb, px, float(tol), int(maxit), ctypes.byref(it),
+                                 ctypes.byref(rr), _stream_of(sb, sx))
+        _check(st, self.ctx.handle)
+        return st, it.value, rr.value
+
+    def size(self):
+        return _lib.nek_proj_size(self._h)
+
+    def reset(self):
+        _lib.nek_proj_reset(self._h)
+
+    def free(self):
+        if self._h:
+            _lib.nek_proj_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 # --------------------------------------------------------------- host plans

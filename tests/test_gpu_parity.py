@@ -328,3 +328,29 @@ def test_rod_bundle_parity(nek, N, dirichlet):
         assert rel(x, xo) <= 1e-9
     finally:
         nek.free(ctx)
+
+
+@pytest.mark.parametrize("L", [0, 4, 8])
+def test_projection_sequence_matches_oracle(nek, L):
+    """Projection initial guess (NEXT #2) over a drifting sequence of right-hand sides:
+    same PCG iteration counts as the oracle (+-1) and solutions within 1e-8."""
+    from oracle.projection import Projection as OProj
+    m = mg.box_mesh(4, 3, 3, 7, deform="bubble")
+    O = oracle.Oracle.from_mesh(m)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    P = nek.Projection(ctx, L)
+    OP = OProj(O, L)
+    try:
+        b0, b1, b2 = (mg.smooth_field(m, seed=s) for s in (11, 12, 13))
+        for t in range(12):
+            b = b0 + 0.02 * t * b1 + 1e-3 * np.sin(t) * b2
+            xo, ito, sto = OP.solve(1.0, 0.0, b, 1e-9, 1000)
+            x = np.zeros(m.n_local)
+            st, it, rr = P.solve(1.0, 0.0, b, x, 1e-9, 1000)
+            assert st == nek.OK and abs(it - ito) <= 1, (t, it, ito)
+            assert rel(x, xo) <= 1e-8
+            assert rr <= 1e-9 * (1 + 1e-6)
+            assert P.size() == min(len(OP.X), L) or L == 0
+    finally:
+        P.free()
+        nek.free(ctx)
