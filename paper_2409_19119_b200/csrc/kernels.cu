@@ -180,7 +180,7 @@ cudaError_t launch_geom(int N, int64_t E, const double *xyz, double *G, double *
 // (threadIdx.x, i fastest), the k-column of u and of the result in registers,
 // one (i,j) slice per element in shared memory at a time.  One <u, w> partial
 // per CTA.
-constexpr int v0_epb(int NQ) { return NQ * NQ >= 256 ? 1 : 256 / (NQ * NQ); }
+constexpr int v0_epb(int NQ) { return NQ * NQ >= 128 ? 1 : 128 / (NQ * NQ); }
 
 template <int NQ>
 __global__ void __launch_bounds__(NQ *NQ *v0_epb(NQ))
