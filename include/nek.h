@@ -223,7 +223,11 @@ typedef struct {
 int nek_set_timing(nek_ctx *ctx, int on);
 int nek_get_stats(nek_ctx *ctx, nek_stats_t *stats, int reset);
 
-/* Ax kernel variant selection (0 = default).  For experiments and tests. */
+/* Ax kernel variant selection (0 = default).  For experiments and tests.
+ *   0  default: N = 7 -> v5 (DMMA k-slabs, fused PCG prologue); N <= 9 otherwise -> v6
+ *      (TMA-staged metric ring, line-wise contractions, fused prologue); N >= 10 -> v0
+ *   1  v0 (any N, (i,j)-thread columns)       11  v6 at any N <= 9 (N = 7 included)
+ *   2..10  N = 7 experiments (v1..v5 configurations); other N -> v0 */
 int nek_set_variant(nek_ctx *ctx, int ax_variant);
 
 /* --------------------------------------------- host-only planning (no GPU) */

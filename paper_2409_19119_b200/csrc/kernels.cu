@@ -1280,7 +1280,33 @@ static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double
     return cudaGetLastError();
 }
 
-bool ax_has_fused(int variant, int N) { return (variant == 0 || variant == 8 || variant == 9 || variant == 10) && N == 7; }
+#include "ax_v6.cuh"
+
+// v6 (any N <= 9): the default for N != 7, variant 11 at any N <= 9
+static bool use_v6(int variant, int N) { return N <= 9 && ((variant == 0 && N != 7) || variant == 11); }
+static int v6_minb(int N)
+{
+    switch (N + 1) {
+#define NEK_CASE(NQ) case NQ: return V6<NQ>::MINB;
+        NEK_CASE(2) NEK_CASE(3) NEK_CASE(4) NEK_CASE(5) NEK_CASE(6) NEK_CASE(7) NEK_CASE(8) NEK_CASE(9) NEK_CASE(10)
+#undef NEK_CASE
+    }
+    return 1;
+}
+static int v6_epb(int N)
+{
+    switch (N + 1) {
+#define NEK_CASE(NQ) case NQ: return V6<NQ>::EPB;
+        NEK_CASE(2) NEK_CASE(3) NEK_CASE(4) NEK_CASE(5) NEK_CASE(6) NEK_CASE(7) NEK_CASE(8) NEK_CASE(9) NEK_CASE(10)
+#undef NEK_CASE
+    }
+    return 1;
+}
+
+bool ax_has_fused(int variant, int N)
+{
+    return ((variant == 0 || variant == 8 || variant == 9 || variant == 10) && N == 7) || use_v6(variant, N);
+}
 
 // variant (N = 7): 0 = default (v5, DMMA, k-slabs, 4 CTAs/SM), 8 = v5 at 3 CTAs/SM,
 // 9 = v5 + L2 bulk prefetch of the next element, 10 = v5 + TMA ring for G (3 CTAs/SM), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
@@ -1308,11 +1334,19 @@ int64_t ax_grid(int variant, int N, int64_t nelem)
     if (N == 7 && variant == 0 && nelem <= (int64_t)V5_SMALL_ELEMS_PER_CTA * 4 * 148)
         return std::min<int64_t>(nelem, 3 * 148);   // auto: the TMA-staged configuration (see launch_ax)
     if (N == 7 && per_sm_of(variant) > 0) return std::min<int64_t>(nelem, (int64_t)per_sm_of(variant) * 148);
+    if (use_v6(variant, N)) {
+        const int64_t nbat = (nelem + v6_epb(N) - 1) / v6_epb(N);
+        return std::min<int64_t>(nbat, (int64_t)v6_minb(N) * 148);
+    }
     const int epb = v0_epb(N + 1);
     return (nelem + epb - 1) / epb;
 }
 
-int ax_partials_needed(int variant, int N, int64_t E) { return (int)std::max<int64_t>(2 * ax_grid(variant, N, E), E); }
+// enough partial slots for any variant (two concurrent launches of up to 4 CTAs per SM each)
+int ax_partials_needed(int variant, int N, int64_t E)
+{
+    return (int)std::max<int64_t>(std::max<int64_t>(2 * ax_grid(variant, N, E), E), 2 * 4 * 148);
+}
 
 template <bool HELM>
 static cudaError_t ax_v1_launch(const AxLaunch &L, const double *u, const double *G, const double *wJ,
@@ -1386,6 +1420,20 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         }
         return h2 != 0.0 ? ax_v5_launch<true, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                          : ax_v5_launch<false, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+    }
+    if (use_v6(variant, N)) {
+        if (nlaunch) ++*nlaunch;
+        const int64_t grid = ax_grid(variant, N, L.nelem);
+        switch (N + 1) {
+#define NEK_CASE(NQ)                                                                        \
+    case NQ:                                                                                \
+        return h2 != 0.0 ? ax_v6_launch<NQ, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s) \
+                         : ax_v6_launch<NQ, false>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+            NEK_CASE(2) NEK_CASE(3) NEK_CASE(4) NEK_CASE(5) NEK_CASE(6) NEK_CASE(7) NEK_CASE(8) NEK_CASE(9)
+            NEK_CASE(10)
+#undef NEK_CASE
+        }
+        return cudaErrorInvalidValue;
     }
     if (N == 7 && variant == 7) {
         if (nlaunch) ++*nlaunch;

@@ -246,7 +246,7 @@ def test_config2_full_size(nek):
         nek.free(ctx)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11])
 def test_ax_all_variants_N7(nek, variant):
     """Every Ax kernel variant (nek_set_variant) against the oracle, Poisson and Helmholtz."""
     m = mg.box_mesh(3, 4, 5, 7, deform="bubble")
@@ -264,6 +264,34 @@ def test_ax_all_variants_N7(nek, variant):
         x = np.zeros(m.n_local)
         st, it, _, hg = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, 30, want_hist=True)
         assert it == 30 and np.all(np.abs(hg - ho) <= O.hist_tolerance(1.0, 0.0, b, 30))
+    finally:
+        nek.free(ctx)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 8, 9])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_ax_generic_orders(nek, N, variant):
+    """The any-order kernels (default 0 = v6 TMA/line kernel, 1 = v0) at every tuned order, on a
+    mesh spanning several element batches per CTA with a ragged last batch, Poisson and
+    Helmholtz, plus a fused PCG window (the v6 prologue) against the oracle."""
+    E3 = {1: (7, 6, 5), 2: (7, 5, 5), 3: (6, 5, 5), 4: (5, 5, 4), 5: (5, 4, 4), 6: (4, 4, 3), 8: (3, 3, 3),
+          9: (3, 3, 2)}[N]
+    m = mg.box_mesh(*E3, N, deform="sin", eps=0.06)
+    O = oracle.Oracle.from_mesh(m)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        nek.set_variant(ctx, variant)
+        u = mg.random_evector(m, seed=23)
+        for h in ((1.0, 0.0), (0.7, 2.0)):
+            w = np.empty(m.n_local)
+            nek.ax(ctx, h[0], h[1], u, w)
+            assert rel(w, O.apply(h[0], h[1], u)) <= 1e-12, (variant, h)
+        b = mg.smooth_field(m, seed=2)
+        for h in ((1.0, 0.0), (1.0, 5.0)):
+            _, ito, _, ho = O.pcg(h[0], h[1], b, 0.0, 20)
+            x = np.zeros(m.n_local)
+            st, it, _, hg = nek.pcg_solve(ctx, h[0], h[1], b, x, 0.0, 20, want_hist=True)
+            assert it == 20 and np.all(np.abs(hg - ho) <= O.hist_tolerance(h[0], h[1], b, 20)), h
     finally:
         nek.free(ctx)
 

@@ -1,5 +1,4 @@
-set -x
-python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
-python bench.py --steps 10 --warmup 3 > gpurun_out/bench15.json 2> gpurun_out/bench15.err
-python bench.py --steps 5 --warmup 3 --no-cpu-baseline --ez 128 > gpurun_out/bench15_ez128.json 2>> gpurun_out/bench15.err
-timeout 900 python tools/nsweep.py 3 4 5 6 8 9 > gpurun_out/nsweep.jsonl 2> gpurun_out/nsweep.err
+timeout 600 python tools/nsweep.py 3 4 5 6 8 9 > gpurun_out/nsweep_v6.jsonl 2> gpurun_out/nsweep_v6.err
+NSWEEP_VARIANT=1 timeout 600 python tools/nsweep.py 3 5 9 > gpurun_out/nsweep_v0.jsonl 2>> gpurun_out/nsweep_v6.err
+cat gpurun_out/nsweep_v6.jsonl gpurun_out/nsweep_v0.jsonl
+echo done

@@ -21,6 +21,9 @@ for N in orders:
     Ex, Ey, Ez = BOXES[N]
     m = mg.box_mesh(Ex, Ey, Ez, N, deform="bubble", dirichlet="all")
     ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask)
+    variant = int(os.environ.get("NSWEEP_VARIANT", "0"))
+    if variant:
+        nek.set_variant(ctx, variant)
     u = torch.from_numpy(mg.smooth_field(m, 1)).cuda()
     w = torch.empty_like(u)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -41,7 +44,7 @@ for N in orders:
     st = nek.get_stats(ctx, reset=True)
     ax_ms = st["ax_ms"] / st["ax_launches"]
     gbs = st["ax_bytes"] / st["ax_launches"] / (ax_ms * 1e-3) / 1e9
-    print(json.dumps({"N": N, "box": [Ex, Ey, Ez], "n_dof": m.n_dof, "n_local": m.n_local,
+    print(json.dumps({"N": N, "variant": variant, "box": [Ex, Ey, Ez], "n_dof": m.n_dof, "n_local": m.n_local,
                       "ax_gs_gdof_per_s": m.n_dof * reps / (tot * 1e-3) / 1e9, "ax_ms": ax_ms,
                       "gs_ms": st["gs_ms"] / max(1, st["gs_launches"]), "ax_GBps": gbs, "ax_frac_of_peak": gbs / peak}),
           flush=True)
