@@ -173,6 +173,61 @@ int nek_proj_size(const nek_proj *proj);      /* vectors currently in the space 
 int nek_proj_reset(nek_proj *proj);
 int nek_proj_free(nek_proj *proj);
 
+/* ------------------------------------------- p-multigrid preconditioned CG */
+/*
+ * p-multigrid V-cycle with Chebyshev smoothing as the preconditioner of the same
+ * Hestenes-Stiefel PCG ("local smoothers for
+ * p-multigrid", "p-multigrid schedules of p=7, 5, 3, and 1 with
+ * 6th-order Chebyshev smoothing").  DESIGN.md readings P1-P7:
+ *   levels    orders[0] = N > orders[1] > ... > orders[nlevels-1] = 1 (default
+ *             [N,5,3,1] for N >= 7, [N,3,1] for 4 <= N < 7, [N,1] for N = 2, 3);
+ *             each coarse level re-discretises the same elements: GLL-node
+ *             coordinates interpolated from `xyz` (the array given to nek_setup),
+ *             node ids keyed by mesh entities of the fine ids, the fine mask
+ *             carried over (it must be constant on every edge / face interior:
+ *             a union of closed boundary faces, else NEK_EINVAL);
+ *   transfer  prolongation J x J x J per element; restriction its transpose
+ *             applied to the owner copies, then QQ^T and the mask of the level;
+ *   smoother  Chebyshev (Saad Alg. 12.1) of `degree` with Jacobi on
+ *             [lmin_frac lam, lmax_factor lam], lam the largest Ritz value of
+ *             `lanczos_steps` Jacobi-PCG steps from M hash(gid);
+ *   coarse    Chebyshev of `coarse_degree` on [coarse_lo lam_min, lmax_factor lam]
+ *             of the order-1 level (no host solver);
+ *   V-cycle   x = S(f); r = f - A x; e = V(R r); x += P e; x = x + S(f - A x).
+ * All levels run on the context's device and streams; for nranks > 1 every call
+ * is collective and each level exchanges its own halo like the fine operator.
+ * (h1, h2) are fixed at creation (eigenvalue bounds and diagonals depend on them).
+ * Zero-valued option fields take the defaults in brackets: degree [6],
+ * coarse_degree [20], lmin_frac [0.1], lmax_factor [1.1], coarse_lo [1.0],
+ * lanczos_steps [20], nlevels [0 = default schedule].
+ * nek_pmg_apply:  z = V(r), r and z E-vectors (device or host), not aliasing.
+ * nek_pmg_solve:  PCG on A x = M b with z = V(r); arguments, stopping rule and
+ *                 status as nek_pcg_solve.
+ */
+#define NEK_PMG_MAX_LEVELS 8
+typedef struct nek_pmg nek_pmg;
+typedef struct {
+    int32_t nlevels;
+    int32_t orders[NEK_PMG_MAX_LEVELS];
+    int32_t degree, coarse_degree, lanczos_steps;
+    double lmin_frac, lmax_factor, coarse_lo;
+} nek_pmg_opts;
+typedef struct {
+    int32_t nlevels;
+    int32_t orders[NEK_PMG_MAX_LEVELS];
+    int32_t degree, coarse_degree;
+    int64_t n_local[NEK_PMG_MAX_LEVELS];
+    double lam_min[NEK_PMG_MAX_LEVELS], lam_max[NEK_PMG_MAX_LEVELS];
+    int64_t vcycles;           /* V-cycles applied so far                         */
+} nek_pmg_info_t;
+int nek_pmg_create(nek_ctx *ctx, const double *xyz, double h1, double h2, const nek_pmg_opts *opts, nek_pmg **out,
+                   void *stream);
+int nek_pmg_apply(nek_pmg *pmg, const double *r, double *z, void *stream);
+int nek_pmg_solve(nek_pmg *pmg, const double *b, double *x, double tol, int maxit, int *iters, double *relres,
+                  double *hist, void *stream);
+int nek_pmg_info(const nek_pmg *pmg, nek_pmg_info_t *info);
+int nek_pmg_free(nek_pmg *pmg);
+
 /* ----------------------------------------------------------- introspection */
 typedef struct {
     int64_t E;                 /* local elements                                   */

@@ -287,7 +287,18 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     const int64_t g1 = ax_grid(ctx->variant, ctx->N, nb), g2 = ax_grid(ctx->variant, ctx->N, ni);
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
     L.elist = ctx->elist;
-    if (ax_has_fused(ctx->variant, ctx->N)) {
+    if (ax_has_fused(ctx->variant, ctx->N) && ctx->p2p && !ctx->concurrent_bnd) {
+        // Boundary elements, then the halo send, then the interior elements, in stream order: the
+        // NVLink transfer overlaps the interior work and the send never waits for SM
+        // slots held by the persistent interior grid; the last CTA of either launch finalises sigma.
+        if (dot) { L.part = ctx->part; L.fin_total = g1 + g2; L.ctas_total = (unsigned)(g1 + g2); }
+        if (push) L.mail = mail_of(ctx);
+        L.nelem = nb; L.eoff = 0; L.part_off = 0;
+        if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
+        if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
+        L.nelem = ni; L.eoff = nb; L.part_off = g1;
+        if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
+    } else if (ax_has_fused(ctx->variant, ctx->N)) {
         // Boundary elements and the halo send on the high-priority stream, interior elements on
         // the main stream, concurrently; the last CTA of either launch finalises sigma.
         CK(cudaEventRecord(ctx->ev_fork2, ctx->s_main));
@@ -489,8 +500,9 @@ int nek_comm_unique_id(unsigned char id[128])
     return NEK_OK;
 }
 
+// parent != NULL: an internal pMG level context on the parent's streams and NCCL communicator
 static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const int64_t *gid,
-                      const uint8_t *dirichlet, const nek_comm *comm, void *stream)
+                      const uint8_t *dirichlet, const nek_comm *comm, void *stream, nek_ctx *parent = nullptr)
 {
     if (N < 1 || N > 15) return fail(ctx, NEK_EORDER, "order N=" + std::to_string(N) + " outside [1,15]");
     if (E < 0 || (E > 0 && (!xyz || !gid))) return fail(ctx, NEK_EINVAL, "E < 0 or null xyz/gid");
@@ -508,6 +520,7 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     ctx->E = E; ctx->N = N; ctx->Nq = N + 1; ctx->P3 = ctx->Nq * ctx->Nq * ctx->Nq; ctx->n = E * ctx->P3;
     ctx->rank = comm && comm->nranks > 1 ? comm->rank : 0;
     ctx->nranks = comm && comm->nranks > 1 ? comm->nranks : 1;
+    if (parent) { ctx->rank = parent->rank; ctx->nranks = parent->nranks; }
 
     // host planning (local maps + validation)
     nek_plan *p = nullptr;
@@ -515,9 +528,12 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     ctx->plan = p;
     if (st != NEK_OK) return fail(ctx, st, p ? p->err : "plan allocation failed");
 
-    CK(cudaStreamCreateWithFlags(&ctx->s_main, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ctx->s_comm, cudaStreamNonBlocking));
-    {
+    if (parent) {
+        ctx->s_main = parent->s_main; ctx->s_comm = parent->s_comm; ctx->s_hi = parent->s_hi;
+        ctx->owns_streams = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&ctx->s_main, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->s_comm, cudaStreamNonBlocking));
         int lo = 0, hi = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CK(cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi));
@@ -527,9 +543,14 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     enter(ctx, stream);
 
     if (ctx->nranks > 1) {
-        ncclUniqueId uid;
-        std::memcpy(&uid, comm->nccl_id, 128);
-        NK(ncclCommInitRank(&ctx->nccl, ctx->nranks, uid, ctx->rank));
+        if (parent) {
+            ctx->nccl = parent->nccl;
+            ctx->owns_nccl = false;
+        } else {
+            ncclUniqueId uid;
+            std::memcpy(&uid, comm->nccl_id, 128);
+            NK(ncclCommInitRank(&ctx->nccl, ctx->nranks, uid, ctx->rank));
+        }
         // setup collective: allgather of element-surface gids (sorted) of every rank
         int64_t ns = nek_plan_surface_gids(p, nullptr);
         std::vector<int64_t> mine(ns);
@@ -598,6 +619,8 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         CK(upload(ctx, &ctx->gsi_idx, idx)); CK(upload(ctx, &ctx->gsi_perm, gp)); CK(upload(ctx, &ctx->gsi_offs, go));
         // off by default: measured slower (the partner gathers are dependent loads inside a
         // streaming kernel, and miss L2 at scale); NEK_GS_INLINE=1 turns it on
+        const char *cenv = getenv("NEK_CONCURRENT_BND");
+        ctx->concurrent_bnd = cenv && std::strcmp(cenv, "1") == 0;
         const char *genv = getenv("NEK_GS_INLINE");
         ctx->gs_inline = genv && std::strcmp(genv, "1") == 0;
     }
@@ -723,10 +746,12 @@ int nek_free(nek_ctx *ctx)
     P.pending.clear(); P.free_ev.clear();
     for (cudaEvent_t e : {ctx->ev_in, ctx->ev_out, ctx->ev_fork, ctx->ev_join, ctx->ev_fork2, ctx->ev_bnd})
         if (e) cudaEventDestroy(e);
-    if (ctx->nccl) ncclCommDestroy(ctx->nccl);
-    if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
-    if (ctx->s_comm) cudaStreamDestroy(ctx->s_comm);
-    if (ctx->s_hi) cudaStreamDestroy(ctx->s_hi);
+    if (ctx->nccl && ctx->owns_nccl) ncclCommDestroy(ctx->nccl);
+    if (ctx->owns_streams) {
+        if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
+        if (ctx->s_comm) cudaStreamDestroy(ctx->s_comm);
+        if (ctx->s_hi) cudaStreamDestroy(ctx->s_hi);
+    }
     nek_plan_free(ctx->plan);
     delete ctx;
     return NEK_OK;
@@ -1218,3 +1243,5 @@ extern "C" int nek_proj_solve(nek_proj *P, double h1, double h2, const double *b
     leave(ctx, stream);
     return pst;
 }
+
+#include "pmg.inc"

@@ -857,9 +857,14 @@ __global__ void __launch_bounds__(128, 3)
     }
     const int jb = 2 * wq;                       // this warp's first slab
     double dot = 0.0;
-    for (int64_t it = 0; it < nit; ++it) {
+    auto elem_at = [&](int64_t it) -> int64_t {
         const int64_t pos = eoff + blockIdx.x + it * (int64_t)gridDim.x;
-        const int64_t e = elist ? (int64_t)elist[pos] : pos;
+        return elist ? (int64_t)elist[pos] : pos;
+    };
+    int64_t e_next = nit > 0 ? elem_at(0) : 0;
+    for (int64_t it = 0; it < nit; ++it) {
+        const int64_t e = e_next;                // element list read one iteration ahead
+        if (it + 1 < nit) e_next = elem_at(it + 1);
         const double *ue = u + e * P3;
         const double *Ge = G + e * 6 * (int64_t)P3;
         const int par = (int)(it & 1);
@@ -1067,9 +1072,10 @@ __global__ void __launch_bounds__(128, MINB)
     }
     const int kb = 2 * wq;                       // this warp's first k-slab
     double dot = 0.0;
+    int64_t e_next = nit > 0 ? elem_at(0) : 0;
     for (int64_t it = 0; it < nit; ++it) {
-        const int64_t pos = eoff + blockIdx.x + it * (int64_t)gridDim.x;
-        const int64_t e = elist ? (int64_t)elist[pos] : pos;
+        const int64_t e = e_next;                // element list read one iteration ahead
+        if (it + 1 < nit) e_next = elem_at(it + 1);
         const double *ue = u + e * P3;
         const double *Ge = G + e * 6 * (int64_t)P3;
         const int par = (int)(it & 1);
@@ -2257,8 +2263,9 @@ cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, c
                                      const int64_t *remote_half, int nnbr, int me, uint64_t *const *peer_hflags,
                                      uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s)
 {
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + 255) / 256, 296));
-    gs_pack_p2p_fused_kernel<<<blocks, 256, 0, s>>>(nslots, perm, offs, v, partial, send_run, slot_nbr, peer_recv,
+    // latency-bound gathers (slot -> run -> copies -> values): many small CTAs in flight
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + 127) / 128, 148 * 16));
+    gs_pack_p2p_fused_kernel<<<blocks, 128, 0, s>>>(nslots, perm, offs, v, partial, send_run, slot_nbr, peer_recv,
                                                     remote_off, send_offs, remote_half, nnbr, me, peer_hflags, epochs,
                                                     counter, done);
     return cudaGetLastError();
@@ -2334,5 +2341,7 @@ cudaError_t launch_axpby(int64_t n, double alpha, const double *x, double beta, 
     axpby_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(n, alpha, x, beta, y, z);
     return cudaGetLastError();
 }
+
+#include "pmg_kernels.cuh"
 
 }  // namespace nekb200

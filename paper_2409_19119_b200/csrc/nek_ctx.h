@@ -61,6 +61,12 @@ struct TimedLaunch { int cls; cudaEvent_t a, b; };
 void gll_rule(int N, double *x, double *w);
 void deriv_matrix(int N, const double *x, double *D);
 
+// pmg_topo.cpp: p-multigrid level construction (host)
+void interp_matrix(int Nfrom, int Nto, double *J);
+void interp_elements_host(int64_t E, int Nin, int Nout, const double *J, const double *in, double *out);
+int pmg_coarse_ids(int64_t E, int Nf, const int64_t *gid, const uint8_t *mask, int Nc, int64_t *gid_c,
+                   uint8_t *mask_c, std::string &err);
+
 // kernels.cu entry points (all launched on `s`)
 cudaError_t upload_D(int N, const double *D);
 cudaError_t launch_geom(int N, int64_t E, const double *xyz, double *G, double *wJ, const double *wq,
@@ -163,6 +169,19 @@ cudaError_t launch_pcg_pupdate(int64_t n, const double *dinv, const double *r, d
 int vec_blocks();
 int upd_blocks();
 
+// pmg_kernels.cuh
+cudaError_t launch_prolong_add(int64_t E, int Nc, int Nf, const double *J, const double *ec, double *uf,
+                               const int *done, cudaStream_t s);
+cudaError_t launch_restrict(int64_t E, int Nf, int Nc, const double *J, const double *rf, const uint32_t *obits,
+                            double *fc, const int *done, cudaStream_t s);
+cudaError_t launch_cheb(int mode, int64_t n, const double *dinv, const double *f, const double *w, double theta,
+                        double c1, double c2, double *d, double *x, double *r, const int *done, cudaStream_t s);
+cudaError_t launch_dot_owner(int64_t n, const uint32_t *obits, const double *a, const double *b, double *part,
+                             int nblk, double *dst, unsigned int *counter, const int *done, cudaStream_t s);
+cudaError_t launch_pcg_pupdate_z(int64_t n, const double *z, double *p, const double *red_all, int nranks,
+                                 PcgScalars *sc, double *hist, unsigned int *counter, int nblk, cudaStream_t s);
+cudaError_t launch_lanczos_rz(int64_t n, double alpha, const double *w, const double *dinv, double *r, double *z,
+                              cudaStream_t s);
 }  // namespace nekb200
 
 struct nek_ctx {
@@ -187,6 +206,8 @@ struct nek_ctx {
     int32_t *gs_p2 = nullptr, *gs_p4 = nullptr, *gs_p8 = nullptr, *gs_pg = nullptr, *gs_og = nullptr;
     int32_t *gsi_idx = nullptr, *gsi_perm = nullptr, *gsi_offs = nullptr;   // GsInline tables
     bool gs_inline = false;
+    bool concurrent_bnd = false;
+    bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts         // NEK_CONCURRENT_BND=1: boundary Ax + send on s_hi beside the interior
     nekb200::GsClasses gsc;
     int32_t *ifc_perm = nullptr, *ifc_offs = nullptr, *send_run = nullptr, *coffs = nullptr, *contrib = nullptr;
     int64_t nifc = 0, nifc_perm = 0, nslots = 0;

@@ -61,6 +61,22 @@ class nek_stats_t(ctypes.Structure):
                 ("ax_elements", ctypes.c_int64), ("ax_bytes", ctypes.c_double)]
 
 
+PMG_MAX_LEVELS = 8
+
+
+class nek_pmg_opts(ctypes.Structure):
+    _fields_ = [("nlevels", ctypes.c_int32), ("orders", ctypes.c_int32 * PMG_MAX_LEVELS),
+                ("degree", ctypes.c_int32), ("coarse_degree", ctypes.c_int32), ("lanczos_steps", ctypes.c_int32),
+                ("lmin_frac", ctypes.c_double), ("lmax_factor", ctypes.c_double), ("coarse_lo", ctypes.c_double)]
+
+
+class nek_pmg_info_t(ctypes.Structure):
+    _fields_ = [("nlevels", ctypes.c_int32), ("orders", ctypes.c_int32 * PMG_MAX_LEVELS),
+                ("degree", ctypes.c_int32), ("coarse_degree", ctypes.c_int32),
+                ("n_local", ctypes.c_int64 * PMG_MAX_LEVELS), ("lam_min", ctypes.c_double * PMG_MAX_LEVELS),
+                ("lam_max", ctypes.c_double * PMG_MAX_LEVELS), ("vcycles", ctypes.c_int64)]
+
+
 _P, _I, _I64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 _sig = {
     "nek_version": ([], _I),
@@ -84,6 +100,11 @@ _sig = {
     "nek_proj_size": ([_P], _I),
     "nek_proj_reset": ([_P], _I),
     "nek_proj_free": ([_P], _I),
+    "nek_pmg_create": ([_P, _P, _D, _D, ctypes.POINTER(nek_pmg_opts), ctypes.POINTER(_P), _P], _I),
+    "nek_pmg_apply": ([_P, _P, _P, _P], _I),
+    "nek_pmg_solve": ([_P, _P, _P, _D, _I, ctypes.POINTER(_I), ctypes.POINTER(_D), _P, _P], _I),
+    "nek_pmg_info": ([_P, ctypes.POINTER(nek_pmg_info_t)], _I),
+    "nek_pmg_free": ([_P], _I),
     "nek_plan_create": ([ctypes.POINTER(_P), _I64, _I, _P, _P, _P], _I),
     "nek_plan_surface_gids": ([_P, _P], _I64),
     "nek_plan_set_ranks": ([_P, _I, _I, _P, _P], _I),
@@ -317,6 +338,71 @@ class Projection:
     def free(self):
         if self._h:
             _lib.nek_proj_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class PMG:
+    """nek_pmg_*: p-multigrid V-cycle with Chebyshev smoothing as the PCG preconditioner
+    (P:195-198).  xyz: the (3, E*(N+1)^3) coordinates given to setup.  Options (0 =
+    default): orders (schedule list), degree, coarse_degree, lanczos_steps, lmin_frac, lmax_factor,
+    coarse_lo."""
+
+    def __init__(self, ctx: Context, xyz, h1, h2, orders=None, degree=0, coarse_degree=0, lanczos_steps=0,
+                 lmin_frac=0.0, lmax_factor=0.0, coarse_lo=0.0):
+        self.ctx = ctx
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        if xyz.size != 3 * ctx.n:
+            raise ValueError("xyz must hold 3*E*(N+1)^3 entries")
+        o = nek_pmg_opts()
+        if orders:
+            o.nlevels = len(orders)
+            for i, v in enumerate(orders):
+                o.orders[i] = int(v)
+        o.degree, o.coarse_degree, o.lanczos_steps = int(degree), int(coarse_degree), int(lanczos_steps)
+        o.lmin_frac, o.lmax_factor, o.coarse_lo = float(lmin_frac), float(lmax_factor), float(coarse_lo)
+        h = ctypes.c_void_p()
+        _check(_lib.nek_pmg_create(ctx.handle, _np_ptr(xyz), float(h1), float(h2), ctypes.byref(o),
+                                   ctypes.byref(h), None), ctx.handle)
+        self._h = h
+
+    def apply(self, r, z):
+        """z = V(r)."""
+        pr, sr = _field_ptr(r, self.ctx.n, "r")
+        pz, sz = _field_ptr(z, self.ctx.n, "z", writable=True)
+        _check(_lib.nek_pmg_apply(self._h, pr, pz, _stream_of(sr, sz)), self.ctx.handle)
+        return z
+
+    def solve(self, b, x, tol, maxit, want_hist=False):
+        """-> (status, iters, relres, hist or None)"""
+        pb, sb = _field_ptr(b, self.ctx.n, "b")
+        px, sx = _field_ptr(x, self.ctx.n, "x", writable=True)
+        it = ctypes.c_int(0)
+        rr = ctypes.c_double(0.0)
+        hist = np.zeros(int(maxit) + 1) if want_hist else None
+        st = _lib.nek_pmg_solve(self._h, pb, px, float(tol), int(maxit), ctypes.byref(it), ctypes.byref(rr),
+                                _np_ptr(hist), _stream_of(sb, sx))
+        _check(st, self.ctx.handle)
+        if hist is not None:
+            hist = hist[: it.value + 1]
+        return st, it.value, rr.value, hist
+
+    def info(self) -> dict:
+        i = nek_pmg_info_t()
+        _check(_lib.nek_pmg_info(self._h, ctypes.byref(i)))
+        L = i.nlevels
+        return {"nlevels": L, "orders": list(i.orders[:L]), "degree": i.degree, "coarse_degree": i.coarse_degree,
+                "n_local": list(i.n_local[:L]), "lam_min": list(i.lam_min[:L]), "lam_max": list(i.lam_max[:L]),
+                "vcycles": i.vcycles}
+
+    def free(self):
+        if self._h:
+            _lib.nek_pmg_free(self._h)
             self._h = None
 
     def __del__(self):

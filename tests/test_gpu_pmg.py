@@ -1,0 +1,175 @@
+"""GPU parity of the p-multigrid preconditioner (NEXT #1) against the oracle (oracle/pmg.py).
+
+Tolerances: the Lanczos bounds of each level are computed independently on both sides (20 CG
+steps, different summation orders), so they agree to rounding amplified by the Lanczos
+recurrence: relative 1e-9 is asserted.  The V-cycle is a fixed polynomial in those bounds, so its
+output moves by O(degree * d(lambda)/lambda) on top of its own rounding: the test allows
+max(1e-11, 100 * observed bound difference) normwise.  Converged pMG-PCG solves must take the
+oracle's iteration count (+-1) and agree in x to 1e-8 relative (tol 1e-10)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import pmg as opmg  # noqa: E402
+from workloads import meshgen as mg  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def nek():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_19119_b200 import nek as _nek
+    return _nek
+
+
+def rel(a, b):
+    b = np.asarray(b)
+    return np.abs(np.asarray(a) - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+CASES = {
+    "N7_box": (lambda: mg.box_mesh(3, 3, 2, 7, deform="bubble"), None, (1.0, 0.0)),
+    "N7_sched731_helm": (lambda: mg.box_mesh(2, 3, 2, 7, deform="sin", eps=0.05), [7, 3, 1], (1.0, 3.0)),
+    "N5_top": (lambda: mg.box_mesh(3, 2, 3, 5, deform="bubble", dirichlet="top"), None, (1.0, 0.0)),
+    "N3_jitter": (lambda: mg.box_mesh(4, 3, 3, 3, deform="affine", jitter=0.1, seed=2), None, (1.0, 0.0)),
+    "N8": (lambda: mg.box_mesh(2, 2, 3, 8, deform="bubble"), None, (1.0, 0.0)),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def case(request, nek):
+    mk, sched, h = CASES[request.param]
+    m = mk()
+    O = oracle.Oracle.from_mesh(m)
+    Po = opmg.PMG(O, m.xyz, h[0], h[1], schedule=sched)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    Pg = nek.PMG(ctx, m.xyz, h[0], h[1], orders=sched)
+    yield m, O, Po, ctx, Pg, h
+    Pg.free()
+    nek.free(ctx)
+
+
+def _lam_diff(Po, Pg):
+    info = Pg.info()
+    assert info["orders"] == [L.N for L in Po.levels]
+    d = 0.0
+    for l, L in enumerate(Po.levels):
+        d = max(d, abs(info["lam_max"][l] - L.lam_max) / L.lam_max, abs(info["lam_min"][l] - L.lam_min) / L.lam_max)
+    return d
+
+
+def test_level_bounds(case):
+    m, O, Po, ctx, Pg, h = case
+    assert _lam_diff(Po, Pg) <= 1e-9
+
+
+def test_vcycle_parity(case):
+    m, O, Po, ctx, Pg, h = case
+    rng = np.random.default_rng(5)
+    r = oracle.mask(m.mask, O.gs_apply(rng.standard_normal(O.n)))
+    z = np.empty(O.n)
+    Pg.apply(r, z)
+    want = Po.apply(r)
+    tol = max(1e-11, 100 * _lam_diff(Po, Pg))
+    assert rel(z, want) <= tol
+    zd = torch.empty(O.n, dtype=torch.float64, device="cuda")
+    Pg.apply(torch.from_numpy(r).cuda(), zd)
+    assert np.array_equal(zd.cpu().numpy(), z)          # host and device calls: same bits
+
+
+def test_pmg_pcg_converged_parity(case):
+    m, O, Po, ctx, Pg, h = case
+    b = mg.smooth_field(m, seed=3)
+    xo, ito, sto, ho = opmg.pcg(O, h[0], h[1], b, 1e-10, 200, Po.apply)
+    x = np.zeros(O.n)
+    st, it, rr, hg = Pg.solve(b, x, 1e-10, 200, want_hist=True)
+    assert st == 0 and sto == 0
+    assert abs(it - ito) <= 1
+    assert rel(x, xo) <= 1e-8
+    k = min(it, ito) + 1
+    assert np.abs(hg[:k] - ho[:k]).max() <= 1e-8
+    # Jacobi-PCG on the same context still works and agrees with the pMG solution
+    xj = np.zeros(O.n)
+    stj, itj, _, _ = nek_pcg(ctx, h, b, xj)
+    assert stj == 0 and it < itj and rel(xj, x) <= 1e-7
+
+
+def nek_pcg(ctx, h, b, x):
+    from paper_2409_19119_b200 import nek as _nek
+    st, it, rr, _ = _nek.pcg_solve(ctx, h[0], h[1], b, x, 1e-10, 5000)
+    return st, it, rr, None
+
+
+def test_zero_rhs(case):
+    m, O, Po, ctx, Pg, h = case
+    x = np.ones(O.n)
+    st, it, rr, _ = Pg.solve(np.zeros(O.n), x, 1e-10, 50)
+    assert st == 0 and it == 0 and np.all(x == 0.0)
+    z = np.ones(O.n)
+    Pg.apply(np.zeros(O.n), z)
+    assert np.all(z == 0.0)
+
+
+def test_pmg_full_size_symmetry_and_iterations(nek):
+    """Config 2 (16^3, N = 7), the size bench.py times: the V-cycle is symmetric in the owner
+    inner product (property at any size) and pMG-PCG converges in far fewer iterations than
+    Jacobi-PCG (665 oracle iterations)."""
+    m = mg.config_mesh(2)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        Pg = nek.PMG(ctx, m.xyz, 1.0, 0.0)
+        owner = oracle.owner_flags(m.gid) != 0
+        rng = np.random.default_rng(1)
+        mult = oracle.multiplicity(m.gid)
+        u = np.zeros(m.n_local); v = np.zeros(m.n_local)
+        for a in (u, v):
+            g = rng.standard_normal(m.n_local)
+            a[:] = g
+            nek.gs(ctx, a)
+            a /= mult
+            a[m.mask != 0] = 0.0
+        zu, zv = np.empty_like(u), np.empty_like(v)
+        Pg.apply(u, zu)
+        Pg.apply(v, zv)
+        a1, a2 = np.dot(zu[owner], v[owner]), np.dot(u[owner], zv[owner])
+        assert abs(a1 - a2) <= 1e-11 * abs(a1)
+        b = mg.smooth_field(m, seed=1)
+        x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+        st, it, rr, _ = Pg.solve(torch.from_numpy(b).cuda(), x, 1e-10, 300)
+        assert st == 0 and it < 60 and rr <= 1e-10
+        Pg.free()
+    finally:
+        nek.free(ctx)
+
+
+def test_pmg_errors(nek):
+    from paper_2409_19119_b200.nek import NekError
+    m = mg.box_mesh(2, 2, 2, 5, deform="bubble")
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        for orders in ([5, 3], [4, 3, 1], [5, 5, 1], [5, 3, 4, 1]):
+            with pytest.raises(NekError) as ei:
+                nek.PMG(ctx, m.xyz, 1.0, 0.0, orders=orders)
+            assert ei.value.code == -1
+        with pytest.raises(NekError):
+            nek.PMG(ctx, m.xyz, 0.0, 1.0)
+    finally:
+        nek.free(ctx)
+    # one Dirichlet node inside a face (all its copies): the mask is not entity-wise
+    bad = m.mask.copy()
+    q = np.arange(m.n_local) % (m.N + 1) ** 3
+    i, j, k = q % (m.N + 1), (q // (m.N + 1)) % (m.N + 1), q // (m.N + 1) ** 2
+    inner = lambda a: (a > 0) & (a < m.N)  # noqa: E731
+    face = (i == 0) & inner(j) & inner(k) & (bad == 0)
+    g = m.gid[np.nonzero(face)[0][0]]
+    bad[m.gid == g] = 1
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, bad, device=0)
+    try:
+        with pytest.raises(NekError) as ei:
+            nek.PMG(ctx, m.xyz, 1.0, 0.0)
+        assert ei.value.code == -1
+    finally:
+        nek.free(ctx)

@@ -29,6 +29,7 @@ ap.add_argument("--rod-layers", type=int, default=3)
 ap.add_argument("--h2", type=float, default=0.0)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--graph", action="store_true", help="profile the CUDA-graph path (default: eager launches)")
+ap.add_argument("--tag", default="")
 a = ap.parse_args()
 rank, world, local = bench.rank_env()
 torch.cuda.set_device(local)
@@ -61,7 +62,7 @@ ev.sort(key=lambda e: e["ts"])
 t0 = ev[0]["ts"] if ev else 0.0
 recs = [{"name": e["name"].split("(")[0].replace("void ", "").replace("nekb200::", "").split("<")[0],
          "stream": e["args"].get("stream"), "t": round(e["ts"] - t0, 2), "d": round(e["dur"], 2)} for e in ev]
-json.dump(recs, open(f"gpurun_out/timeline_r{rank}.json", "w"))
+json.dump(recs, open(f"gpurun_out/timeline{a.tag}_r{rank}.json", "w"))
 os.remove(path)
 # per-iteration summary: iterations delimited by the update kernel on the main stream
 busy = collections.defaultdict(float)
