@@ -619,8 +619,11 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         CK(upload(ctx, &ctx->gsi_idx, idx)); CK(upload(ctx, &ctx->gsi_perm, gp)); CK(upload(ctx, &ctx->gsi_offs, go));
         // off by default: measured slower (the partner gathers are dependent loads inside a
         // streaming kernel, and miss L2 at scale); NEK_GS_INLINE=1 turns it on
+        // boundary Ax + halo send beside the interior Ax (concurrent streams) pays off for small
+        // per-rank problems, where the boundary launch alone would leave most SMs idle; for large
+        // ones the send must not queue behind the persistent interior grid (measured)
         const char *cenv = getenv("NEK_CONCURRENT_BND");
-        ctx->concurrent_bnd = cenv && std::strcmp(cenv, "1") == 0;
+        ctx->concurrent_bnd = cenv ? std::strcmp(cenv, "1") == 0 : E < 16384;
         const char *genv = getenv("NEK_GS_INLINE");
         ctx->gs_inline = genv && std::strcmp(genv, "1") == 0;
     }
