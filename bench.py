@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--ez", type=int, default=EZ_PER_RANK, help="element layers per rank")
     ap.add_argument("--order", type=int, default=NORD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pmg", action="store_true", help="skip the Jacobi vs pMG time-to-solution section")
     ap.add_argument("--variant", type=int, default=0, help="Ax kernel variant (nek_set_variant; 0 = default)")
     ap.add_argument("--mesh", default="box", choices=["box", "rod"],
                     help="box: 16x16xez elements per GPU (config 2 at ez=16); rod: 17x17-pin rod bundle, "
@@ -309,11 +310,45 @@ def main():
     torch.cuda.synchronize(); barrier()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
 
+    # ---- time to solution, Jacobi-PCG vs pMG-PCG (NEXT #1), outside the headline metric
+    pmg = None
+    pm = [0.0, 0.0, 0.0]
+    if not args.no_pmg:
+        tol = 1e-8
+        P = nek.PMG(ctx, mesh.xyz, 1.0, args.h2)
+        P.solve(b, x, tol, 500)
+        nek.pcg_solve(ctx, 1.0, args.h2, b, x, tol, 5000)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        barrier(); torch.cuda.synchronize()
+        evs[0].record(stream)
+        _, itj, _, _ = nek.pcg_solve(ctx, 1.0, args.h2, b, x, tol, 5000)
+        evs[1].record(stream)
+        evs[2].record(stream)
+        pst, itp, prr, _ = P.solve(b, x, tol, 500)
+        evs[3].record(stream)
+        z = torch.empty_like(b)
+        evs[4].record(stream)
+        P.apply(b, z)
+        evs[5].record(stream)
+        torch.cuda.synchronize(); barrier()
+        pm = [evs[0].elapsed_time(evs[1]), evs[2].elapsed_time(evs[3]), evs[4].elapsed_time(evs[5])]
+        pinfo = P.info()
+        P.free()
+        pmg = {"tol": tol, "orders": pinfo["orders"], "degree": pinfo["degree"],
+               "coarse_degree": pinfo["coarse_degree"], "iters": itp, "jacobi_iters": itj}
+    log("pmg done")
+
     # ---- max over ranks
-    vals = torch.tensor([t_ms, ax_ms, e2e_s], dtype=torch.float64, device=dev)
+    vals = torch.tensor([t_ms, ax_ms, e2e_s] + pm, dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    t_ms, ax_ms, e2e_s = [float(v) for v in vals.cpu()]
+    t_ms, ax_ms, e2e_s = [float(v) for v in vals.cpu()[:3]]
+    pm = [float(v) for v in vals.cpu()[3:]]
+    if pmg is not None:
+        pmg.update({"ms": pm[1], "jacobi_ms": pm[0], "speedup": pm[0] / pm[1] if pm[1] > 0 else None,
+                    "ms_per_vcycle": pm[2],
+                    "note": "time to ||r|| <= 1e-8 ||b|| on the same mesh and right-hand side, CUDA events, "
+                            "max over ranks; pMG schedule / Chebyshev degrees as listed (DESIGN.md readings P1-P7)"})
     n_dof_total = mesh.n_dof * world
     value = n_dof_total * args.iters * args.steps / (t_ms * 1e-3) / 1e9
     ax_gdofs = n_dof_total * reps / (ax_ms * 1e-3) / 1e9
@@ -340,7 +375,9 @@ def main():
             except Exception:
                 pass
             roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                        "traffic": traffic, "kernel": "ax_v5 (SEM Helmholtz apply, fused PCG prologue)",
+                        "traffic": traffic,
+                        "kernel": ("ax_v5 (SEM Helmholtz apply, DMMA, fused PCG prologue)" if args.order == 7 else
+                                   "ax_v6 (SEM Helmholtz apply, TMA metric ring, fused PCG prologue)"),
                         "peak_source": peak_src, "algorithmic_bytes_per_launch": per_launch_bytes,
                         "avg_launch_ms": per_launch_ms,
                         "share_of_step": stats["ax_ms"] / kt_ms if kt_ms else None,
@@ -364,7 +401,7 @@ def main():
             "gpu_launches": int(launch_stats["launches"]),
             "e2e": {"value": n_dof_total * args.iters / e2e_s / 1e9, "unit": "GDOF/s",
                     "h2d_bytes_per_step": mesh.n_local * 8, "d2h_bytes_per_step": mesh.n_local * 8},
-            "roofline": roofline, "clocks": clocks,
+            "roofline": roofline, "clocks": clocks, "pmg": pmg,
             "halo": {"doubles_per_gs": info["halo_doubles"], "neighbors": info["n_neighbors"],
                      "transport": {0: "none", 1: "nccl", 2: "nvlink-p2p"}[info["transport"]]},
         }

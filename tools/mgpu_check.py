@@ -58,9 +58,20 @@ def main():
         b = mg.smooth_field(m, seed=3)[loc]
         xd = torch.zeros_like(ud)
         st, it, rr, hist = nek.pcg_solve(ctx, 1.0, 0.0, torch.from_numpy(b).to(dev), xd, 0.0, 40, want_hist=True)
+        # p-multigrid (NEXT #1): one V-cycle of M QQ^T u and a converged pMG-PCG solve
+        P = nek.PMG(ctx, sub.xyz, 1.0, 0.0)
+        rd = vd.clone()
+        rd[torch.from_numpy(sub.mask != 0).to(dev)] = 0.0
+        zd = torch.empty_like(rd)
+        P.apply(rd, zd)
+        xpd = torch.zeros_like(ud)
+        pst, pit, prr, _ = P.solve(torch.from_numpy(b).to(dev), xpd, 1e-10, 200)
+        pinfo = P.info()
+        P.free()
         torch.cuda.synchronize()
         payload = {"w": wd.cpu().numpy(), "v": vd.cpu().numpy(), "x": xd.cpu().numpy(), "hist": hist, "it": it,
-                   "info": info}
+                   "info": info, "z": zd.cpu().numpy(), "xp": xpd.cpu().numpy(), "pit": pit, "pst": pst,
+                   "lam": pinfo["lam_max"] + pinfo["lam_min"]}
         gathered = [None] * world
         dist.all_gather_object(gathered, payload)
         if rank == 0:
@@ -89,13 +100,33 @@ def main():
             order = np.argsort(allg, kind="stable")
             sg, sw = allg[order], allw[order]
             same = np.all((sg[1:] != sg[:-1]) | (sw[1:] == sw[:-1]))
-            case_ok = ax_err <= 1e-12 and gs_bit and gs_err <= 1e-14 and hist_ok and x_err <= 1e-10 and bool(same)
+            # pMG against the single-rank oracle hierarchy on the whole mesh
+            from oracle import pmg as opmg
+            Po = opmg.PMG(O, m.xyz, 1.0, 0.0)
+            lam_o = [L.lam_max for L in Po.levels] + [L.lam_min for L in Po.levels]
+            lam_diff = max(abs(a - b_) / max(lam_o[:len(Po.levels)]) for pl in gathered for a, b_ in zip(pl["lam"], lam_o))
+            rf = oracle.mask(m.mask, O.gs_apply(uf))
+            zref = Po.apply(rf)
+            zgot = np.zeros(m.n_local); xpgot = np.zeros(m.n_local)
+            for r_, pl in enumerate(gathered):
+                lr = (parts[r_][:, None] * P3 + np.arange(P3)).reshape(-1)
+                zgot[lr] = pl["z"]; xpgot[lr] = pl["xp"]
+            z_err = float(np.abs(zgot - zref).max() / np.abs(zref).max())
+            xpo, pito, psto, _ = opmg.pcg(O, 1.0, 0.0, bf, 1e-10, 200, Po.apply)
+            xp_err = float(np.abs(xpgot - xpo).max() / np.abs(xpo).max())
+            pmg_ok = (lam_diff <= 1e-9 and z_err <= max(1e-11, 100 * lam_diff) and xp_err <= 1e-8
+                      and all(abs(pl["pit"] - pito) <= 1 and pl["pst"] == 0 for pl in gathered))
+            case_ok = (ax_err <= 1e-12 and gs_bit and gs_err <= 1e-14 and hist_ok and x_err <= 1e-10 and bool(same)
+                       and pmg_ok)
             ok &= case_ok
             results[name] = {"ax_err": ax_err, "gs_bitexact_vs_multirank_oracle": gs_bit, "gs_err_vs_1rank": gs_err,
                              "hist_ok": hist_ok, "x_err": x_err, "copies_identical": bool(same), "iters": ito,
                              "halo_doubles": [pl["info"]["halo_doubles"] for pl in gathered],
                              "neighbors": [pl["info"]["n_neighbors"] for pl in gathered],
-                             "transport": [pl["info"]["transport"] for pl in gathered], "ok": case_ok}
+                             "transport": [pl["info"]["transport"] for pl in gathered],
+                             "pmg": {"lam_diff": lam_diff, "vcycle_err": z_err, "x_err": xp_err, "iters_oracle": pito,
+                                     "iters": [pl["pit"] for pl in gathered], "ok": bool(pmg_ok)},
+                             "ok": case_ok}
         nek.free(ctx)
     if rank == 0:
         print(json.dumps({"world": world, "ok": bool(ok), "cases": results}))
