@@ -312,7 +312,7 @@ def main():
 
     # ---- time to solution, Jacobi-PCG vs pMG-PCG (NEXT #1), outside the headline metric
     pmg = None
-    pm = [0.0, 0.0, 0.0]
+    pm = [0.0] * 5
     if not args.no_pmg:
         tol = 1e-8
         P = nek.PMG(ctx, mesh.xyz, 1.0, args.h2)
@@ -334,6 +334,22 @@ def main():
         pm = [evs[0].elapsed_time(evs[1]), evs[2].elapsed_time(evs[3]), evs[4].elapsed_time(evs[5])]
         pinfo = P.info()
         P.free()
+        itp32 = None
+        if args.order <= 9:     # FP32 preconditioner (NEXT #3), same schedule
+            P32 = nek.PMG(ctx, mesh.xyz, 1.0, args.h2, precision=1)
+            P32.solve(b, x, tol, 500)
+            barrier(); torch.cuda.synchronize()
+            evs[2].record(stream)
+            _, itp32, _, _ = P32.solve(b, x, tol, 500)
+            evs[3].record(stream)
+            evs[4].record(stream)
+            P32.apply(b, z)
+            evs[5].record(stream)
+            torch.cuda.synchronize(); barrier()
+            pm += [evs[2].elapsed_time(evs[3]), evs[4].elapsed_time(evs[5])]
+            P32.free()
+        else:
+            pm += [0.0, 0.0]
         pmg = {"tol": tol, "orders": pinfo["orders"], "degree": pinfo["degree"],
                "coarse_degree": pinfo["coarse_degree"], "iters": itp, "jacobi_iters": itj}
     log("pmg done")
@@ -347,6 +363,8 @@ def main():
     if pmg is not None:
         pmg.update({"ms": pm[1], "jacobi_ms": pm[0], "speedup": pm[0] / pm[1] if pm[1] > 0 else None,
                     "ms_per_vcycle": pm[2],
+                    "fp32": {"iters": itp32, "ms": pm[3], "ms_per_vcycle": pm[4],
+                             "speedup_vs_fp64_pmg": pm[1] / pm[3] if pm[3] > 0 else None},
                     "note": "time to ||r|| <= 1e-8 ||b|| on the same mesh and right-hand side, CUDA events, "
                             "max over ranks; pMG schedule / Chebyshev degrees as listed (DESIGN.md readings P1-P7)"})
     n_dof_total = mesh.n_dof * world

@@ -211,11 +211,15 @@ typedef struct {
     int32_t orders[NEK_PMG_MAX_LEVELS];
     int32_t degree, coarse_degree, lanczos_steps;
     double lmin_frac, lmax_factor, coarse_lo;
+    int32_t precision;         /* 0: FP64; 1: FP32 preconditioner (NEXT #3):
+                                  every level's metric factors, diagonal, transfer matrix
+                                  and work vectors in single precision, r converted on
+                                  entry and z on exit; the outer CG stays FP64; N <= 9 */
 } nek_pmg_opts;
 typedef struct {
     int32_t nlevels;
     int32_t orders[NEK_PMG_MAX_LEVELS];
-    int32_t degree, coarse_degree;
+    int32_t degree, coarse_degree, precision;
     int64_t n_local[NEK_PMG_MAX_LEVELS];
     double lam_min[NEK_PMG_MAX_LEVELS], lam_max[NEK_PMG_MAX_LEVELS];
     int64_t vcycles;           /* V-cycles applied so far                         */

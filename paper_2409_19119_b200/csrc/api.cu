@@ -184,23 +184,31 @@ static P2PMail mail_of(const nek_ctx *ctx)
     return m;
 }
 
-static int halo_start(nek_ctx *ctx, const double *v, const int *done, cudaStream_t strm = nullptr)
+template <class T> static ncclDataType_t nccl_type();
+template <> ncclDataType_t nccl_type<double>() { return ncclDouble; }
+template <> ncclDataType_t nccl_type<float>() { return ncclFloat; }
+
+// halo buffers are allocated as doubles; FP32 levels (NEXT #3) use them as floats (same slot counts)
+template <class T> static T *as(double *p) { return reinterpret_cast<T *>(p); }
+
+template <class T>
+static int halo_start(nek_ctx *ctx, const T *v, const int *done, cudaStream_t strm = nullptr)
 {
     if (!strm) strm = ctx->s_main;
     if (ctx->p2p) {   // interface partials written straight into the neighbours' buffers over NVLink
         Scope sc(ctx, CLS_HALO, strm);
-        CK(launch_gs_pack_p2p_fused(ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots, ctx->send_run,
-                                    ctx->d_slot_nbr, ctx->d_peer_recv, ctx->d_remote_off, ctx->d_send_offs,
-                                    ctx->d_remote_half, (int)ctx->neighbors.size(), ctx->rank, ctx->d_peer_hflags,
-                                    ctx->epochs, ctx->counter + 3, done, strm));
+        CK(launch_gs_pack_p2p_fused<T>(ctx->ifc_perm, ctx->ifc_offs, v, as<T>(ctx->ifc_partial), ctx->nslots,
+                                       ctx->send_run, ctx->d_slot_nbr, ctx->d_peer_recv, ctx->d_remote_off,
+                                       ctx->d_send_offs, ctx->d_remote_half, (int)ctx->neighbors.size(), ctx->rank,
+                                       ctx->d_peer_hflags, ctx->epochs, ctx->counter + 3, done, strm));
         ctx->stats.launches += 1;
         ctx->stats.halo_launches += 1;
         return NEK_OK;
     }
     {
         Scope sc(ctx, CLS_HALO, strm);
-        CK(launch_gs_ifc_pack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, v, ctx->ifc_partial, ctx->nslots,
-                              ctx->send_run, ctx->sendbuf, done, strm));
+        CK(launch_gs_ifc_pack<T>(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, v, as<T>(ctx->ifc_partial), ctx->nslots,
+                                 ctx->send_run, as<T>(ctx->sendbuf), done, strm));
         ctx->stats.launches += (ctx->nifc > 0) + (ctx->nslots > 0);
         ctx->stats.halo_launches += 1;
     }
@@ -209,35 +217,40 @@ static int halo_start(nek_ctx *ctx, const double *v, const int *done, cudaStream
     NK(ncclGroupStart());
     for (size_t k = 0; k < ctx->neighbors.size(); ++k) {
         size_t cnt = (size_t)(ctx->send_offs[k + 1] - ctx->send_offs[k]);
-        NK(ncclSend(ctx->sendbuf + ctx->send_offs[k], cnt, ncclDouble, ctx->neighbors[k], ctx->nccl, ctx->s_comm));
-        NK(ncclRecv(ctx->recvbuf + ctx->send_offs[k], cnt, ncclDouble, ctx->neighbors[k], ctx->nccl, ctx->s_comm));
+        NK(ncclSend(as<T>(ctx->sendbuf) + ctx->send_offs[k], cnt, nccl_type<T>(), ctx->neighbors[k], ctx->nccl,
+                    ctx->s_comm));
+        NK(ncclRecv(as<T>(ctx->recvbuf) + ctx->send_offs[k], cnt, nccl_type<T>(), ctx->neighbors[k], ctx->nccl,
+                    ctx->s_comm));
     }
     NK(ncclGroupEnd());
     CK(cudaEventRecord(ctx->ev_join, ctx->s_comm));
     return NEK_OK;
 }
 
-static int halo_finish(nek_ctx *ctx, double *v, const int *done)
+template <class T>
+static int halo_finish(nek_ctx *ctx, T *v, const int *done)
 {
     CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_join, 0));
     Scope sc(ctx, CLS_HALO);
-    CK(launch_gs_ifc_unpack(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, ctx->coffs, ctx->contrib, ctx->ifc_partial,
-                            ctx->recvbuf, v, done, ctx->s_main));
+    CK(launch_gs_ifc_unpack<T>(ctx->nifc, ctx->ifc_perm, ctx->ifc_offs, ctx->coffs, ctx->contrib,
+                               as<T>(ctx->ifc_partial), as<T>(ctx->recvbuf), v, done, ctx->s_main));
     ctx->stats.launches += (ctx->nifc > 0);
     return NEK_OK;
 }
 
-static int do_gs_local(nek_ctx *ctx, double *v, const int *done)
+template <class T>
+static int do_gs_local(nek_ctx *ctx, T *v, const int *done)
 {
     Scope sc(ctx, CLS_GS);
-    CK(launch_gs_classes(ctx->gsc, v, done, ctx->s_main));
+    CK(launch_gs_classes<T>(ctx->gsc, v, done, ctx->s_main));
     ctx->stats.gs_launches += 1;
     ctx->stats.launches += (ctx->nruns > 0);
     return NEK_OK;
 }
 
 // P2P: the local runs and the halo unpack (which waits for the neighbours' data) in one launch
-static int gs_local_and_unpack_p2p(nek_ctx *ctx, double *v, const int *done, bool skip_local = false)
+template <class T>
+static int gs_local_and_unpack_p2p(nek_ctx *ctx, T *v, const int *done, bool skip_local = false)
 {
     Scope sc(ctx, CLS_GS);
     HaloUnpack U;
@@ -245,20 +258,21 @@ static int gs_local_and_unpack_p2p(nek_ctx *ctx, double *v, const int *done, boo
     U.contrib = ctx->contrib; U.nbr = ctx->d_nbr; U.partial = ctx->ifc_partial; U.recv = ctx->recv2;
     U.half = std::max<int64_t>(ctx->nslots, 1); U.hflags = ctx->hflags; U.epochs = ctx->epochs; U.nnbr = (int)ctx->neighbors.size();
     U.err = ctx->p2p_err;
-    CK(launch_gs_classes_unpack(skip_local ? GsClasses() : ctx->gsc, U, v, done, ctx->s_main));
+    CK(launch_gs_classes_unpack<T>(skip_local ? GsClasses() : ctx->gsc, U, v, done, ctx->s_main));
     ctx->stats.gs_launches += 1;
     ctx->stats.launches += 1;
     return NEK_OK;
 }
 
 // v <- QQ^T v (global)
-static int gs_full(nek_ctx *ctx, double *v, const int *done)
+template <class T>
+static int gs_full(nek_ctx *ctx, T *v, const int *done)
 {
     int st;
-    if (ctx->nranks > 1 && (st = halo_start(ctx, v, done)) != NEK_OK) return st;
-    if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, v, done);
-    if ((st = do_gs_local(ctx, v, done)) != NEK_OK) return st;
-    if (ctx->nranks > 1 && (st = halo_finish(ctx, v, done)) != NEK_OK) return st;
+    if (ctx->nranks > 1 && (st = halo_start<T>(ctx, v, done)) != NEK_OK) return st;
+    if (ctx->p2p) return gs_local_and_unpack_p2p<T>(ctx, v, done);
+    if ((st = do_gs_local<T>(ctx, v, done)) != NEK_OK) return st;
+    if (ctx->nranks > 1 && (st = halo_finish<T>(ctx, v, done)) != NEK_OK) return st;
     return NEK_OK;
 }
 

@@ -21,10 +21,16 @@
 namespace nekb200 {
 
 __constant__ double c_D[16][256];   // D for every order N (row-major, (N+1)^2 used)
+__constant__ float c_Df[16][256];   // the same in FP32 (reduced-precision pMG levels, NEXT #3)
 
 cudaError_t upload_D(int N, const double *D)
 {
-    return cudaMemcpyToSymbol(c_D, D, sizeof(double) * (N + 1) * (N + 1), sizeof(double) * 256 * N,
+    cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * (N + 1) * (N + 1), sizeof(double) * 256 * N,
+                                       cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    float Df[256];
+    for (int i = 0; i < (N + 1) * (N + 1); ++i) Df[i] = (float)D[i];
+    return cudaMemcpyToSymbol(c_Df, Df, sizeof(float) * (N + 1) * (N + 1), sizeof(float) * 256 * N,
                               cudaMemcpyHostToDevice);
 }
 
@@ -1349,6 +1355,24 @@ int64_t ax_grid(int variant, int N, int64_t nelem)
 }
 
 // enough partial slots for any variant (two concurrent launches of up to 4 CTAs per SM each)
+// FP32 Ax (v6) on all elements, for the reduced-precision pMG levels; N <= 9
+cudaError_t launch_ax_f(int N, int64_t E, const float *u, const float *Gf, const float *wJf, const uint32_t *mbits,
+                        double h1, double h2, float *w, cudaStream_t s)
+{
+    if (E <= 0) return cudaSuccess;
+    switch (N + 1) {
+#define NEK_CASE(NQ)                                                                         \
+    case NQ:                                                                                 \
+        return h2 != 0.0 ? ax_v6_launch_f<NQ, true>(E, u, Gf, wJf, mbits, h1, h2, w, s)   \
+                         : ax_v6_launch_f<NQ, false>(E, u, Gf, wJf, mbits, h1, h2, w, s);
+        NEK_CASE(2) NEK_CASE(3) NEK_CASE(4) NEK_CASE(5) NEK_CASE(6) NEK_CASE(7) NEK_CASE(8) NEK_CASE(9) NEK_CASE(10)
+#undef NEK_CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+int ax_gstride_f(int N) { return ((6 * (N + 1) * (N + 1) * (N + 1) + 3) / 4) * 4; }
+
 int ax_partials_needed(int variant, int N, int64_t E)
 {
     return (int)std::max<int64_t>(std::max<int64_t>(2 * ax_grid(variant, N, E), E), 2 * 4 * 148);
@@ -1507,11 +1531,12 @@ constexpr int GS_PAIRS_PER_THREAD = 8, GS_QUADS_PER_THREAD = 4;
 // Each warp takes a contiguous block of runs of one class and lane l handles
 // runs l, l+32, ... of it, so every warp-wide load touches consecutive runs
 // (first-touch order keeps their copies close in memory).
+template <class T>
 __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n2, const int2 *__restrict__ p2,
                                                 int64_t n4, const int4 *__restrict__ p4, int64_t n8,
                                                 const int4 *__restrict__ p8, int64_t ng,
                                                 const int32_t *__restrict__ pg, const int32_t *__restrict__ og,
-                                                double *__restrict__ v)
+                                                T *__restrict__ v)
 {
     const int64_t w2 = (n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD);
     const int64_t w4 = (n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD);
@@ -1519,7 +1544,7 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
     if (wid < w2) {
         const int64_t r0 = wid * 32 * GS_PAIRS_PER_THREAD + lane;
         int2 c[GS_PAIRS_PER_THREAD];
-        double a[GS_PAIRS_PER_THREAD], b[GS_PAIRS_PER_THREAD];
+        T a[GS_PAIRS_PER_THREAD], b[GS_PAIRS_PER_THREAD];
 #pragma unroll
         for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (r0 + 32 * q < n2) c[q] = p2[r0 + 32 * q];
 #pragma unroll
@@ -1527,14 +1552,14 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
             if (r0 + 32 * q < n2) { a[q] = v[c[q].x]; b[q] = v[c[q].y]; }
 #pragma unroll
         for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
-            if (r0 + 32 * q < n2) { const double s = a[q] + b[q]; v[c[q].x] = s; v[c[q].y] = s; }
+            if (r0 + 32 * q < n2) { const T s = a[q] + b[q]; v[c[q].x] = s; v[c[q].y] = s; }
         return;
     }
     wid -= w2;
     if (wid < w4) {
         const int64_t r0 = wid * 32 * GS_QUADS_PER_THREAD + lane;
         int4 c[GS_QUADS_PER_THREAD];
-        double a[GS_QUADS_PER_THREAD][4];
+        T a[GS_QUADS_PER_THREAD][4];
 #pragma unroll
         for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (r0 + 32 * q < n4) c[q] = p4[r0 + 32 * q];
 #pragma unroll
@@ -1543,7 +1568,7 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
 #pragma unroll
         for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
             if (r0 + 32 * q < n4) {
-                const double s = ((a[q][0] + a[q][1]) + a[q][2]) + a[q][3];
+                const T s = ((a[q][0] + a[q][1]) + a[q][2]) + a[q][3];
                 v[c[q].x] = s; v[c[q].y] = s; v[c[q].z] = s; v[c[q].w] = s;
             }
         return;
@@ -1553,7 +1578,7 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
         const int64_t r = wid * 32 + lane;
         if (r >= n8) return;
         const int4 a = p8[2 * r], b = p8[2 * r + 1];
-        const double s = ((((((v[a.x] + v[a.y]) + v[a.z]) + v[a.w]) + v[b.x]) + v[b.y]) + v[b.z]) + v[b.w];
+        const T s = ((((((v[a.x] + v[a.y]) + v[a.z]) + v[a.w]) + v[b.x]) + v[b.y]) + v[b.z]) + v[b.w];
         v[a.x] = s; v[a.y] = s; v[a.z] = s; v[a.w] = s;
         v[b.x] = s; v[b.y] = s; v[b.z] = s; v[b.w] = s;
         return;
@@ -1562,16 +1587,17 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
     const int64_t r = wid * 32 + lane;
     if (r < ng) {
         const int o0 = og[r], o1 = og[r + 1];
-        double s = v[pg[o0]];
+        T s = v[pg[o0]];
         for (int c = o0 + 1; c < o1; ++c) s += v[pg[c]];
         for (int c = o0; c < o1; ++c) v[pg[c]] = s;
     }
 }
 
+template <class T>
 __global__ void __launch_bounds__(256)
     gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
                       const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
-                      const int32_t *__restrict__ og, double *__restrict__ v, const int *done)
+                      const int32_t *__restrict__ og, T *__restrict__ v, const int *done)
 {
     if (done && *(volatile const int *)done) return;
     gs_classes_body((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, n2, p2, n4, p4, n8, p8,
@@ -1587,10 +1613,11 @@ static int64_t gs_class_warps(const GsClasses &C)
 // local runs (warps [0, cw)) and, after them, the halo unpack (warps [cw, ...)):
 // one lane per interface run waits for this epoch's halo of every neighbour,
 // folds the contributions in rank order and writes the total to the local copies.
+template <class T>
 __global__ void __launch_bounds__(256)
     gs_classes_unpack_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4,
                              int64_t n8, const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
-                             const int32_t *__restrict__ og, int64_t cw, HaloUnpack U, double *__restrict__ v,
+                             const int32_t *__restrict__ og, int64_t cw, HaloUnpack U, T *__restrict__ v,
                              const int *done)
 {
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1607,18 +1634,20 @@ __global__ void __launch_bounds__(256)
     if (skip) return;
     const int64_t r = (wid - cw) * 32 + lane;
     if (r >= U.nifc) return;
-    const double *recv = U.recv + (int64_t)(e & 1) * U.half;
+    const T *recv = reinterpret_cast<const T *>(U.recv) + (int64_t)(e & 1) * U.half;
+    const T *partial = reinterpret_cast<const T *>(U.partial);
     const int c0 = U.coffs[r], c1 = U.coffs[r + 1];
     int src = U.contrib[c0];
-    double s = src < 0 ? U.partial[r] : ((volatile const double *)recv)[src];
+    T s = src < 0 ? partial[r] : ((volatile const T *)recv)[src];
     for (int c = c0 + 1; c < c1; ++c) {
         src = U.contrib[c];
-        s += src < 0 ? U.partial[r] : ((volatile const double *)recv)[src];
+        s += src < 0 ? partial[r] : ((volatile const T *)recv)[src];
     }
     for (int c = U.offs[r]; c < U.offs[r + 1]; ++c) v[U.perm[c]] = s;
 }
 
-cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, double *v, const int *done,
+template <class T>
+cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, T *v, const int *done,
                                      cudaStream_t s)
 {
     const int64_t cw = gs_class_warps(C), uw = (U.nifc + 31) / 32;
@@ -1629,7 +1658,8 @@ cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, do
     return cudaGetLastError();
 }
 
-cudaError_t launch_gs_classes(const GsClasses &C, double *v, const int *done, cudaStream_t s)
+template <class T>
+cudaError_t launch_gs_classes(const GsClasses &C, T *v, const int *done, cudaStream_t s)
 {
     const int64_t warps = gs_class_warps(C);
     if (warps <= 0) return cudaSuccess;
@@ -1638,28 +1668,31 @@ cudaError_t launch_gs_classes(const GsClasses &C, double *v, const int *done, cu
     return cudaGetLastError();
 }
 
+template <class T>
 __global__ void gs_ifc_partial_kernel(int64_t nifc, const int32_t *__restrict__ perm, const int32_t *__restrict__ offs,
-                                      const double *__restrict__ v, double *__restrict__ partial, const int *done)
+                                      const T *__restrict__ v, T *__restrict__ partial, const int *done)
 {
     if (done && *(volatile const int *)done) return;
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= nifc) return;
     const int o0 = offs[r], o1 = offs[r + 1];
-    double s = v[perm[o0]];
+    T s = v[perm[o0]];
     for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
     partial[r] = s;
 }
 
-__global__ void gs_pack_kernel(int64_t nslots, const int32_t *__restrict__ send_run, const double *__restrict__ partial,
-                               double *__restrict__ sendbuf, const int *done)
+template <class T>
+__global__ void gs_pack_kernel(int64_t nslots, const int32_t *__restrict__ send_run, const T *__restrict__ partial,
+                               T *__restrict__ sendbuf, const int *done)
 {
     if (done && *(volatile const int *)done) return;
     const int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (sidx < nslots) sendbuf[sidx] = partial[send_run[sidx]];
 }
 
-cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t *offs, const double *v,
-                               double *partial, int64_t nslots, const int32_t *send_run, double *sendbuf,
+template <class T>
+cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t *offs, const T *v,
+                               T *partial, int64_t nslots, const int32_t *send_run, T *sendbuf,
                                const int *done, cudaStream_t s)
 {
     if (nifc > 0) gs_ifc_partial_kernel<<<(unsigned)((nifc + 255) / 256), 256, 0, s>>>(nifc, perm, offs, v, partial, done);
@@ -1669,10 +1702,11 @@ cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t 
 
 // total = fold of contributions in ascending rank order (own partial or a
 // received slot), then written to every local copy.
+template <class T>
 __global__ void gs_unpack_kernel(int64_t nifc, const int32_t *__restrict__ perm, const int32_t *__restrict__ offs,
                                  const int32_t *__restrict__ coffs, const int32_t *__restrict__ contrib,
-                                 const double *__restrict__ partial, const double *__restrict__ recvbuf,
-                                 double *__restrict__ v, const int *done, const uint64_t *epoch, int64_t half)
+                                 const T *__restrict__ partial, const T *__restrict__ recvbuf,
+                                 T *__restrict__ v, const int *done, const uint64_t *epoch, int64_t half)
 {
     if (done && *(volatile const int *)done) return;
     if (epoch) recvbuf += (int64_t)(*epoch & 1) * half;   // P2P: double-buffered by epoch parity
@@ -1680,7 +1714,7 @@ __global__ void gs_unpack_kernel(int64_t nifc, const int32_t *__restrict__ perm,
     if (r >= nifc) return;
     const int c0 = coffs[r], c1 = coffs[r + 1];
     int src = contrib[c0];
-    double s = src < 0 ? partial[r] : recvbuf[src];
+    T s = src < 0 ? partial[r] : recvbuf[src];
     for (int c = c0 + 1; c < c1; ++c) {
         src = contrib[c];
         s += src < 0 ? partial[r] : recvbuf[src];
@@ -1688,8 +1722,9 @@ __global__ void gs_unpack_kernel(int64_t nifc, const int32_t *__restrict__ perm,
     for (int c = offs[r]; c < offs[r + 1]; ++c) v[perm[c]] = s;
 }
 
+template <class T>
 cudaError_t launch_gs_ifc_unpack(int64_t nifc, const int32_t *perm, const int32_t *offs, const int32_t *coffs,
-                                 const int32_t *contrib, const double *partial, const double *recvbuf, double *v,
+                                 const int32_t *contrib, const T *partial, const T *recvbuf, T *v,
                                  const int *done, cudaStream_t s, const uint64_t *epoch, int64_t half)
 {
     if (nifc <= 0) return cudaSuccess;
@@ -1744,14 +1779,16 @@ cudaError_t launch_dinv(int64_t n, const uint32_t *mbits, const double *d, doubl
     return cudaGetLastError();
 }
 
-__global__ void copy_mask_kernel(int64_t n, const uint32_t *__restrict__ mbits, const double *__restrict__ src,
-                                 double *__restrict__ dst)
+template <class T>
+__global__ void copy_mask_kernel(int64_t n, const uint32_t *__restrict__ mbits, const T *__restrict__ src,
+                                 T *__restrict__ dst)
 {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x)
-        dst[l] = bit_of(mbits, l) ? 0.0 : src[l];
+        dst[l] = bit_of(mbits, l) ? T(0) : src[l];
 }
 
-cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const double *src, double *dst, cudaStream_t s)
+template <class T>
+cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const T *src, T *dst, cudaStream_t s)
 {
     if (n == 0) return cudaSuccess;
     copy_mask_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(n, mbits, src, dst);
@@ -2219,9 +2256,10 @@ cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *r
 
 // pack with the interface partials folded in (one thread per send slot; a run
 // shared with several neighbours is folded once per slot, same bits)
+template <class T>
 __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restrict__ perm,
-                                         const int32_t *__restrict__ offs, const double *__restrict__ v,
-                                         double *__restrict__ partial, const int32_t *__restrict__ send_run,
+                                         const int32_t *__restrict__ offs, const T *__restrict__ v,
+                                         T *__restrict__ partial, const int32_t *__restrict__ send_run,
                                          const int32_t *__restrict__ slot_nbr, double *const *peer_recv,
                                          const int64_t *__restrict__ remote_off, const int64_t *__restrict__ send_offs,
                                          const int64_t *__restrict__ remote_half, int nnbr, int me,
@@ -2236,11 +2274,11 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
              sidx += (int64_t)gridDim.x * blockDim.x) {
             const int run = send_run[sidx];
             const int o0 = offs[run], o1 = offs[run + 1];
-            double s = v[perm[o0]];
+            T s = v[perm[o0]];
             for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
             partial[run] = s;
             const int k = slot_nbr[sidx];
-            peer_recv[k][par * remote_half[k] + remote_off[k] + (sidx - send_offs[k])] = s;
+            reinterpret_cast<T *>(peer_recv[k])[par * remote_half[k] + remote_off[k] + (sidx - send_offs[k])] = s;
         }
     }
     __syncthreads();
@@ -2257,7 +2295,8 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
     }
 }
 
-cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const double *v, double *partial,
+template <class T>
+cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const T *v, T *partial,
                                      int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
                                      double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
                                      const int64_t *remote_half, int nnbr, int me, uint64_t *const *peer_hflags,
@@ -2341,6 +2380,27 @@ cudaError_t launch_axpby(int64_t n, double alpha, const double *x, double beta, 
     axpby_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(n, alpha, x, beta, y, z);
     return cudaGetLastError();
 }
+
+
+// the gather-scatter family for the FP64 path and the FP32 pMG levels (NEXT #3)
+#define NEK_GS_INST(T)                                                                                          \
+    template cudaError_t launch_gs_classes<T>(const GsClasses &, T *, const int *, cudaStream_t);                \
+    template cudaError_t launch_gs_classes_unpack<T>(const GsClasses &, const HaloUnpack &, T *, const int *,   \
+                                                     cudaStream_t);                                             \
+    template cudaError_t launch_gs_ifc_pack<T>(int64_t, const int32_t *, const int32_t *, const T *, T *, int64_t, \
+                                               const int32_t *, T *, const int *, cudaStream_t);                \
+    template cudaError_t launch_gs_ifc_unpack<T>(int64_t, const int32_t *, const int32_t *, const int32_t *,    \
+                                                 const int32_t *, const T *, const T *, T *, const int *,       \
+                                                 cudaStream_t, const uint64_t *, int64_t);                      \
+    template cudaError_t launch_copy_mask<T>(int64_t, const uint32_t *, const T *, T *, cudaStream_t);           \
+    template cudaError_t launch_gs_pack_p2p_fused<T>(const int32_t *, const int32_t *, const T *, T *, int64_t,  \
+                                                     const int32_t *, const int32_t *, double *const *,         \
+                                                     const int64_t *, const int64_t *, const int64_t *, int, int, \
+                                                     uint64_t *const *, uint64_t *, unsigned int *, const int *, \
+                                                     cudaStream_t);
+NEK_GS_INST(double)
+NEK_GS_INST(float)
+#undef NEK_GS_INST
 
 #include "pmg_kernels.cuh"
 

@@ -95,27 +95,33 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
                       const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch);
 int64_t ax_grid(int variant, int N, int64_t nelem);      // partial slots one launch writes
 int ax_partials_needed(int variant, int N, int64_t E);
+// FP32 operator (v6, N <= 9): Gf is [E][ax_gstride_f(N)] (6 planes, padded to 16 bytes per element)
+cudaError_t launch_ax_f(int N, int64_t E, const float *u, const float *Gf, const float *wJf, const uint32_t *mbits,
+                        double h1, double h2, float *w, cudaStream_t s);
+int ax_gstride_f(int N);
 
 // gather-scatter runs grouped by length (see kernels.cu)
 struct GsClasses {
     int64_t n2 = 0, n4 = 0, n8 = 0, ng = 0;
     const int32_t *p2 = nullptr, *p4 = nullptr, *p8 = nullptr, *pg = nullptr, *og = nullptr;
 };
-cudaError_t launch_gs_classes(const GsClasses &C, double *v, const int *done, cudaStream_t s);
+template <class T> cudaError_t launch_gs_classes(const GsClasses &C, T *v, const int *done, cudaStream_t s);
 cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst, const int *done, cudaStream_t s);
 cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *offs, double *v, const int *done,
                             cudaStream_t s);
-cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t *offs, const double *v,
-                               double *partial, int64_t nslots, const int32_t *send_run, double *sendbuf,
+template <class T>
+cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t *offs, const T *v,
+                               T *partial, int64_t nslots, const int32_t *send_run, T *sendbuf,
                                const int *done, cudaStream_t s);
+template <class T>
 cudaError_t launch_gs_ifc_unpack(int64_t nifc, const int32_t *perm, const int32_t *offs, const int32_t *coffs,
-                                 const int32_t *contrib, const double *partial, const double *recvbuf, double *v,
+                                 const int32_t *contrib, const T *partial, const T *recvbuf, T *v,
                                  const int *done, cudaStream_t s, const uint64_t *epoch = nullptr,
                                  int64_t half = 0);
 cudaError_t launch_diag(int N, int64_t E, const double *G, const double *wJ, double h1, double h2, double *d,
                         cudaStream_t s);
 cudaError_t launch_dinv(int64_t n, const uint32_t *mbits, const double *d, double *dinv, cudaStream_t s);
-cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const double *src, double *dst, cudaStream_t s);
+template <class T> cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const T *src, T *dst, cudaStream_t s);
 cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *obits, const double *b,
                             const double *dinv, double *r, double *p, double *x, double *part, int nblk,
                             double *dst, unsigned int *counter, bool p_zero, cudaStream_t s);
@@ -137,7 +143,8 @@ struct HaloUnpack {
     int nnbr = 0;
     int *err = nullptr;
 };
-cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, double *v, const int *done,
+template <class T>
+cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, T *v, const int *done,
                                      cudaStream_t s);   // C empty: halo unpack only
 cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s);
@@ -152,7 +159,8 @@ cudaError_t launch_axpby(int64_t n, double alpha, const double *x, double beta, 
 // NVLink peer-memory exchange (CUDA IPC mappings; see kernels.cu)
 cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *red_loc, double *red_all, double *mbox,
                                 double *const *peer_mbox, uint64_t *epochs, int *err, cudaStream_t s);
-cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const double *v, double *partial,
+template <class T>
+cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const T *v, T *partial,
                                      int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
                                      double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
                                      const int64_t *remote_half, int nnbr, int me, uint64_t *const *peer_hflags,
@@ -170,12 +178,18 @@ int vec_blocks();
 int upd_blocks();
 
 // pmg_kernels.cuh
-cudaError_t launch_prolong_add(int64_t E, int Nc, int Nf, const double *J, const double *ec, double *uf,
-                               const int *done, cudaStream_t s);
-cudaError_t launch_restrict(int64_t E, int Nf, int Nc, const double *J, const double *rf, const uint32_t *obits,
-                            double *fc, const int *done, cudaStream_t s);
-cudaError_t launch_cheb(int mode, int64_t n, const double *dinv, const double *f, const double *w, double theta,
-                        double c1, double c2, double *d, double *x, double *r, const int *done, cudaStream_t s);
+template <class T>
+cudaError_t launch_prolong_add(int64_t E, int Nc, int Nf, const T *J, const T *ec, T *uf, const int *done,
+                               cudaStream_t s);
+template <class T>
+cudaError_t launch_restrict(int64_t E, int Nf, int Nc, const T *J, const T *rf, const uint32_t *obits, T *fc,
+                            const int *done, cudaStream_t s);
+template <class T>
+cudaError_t launch_cheb(int mode, int64_t n, const T *dinv, const T *f, const T *w, double theta, double c1,
+                        double c2, T *d, T *x, T *r, const int *done, cudaStream_t s);
+template <class Ti, class To>
+cudaError_t launch_convert(int64_t n, const Ti *in, To *out, const int *done, cudaStream_t s);
+cudaError_t launch_geom_to_f32(int64_t E, int N, const double *G, float *Gf, cudaStream_t s);
 cudaError_t launch_dot_owner(int64_t n, const uint32_t *obits, const double *a, const double *b, double *part,
                              int nblk, double *dst, unsigned int *counter, const int *done, cudaStream_t s);
 cudaError_t launch_pcg_pupdate_z(int64_t n, const double *z, double *p, const double *red_all, int nranks,

@@ -18,28 +18,29 @@
 constexpr int XF_THREADS = 128;
 
 // one CTA per element; IN points per direction a, OUT points b; TRANS: J^T (b < a) with owner weights
-template <bool TRANS, bool ADD>
+template <bool TRANS, bool ADD, class T>
 __global__ void __launch_bounds__(XF_THREADS)
-    xfer_kernel(int64_t E, int a, int b, const double *__restrict__ J, const double *__restrict__ in,
-                const uint32_t *__restrict__ obits, double *__restrict__ out, const int *__restrict__ done)
+    xfer_kernel(int64_t E, int a, int b, const T *__restrict__ J, const T *__restrict__ in,
+                const uint32_t *__restrict__ obits, T *__restrict__ out, const int *__restrict__ done)
 {
     if (done && *(volatile const int *)done) return;
-    extern __shared__ double xs[];
+    extern __shared__ __align__(16) unsigned char xs_raw[];
+    T *xs = reinterpret_cast<T *>(xs_raw);
     // J as stored: TRANS=false -> [b][a] (rows: output points), TRANS=true -> [a][b] (rows: input points)
-    double *sJ = xs;                              // 256
-    double *s0 = xs + 256;                        // a^3
-    double *s1 = s0 + a * a * a;                  // a^2 b
-    double *s2 = s1 + a * a * b;                  // a b^2
+    T *sJ = xs;                                   // 256
+    T *s0 = xs + 256;                             // a^3
+    T *s1 = s0 + a * a * a;                       // a^2 b
+    T *s2 = s1 + a * a * b;                       // a b^2
     const int t = threadIdx.x;
     const int a3 = a * a * a, b3 = b * b * b;
     for (int q = t; q < a * b; q += blockDim.x) sJ[q] = J[q];
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
-        const double *ue = in + e * a3;
+        const T *ue = in + e * a3;
         for (int q = t; q < a3; q += blockDim.x) {
-            double v = ue[q];
+            T v = ue[q];
             if (TRANS) {
                 const int64_t l = e * a3 + q;
-                if (!((__ldg(obits + (l >> 5)) >> (l & 31)) & 1u)) v = 0.0;
+                if (!((__ldg(obits + (l >> 5)) >> (l & 31)) & 1u)) v = T(0);
             }
             s0[q] = v;
         }
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(XF_THREADS)
         // i direction: s1[k][j][I] = sum_i M[I][i] s0[k][j][i]
         for (int q = t; q < a * a * b; q += blockDim.x) {
             const int I = q % b, kj = q / b;
-            double s = 0.0;
+            T s = 0;
             for (int i = 0; i < a; ++i) s += (TRANS ? sJ[i * b + I] : sJ[I * a + i]) * s0[kj * a + i];
             s1[q] = s;
         }
@@ -55,16 +56,16 @@ __global__ void __launch_bounds__(XF_THREADS)
         // j direction: s2[k][J][I] = sum_j M[J][j] s1[k][j][I]
         for (int q = t; q < a * b * b; q += blockDim.x) {
             const int I = q % b, Jj = (q / b) % b, k = q / (b * b);
-            double s = 0.0;
+            T s = 0;
             for (int j = 0; j < a; ++j) s += (TRANS ? sJ[j * b + Jj] : sJ[Jj * a + j]) * s1[(k * a + j) * b + I];
             s2[q] = s;
         }
         __syncthreads();
         // k direction: out[K][J][I] = sum_k M[K][k] s2[k][J][I]
-        double *oe = out + e * b3;
+        T *oe = out + e * b3;
         for (int q = t; q < b3; q += blockDim.x) {
             const int IJ = q % (b * b), K = q / (b * b);
-            double s = 0.0;
+            T s = 0;
             for (int k = 0; k < a; ++k) s += (TRANS ? sJ[k * b + K] : sJ[K * a + k]) * s2[k * b * b + IJ];
             if (ADD) oe[q] += s;
             else oe[q] = s;
@@ -73,53 +74,63 @@ __global__ void __launch_bounds__(XF_THREADS)
     }
 }
 
-cudaError_t launch_prolong_add(int64_t E, int Nc, int Nf, const double *J, const double *ec, double *uf,
-                               const int *done, cudaStream_t s)
+template <class T>
+static void xfer_attr()
+{
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(xfer_kernel<true, false, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        cudaFuncSetAttribute(xfer_kernel<false, true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        attr = true;
+    }
+}
+
+template <class T>
+cudaError_t launch_prolong_add(int64_t E, int Nc, int Nf, const T *J, const T *ec, T *uf, const int *done,
+                               cudaStream_t s)
 {
     if (E <= 0) return cudaSuccess;
     const int a = Nc + 1, b = Nf + 1;
-    const size_t smem = sizeof(double) * (256 + a * a * a + a * a * b + a * b * b);
+    const size_t smem = sizeof(T) * (256 + a * a * a + a * a * b + a * b * b);
+    xfer_attr<T>();
     const int grid = (int)std::min<int64_t>(E, 148 * 16);
-    xfer_kernel<false, true><<<grid, XF_THREADS, smem, s>>>(E, a, b, J, ec, nullptr, uf, done);
+    xfer_kernel<false, true, T><<<grid, XF_THREADS, smem, s>>>(E, a, b, J, ec, nullptr, uf, done);
     return cudaGetLastError();
 }
 
-cudaError_t launch_restrict(int64_t E, int Nf, int Nc, const double *J, const double *rf, const uint32_t *obits,
-                            double *fc, const int *done, cudaStream_t s)
+template <class T>
+cudaError_t launch_restrict(int64_t E, int Nf, int Nc, const T *J, const T *rf, const uint32_t *obits, T *fc,
+                            const int *done, cudaStream_t s)
 {
     if (E <= 0) return cudaSuccess;
     const int a = Nf + 1, b = Nc + 1;
-    const size_t smem = sizeof(double) * (256 + a * a * a + a * a * b + a * b * b);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(xfer_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-        cudaFuncSetAttribute(xfer_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-        attr = true;
-    }
+    const size_t smem = sizeof(T) * (256 + a * a * a + a * a * b + a * b * b);
+    xfer_attr<T>();
     const int grid = (int)std::min<int64_t>(E, 148 * 16);
-    xfer_kernel<true, false><<<grid, XF_THREADS, smem, s>>>(E, a, b, J, rf, obits, fc, done);
+    xfer_kernel<true, false, T><<<grid, XF_THREADS, smem, s>>>(E, a, b, J, rf, obits, fc, done);
     return cudaGetLastError();
 }
 
 // mode 0: first (x0 = 0), 1: restart (w = A x0), 2: step (w = A d), 3: resid r = f - w only
+template <class T>
 __global__ void __launch_bounds__(256)
-    cheb_kernel(int mode, int64_t n, const double *__restrict__ dinv, const double *__restrict__ f,
-                const double *__restrict__ w, double theta, double c1, double c2, double *__restrict__ d,
-                double *__restrict__ x, double *__restrict__ r, const int *__restrict__ done)
+    cheb_kernel(int mode, int64_t n, const T *__restrict__ dinv, const T *__restrict__ f,
+                const T *__restrict__ w, T theta, T c1, T c2, T *__restrict__ d,
+                T *__restrict__ x, T *__restrict__ r, const int *__restrict__ done)
 {
     if (done && *(volatile const int *)done) return;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x) {
         if (mode == 0) {
-            const double fv = f[l];
-            const double dv = dinv[l] * fv / theta;
+            const T fv = f[l];
+            const T dv = dinv[l] * fv / theta;
             d[l] = dv; x[l] = dv; r[l] = fv;
         } else if (mode == 1) {
-            const double rv = f[l] - w[l];
-            const double dv = dinv[l] * rv / theta;
+            const T rv = f[l] - w[l];
+            const T dv = dinv[l] * rv / theta;
             r[l] = rv; d[l] = dv; x[l] = x[l] + dv;
         } else if (mode == 2) {
-            const double rv = r[l] - w[l];
-            const double dv = c1 * d[l] + c2 * (dinv[l] * rv);
+            const T rv = r[l] - w[l];
+            const T dv = c1 * d[l] + c2 * (dinv[l] * rv);
             r[l] = rv; d[l] = dv; x[l] = x[l] + dv;
         } else {
             r[l] = f[l] - w[l];
@@ -127,14 +138,66 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-cudaError_t launch_cheb(int mode, int64_t n, const double *dinv, const double *f, const double *w, double theta,
-                        double c1, double c2, double *d, double *x, double *r, const int *done, cudaStream_t s)
+template <class T>
+cudaError_t launch_cheb(int mode, int64_t n, const T *dinv, const T *f, const T *w, double theta, double c1,
+                        double c2, T *d, T *x, T *r, const int *done, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
-    cheb_kernel<<<grid, 256, 0, s>>>(mode, n, dinv, f, w, theta, c1, c2, d, x, r, done);
+    cheb_kernel<T><<<grid, 256, 0, s>>>(mode, n, dinv, f, w, (T)theta, (T)c1, (T)c2, d, x, r, done);
     return cudaGetLastError();
 }
+
+// precision conversion (FP32 preconditioner, NEXT #3): out[l] = (To) in[l]
+template <class Ti, class To>
+__global__ void convert_kernel(int64_t n, const Ti *__restrict__ in, To *__restrict__ out, const int *__restrict__ done)
+{
+    if (done && *(volatile const int *)done) return;
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x)
+        out[l] = (To)in[l];
+}
+
+template <class Ti, class To>
+cudaError_t launch_convert(int64_t n, const Ti *in, To *out, const int *done, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    convert_kernel<Ti, To><<<grid, 256, 0, s>>>(n, in, out, done);
+    return cudaGetLastError();
+}
+
+// metric factors [E][6][P3] (FP64) -> [E][gs] (FP32, per-element stride padded to 16 bytes)
+__global__ void geom_to_f32_kernel(int64_t E, int P3, int gs, const double *__restrict__ G, float *__restrict__ Gf)
+{
+    const int64_t tot = E * (int64_t)gs;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < tot; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = q / gs;
+        const int o = (int)(q - e * gs);
+        Gf[q] = o < 6 * P3 ? (float)G[e * 6 * (int64_t)P3 + o] : 0.0f;
+    }
+}
+
+cudaError_t launch_geom_to_f32(int64_t E, int N, const double *G, float *Gf, cudaStream_t s)
+{
+    const int P3 = (N + 1) * (N + 1) * (N + 1), gs = ax_gstride_f(N);
+    const int64_t tot = E * (int64_t)gs;
+    if (tot <= 0) return cudaSuccess;
+    geom_to_f32_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(E, P3, gs, G, Gf);
+    return cudaGetLastError();
+}
+
+#define NEK_PMG_INST(T)                                                                                         \
+    template cudaError_t launch_prolong_add<T>(int64_t, int, int, const T *, const T *, T *, const int *,        \
+                                               cudaStream_t);                                                   \
+    template cudaError_t launch_restrict<T>(int64_t, int, int, const T *, const T *, const uint32_t *, T *,      \
+                                            const int *, cudaStream_t);                                         \
+    template cudaError_t launch_cheb<T>(int, int64_t, const T *, const T *, const T *, double, double, double, T *, \
+                                        T *, T *, const int *, cudaStream_t);
+NEK_PMG_INST(double)
+NEK_PMG_INST(float)
+#undef NEK_PMG_INST
+template cudaError_t launch_convert<double, float>(int64_t, const double *, float *, const int *, cudaStream_t);
+template cudaError_t launch_convert<float, double>(int64_t, const float *, double *, const int *, cudaStream_t);
 
 // dst[0] = sum over owner copies of a[l] b[l] (fixed order: per-thread strided sums, block sums,
 // CTA partials folded by the last CTA)

@@ -67,12 +67,13 @@ PMG_MAX_LEVELS = 8
 class nek_pmg_opts(ctypes.Structure):
     _fields_ = [("nlevels", ctypes.c_int32), ("orders", ctypes.c_int32 * PMG_MAX_LEVELS),
                 ("degree", ctypes.c_int32), ("coarse_degree", ctypes.c_int32), ("lanczos_steps", ctypes.c_int32),
-                ("lmin_frac", ctypes.c_double), ("lmax_factor", ctypes.c_double), ("coarse_lo", ctypes.c_double)]
+                ("lmin_frac", ctypes.c_double), ("lmax_factor", ctypes.c_double), ("coarse_lo", ctypes.c_double),
+                ("precision", ctypes.c_int32)]
 
 
 class nek_pmg_info_t(ctypes.Structure):
     _fields_ = [("nlevels", ctypes.c_int32), ("orders", ctypes.c_int32 * PMG_MAX_LEVELS),
-                ("degree", ctypes.c_int32), ("coarse_degree", ctypes.c_int32),
+                ("degree", ctypes.c_int32), ("coarse_degree", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("n_local", ctypes.c_int64 * PMG_MAX_LEVELS), ("lam_min", ctypes.c_double * PMG_MAX_LEVELS),
                 ("lam_max", ctypes.c_double * PMG_MAX_LEVELS), ("vcycles", ctypes.c_int64)]
 
@@ -354,7 +355,7 @@ class PMG:
     coarse_lo."""
 
     def __init__(self, ctx: Context, xyz, h1, h2, orders=None, degree=0, coarse_degree=0, lanczos_steps=0,
-                 lmin_frac=0.0, lmax_factor=0.0, coarse_lo=0.0):
+                 lmin_frac=0.0, lmax_factor=0.0, coarse_lo=0.0, precision=0):
         self.ctx = ctx
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
         if xyz.size != 3 * ctx.n:
@@ -366,6 +367,7 @@ class PMG:
                 o.orders[i] = int(v)
         o.degree, o.coarse_degree, o.lanczos_steps = int(degree), int(coarse_degree), int(lanczos_steps)
         o.lmin_frac, o.lmax_factor, o.coarse_lo = float(lmin_frac), float(lmax_factor), float(coarse_lo)
+        o.precision = int(precision)
         h = ctypes.c_void_p()
         _check(_lib.nek_pmg_create(ctx.handle, _np_ptr(xyz), float(h1), float(h2), ctypes.byref(o),
                                    ctypes.byref(h), None), ctx.handle)
@@ -397,6 +399,7 @@ class PMG:
         _check(_lib.nek_pmg_info(self._h, ctypes.byref(i)))
         L = i.nlevels
         return {"nlevels": L, "orders": list(i.orders[:L]), "degree": i.degree, "coarse_degree": i.coarse_degree,
+                "precision": i.precision,
                 "n_local": list(i.n_local[:L]), "lam_min": list(i.lam_min[:L]), "lam_max": list(i.lam_max[:L]),
                 "vcycles": i.vcycles}
 

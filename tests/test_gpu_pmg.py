@@ -113,6 +113,33 @@ def test_zero_rhs(case):
     assert np.all(z == 0.0)
 
 
+def test_fp32_preconditioner(case, nek):
+    """NEXT #3: the V-cycle on FP32 level data.  It is the FP64 V-cycle up to single-
+    precision rounding (unit roundoff 6e-8, amplified by the ~40 operator applications of a cycle:
+    bound 1e-4 normwise); the outer FP64 CG still converges to the oracle's solution and needs at
+    most 2 more iterations than with the FP64 preconditioner."""
+    m, O, Po, ctx, Pg, h = case
+    if m.N > 9:
+        pytest.skip("FP32 preconditioner: N <= 9")
+    sched = [L.N for L in Po.levels]
+    P32 = nek.PMG(ctx, m.xyz, h[0], h[1], orders=sched, precision=1)
+    try:
+        assert P32.info()["precision"] == 1
+        rng = np.random.default_rng(5)
+        r = oracle.mask(m.mask, O.gs_apply(rng.standard_normal(O.n)))
+        z = np.empty(O.n)
+        P32.apply(r, z)
+        assert rel(z, Po.apply(r)) <= 1e-4
+        b = mg.smooth_field(m, seed=3)
+        xo, ito, sto, _ = opmg.pcg(O, h[0], h[1], b, 1e-10, 200, Po.apply)
+        x = np.zeros(O.n)
+        st, it, rr, _ = P32.solve(b, x, 1e-10, 200)
+        assert st == 0 and it <= ito + 2 and rr <= 1e-10
+        assert rel(x, xo) <= 1e-8
+    finally:
+        P32.free()
+
+
 def test_pmg_full_size_symmetry_and_iterations(nek):
     """Config 2 (16^3, N = 7), the size bench.py times: the V-cycle is symmetric in the owner
     inner product (property at any size) and pMG-PCG converges in far fewer iterations than

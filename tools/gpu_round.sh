@@ -1,12 +1,7 @@
-R="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1"
-timeout 600 $R --master-port 29530 tools/mgpu_check.py > gpurun_out/mgpu4.log 2>&1; tail -1 gpurun_out/mgpu4.log | python -c "
-import sys,json; d=json.loads(sys.stdin.read()); print(d['ok'], {k:(v['ok'], v['pmg']) for k,v in d['cases'].items()})"
-timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/b1.json 2>gpurun_out/b1.err
-python -c "import json;d=json.loads(open('gpurun_out/b1.json').read().strip().splitlines()[-1]);print(d['value'], d['pmg'], d['cpu_baseline'])"
-for ez in 16 128; do
-timeout 300 $R --master-port 2953$((ez % 7)) bench.py --gpus 4 --steps 10 --warmup 3 --ez $ez > gpurun_out/b4_ez$ez.json 2> gpurun_out/b4.err
-done
-timeout 600 $R --master-port 29551 bench.py --gpus 4 --steps 3 --warmup 3 --mesh rod > gpurun_out/b4_rod.json 2>> gpurun_out/b4.err
-for f in b4_ez16 b4_ez128 b4_rod; do python -c "
-import json;d=json.loads(open('gpurun_out/$f.json').read().strip().splitlines()[-1]);print('$f',round(d['value'],2),round(d['pcg_iter_per_s']),d['clocks']['sm_mhz'], d['pmg'])"; done
+timeout 900 python -m pytest tests/test_gpu_pmg.py -x -q > gpurun_out/pytest_pmg.log 2>&1; tail -20 gpurun_out/pytest_pmg.log
+timeout 300 python tools/pmg_bench.py --ez 16 > gpurun_out/pmgb64.jsonl 2>&1; tail -1 gpurun_out/pmgb64.jsonl
+timeout 300 python tools/pmg_bench.py --ez 16 --precision 1 > gpurun_out/pmgb32.jsonl 2>&1; tail -1 gpurun_out/pmgb32.jsonl
+timeout 300 python tools/pmg_profile.py --precision 1 > gpurun_out/pmg_prof32.json 2> gpurun_out/pmg_prof.err; cat gpurun_out/pmg_prof32.json | python -c "
+import sys,json; d=json.loads(sys.stdin.read()); print(d['us_per_vcycle_kernels'], d['launches_per_vcycle'])
+for r in d['by_kernel'][:16]: print(r)"
 echo done

@@ -27,6 +27,7 @@ ap.add_argument("--coarse-degree", type=int, default=0)
 ap.add_argument("--coarse-lo", type=float, default=0.0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--mesh", default="box")
+ap.add_argument("--precision", type=int, default=0)
 a = ap.parse_args()
 if a.mesh == "rod":
     m = mg.rod_bundle(17, 17, 3, a.order, dirichlet="outlet" if a.h2 == 0 else "pins_walls")
@@ -38,7 +39,7 @@ x = torch.zeros_like(b)
 orders = [int(v) for v in a.orders.split(",")] if a.orders else None
 t0 = torch.cuda.Event(True); t1 = torch.cuda.Event(True)
 P = nek.PMG(ctx, m.xyz, 1.0, a.h2, orders=orders, degree=a.degree, coarse_degree=a.coarse_degree,
-            coarse_lo=a.coarse_lo)
+            coarse_lo=a.coarse_lo, precision=a.precision)
 
 
 def timed(fn):
@@ -60,7 +61,7 @@ z = torch.empty_like(b)
 P.apply(b, z)
 _, mv = timed(lambda: P.apply(b, z))
 info = P.info()
-print(json.dumps({"pc": "pmg", "orders": info["orders"], "degree": info["degree"],
+print(json.dumps({"pc": "pmg", "precision": info["precision"], "orders": info["orders"], "degree": info["degree"],
                   "coarse_degree": info["coarse_degree"], "lam_max": info["lam_max"], "lam_min": info["lam_min"],
                   "iters": it, "relres": rr, "ms": ms, "ms_per_iter": ms / max(it, 1), "ms_per_vcycle": mv}),
       flush=True)
