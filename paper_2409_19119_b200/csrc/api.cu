@@ -895,8 +895,9 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     if (ctx->hist_cap < maxit + 1) {
         if (ctx->hist) cudaFree(ctx->hist);
         ctx->hist = nullptr;
-        CK(dalloc(ctx, &ctx->hist, maxit + 1));
-        ctx->hist_cap = maxit + 1;
+        const int cap = std::max(maxit + 1, std::max(1024, 2 * ctx->hist_cap));   // grow rarely: graphs hold it
+        CK(dalloc(ctx, &ctx->hist, cap));
+        ctx->hist_cap = cap;
         if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
     }
     const bool db = is_device_ptr(b), dx = is_device_ptr(x);

@@ -68,10 +68,15 @@ def main():
         pst, pit, prr, _ = P.solve(torch.from_numpy(b).to(dev), xpd, 1e-10, 200)
         pinfo = P.info()
         P.free()
+        P32 = nek.PMG(ctx, sub.xyz, 1.0, 0.0, precision=1)       # FP32 preconditioner (NEXT #3)
+        x32d = torch.zeros_like(ud)
+        pst32, pit32, _, _ = P32.solve(torch.from_numpy(b).to(dev), x32d, 1e-10, 200)
+        P32.free()
         torch.cuda.synchronize()
         payload = {"w": wd.cpu().numpy(), "v": vd.cpu().numpy(), "x": xd.cpu().numpy(), "hist": hist, "it": it,
                    "info": info, "z": zd.cpu().numpy(), "xp": xpd.cpu().numpy(), "pit": pit, "pst": pst,
-                   "lam": pinfo["lam_max"] + pinfo["lam_min"]}
+                   "lam": pinfo["lam_max"] + pinfo["lam_min"], "x32": x32d.cpu().numpy(), "pit32": pit32,
+                   "pst32": pst32}
         gathered = [None] * world
         dist.all_gather_object(gathered, payload)
         if rank == 0:
@@ -107,15 +112,17 @@ def main():
             lam_diff = max(abs(a - b_) / max(lam_o[:len(Po.levels)]) for pl in gathered for a, b_ in zip(pl["lam"], lam_o))
             rf = oracle.mask(m.mask, O.gs_apply(uf))
             zref = Po.apply(rf)
-            zgot = np.zeros(m.n_local); xpgot = np.zeros(m.n_local)
+            zgot = np.zeros(m.n_local); xpgot = np.zeros(m.n_local); x32got = np.zeros(m.n_local)
             for r_, pl in enumerate(gathered):
                 lr = (parts[r_][:, None] * P3 + np.arange(P3)).reshape(-1)
-                zgot[lr] = pl["z"]; xpgot[lr] = pl["xp"]
+                zgot[lr] = pl["z"]; xpgot[lr] = pl["xp"]; x32got[lr] = pl["x32"]
             z_err = float(np.abs(zgot - zref).max() / np.abs(zref).max())
             xpo, pito, psto, _ = opmg.pcg(O, 1.0, 0.0, bf, 1e-10, 200, Po.apply)
             xp_err = float(np.abs(xpgot - xpo).max() / np.abs(xpo).max())
+            x32_err = float(np.abs(x32got - xpo).max() / np.abs(xpo).max())
             pmg_ok = (lam_diff <= 1e-9 and z_err <= max(1e-11, 100 * lam_diff) and xp_err <= 1e-8
-                      and all(abs(pl["pit"] - pito) <= 1 and pl["pst"] == 0 for pl in gathered))
+                      and all(abs(pl["pit"] - pito) <= 1 and pl["pst"] == 0 for pl in gathered)
+                      and x32_err <= 1e-8 and all(pl["pit32"] <= pito + 2 and pl["pst32"] == 0 for pl in gathered))
             case_ok = (ax_err <= 1e-12 and gs_bit and gs_err <= 1e-14 and hist_ok and x_err <= 1e-10 and bool(same)
                        and pmg_ok)
             ok &= case_ok
@@ -125,7 +132,8 @@ def main():
                              "neighbors": [pl["info"]["n_neighbors"] for pl in gathered],
                              "transport": [pl["info"]["transport"] for pl in gathered],
                              "pmg": {"lam_diff": lam_diff, "vcycle_err": z_err, "x_err": xp_err, "iters_oracle": pito,
-                                     "iters": [pl["pit"] for pl in gathered], "ok": bool(pmg_ok)},
+                                     "iters": [pl["pit"] for pl in gathered], "fp32_x_err": x32_err,
+                                     "fp32_iters": [pl["pit32"] for pl in gathered], "ok": bool(pmg_ok)},
                              "ok": case_ok}
         nek.free(ctx)
     if rank == 0:
