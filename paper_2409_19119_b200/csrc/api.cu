@@ -895,7 +895,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     if (ctx->hist_cap < maxit + 1) {
         if (ctx->hist) cudaFree(ctx->hist);
         ctx->hist = nullptr;
-        const int cap = std::max(maxit + 1, std::max(1024, 2 * ctx->hist_cap));   // grow rarely: graphs hold it
+        const int cap = std::max<int>(maxit + 1, std::max<int>(1024, 2 * (int)ctx->hist_cap));   // grow rarely: graphs hold it
         CK(dalloc(ctx, &ctx->hist, cap));
         ctx->hist_cap = cap;
         if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
