@@ -44,14 +44,23 @@ def launches(path):
 def full(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6,
+             "ns": 1e-3, "us": 1.0, "ms": 1e3}
     print("| kernel | " + " | ".join(lbl for _, lbl in FULL_METRICS) + " | top stalls |")
     print("|---|" + "---|" * (len(FULL_METRICS) + 1))
     for r in rows[2:]:
         name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "")
         vals = []
         for m, _ in FULL_METRICS:
-            vals.append(r[h.index(m)] if m in h else "-")
+            if m not in h:
+                vals.append("-")
+                continue
+            k = h.index(m)
+            v = r[k]
+            if units[k] in scale and v not in ("", "n/a"):   # MB for bytes, us for times
+                v = f"{float(v.replace(',', '')) * scale[units[k]]:.2f}"
+            vals.append(v)
         st = [(h[k].replace("smsp__pcsamp_warps_issue_stalled_", ""), float(r[k] or 0)) for k in range(len(h))
               if "pcsamp_warps_issue_stalled" in h[k] and "not_issued" not in h[k]]
         tot = sum(v for _, v in st) or 1.0
