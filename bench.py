@@ -353,13 +353,40 @@ def main():
         pmg = {"tol": tol, "orders": pinfo["orders"], "degree": pinfo["degree"],
                "coarse_degree": pinfo["coarse_degree"], "iters": itp, "jacobi_iters": itj}
     log("pmg done")
+    # ---- projection initial guess (NEXT #2) over a drifting right-hand-side sequence
+    proj = None
+    pj = [0.0] * 2
+    if not args.no_pmg:
+        b1 = torch.from_numpy(mg.smooth_field(mesh, seed=4)).to(dev)
+        its = {}
+        for k, L in enumerate((0, 8)):
+            Pj = nek.Projection(ctx, L)
+            seq = []
+            barrier(); torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for t in range(12):
+                bt = b + (0.01 * t) * b1
+                _, it, _ = Pj.solve(1.0, args.h2, bt, x, 1e-8, 5000)
+                seq.append(it)
+            e1.record(stream)
+            torch.cuda.synchronize(); barrier()
+            pj[k] = e0.elapsed_time(e1)
+            its[L] = seq
+            Pj.free()
+        proj = {"sequence": "b_t = b0 + 0.01 t b1, t = 0..11, Jacobi-PCG to 1e-8 (S:385)",
+                "iters_L0": its[0], "iters_L8": its[8]}
+    log("projection done")
 
     # ---- max over ranks
-    vals = torch.tensor([t_ms, ax_ms, e2e_s] + pm, dtype=torch.float64, device=dev)
+    vals = torch.tensor([t_ms, ax_ms, e2e_s] + pm + pj, dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     t_ms, ax_ms, e2e_s = [float(v) for v in vals.cpu()[:3]]
-    pm = [float(v) for v in vals.cpu()[3:]]
+    pm = [float(v) for v in vals.cpu()[3:3 + len(pm)]]
+    pj = [float(v) for v in vals.cpu()[3 + len(pm):]]
+    if proj is not None:
+        proj.update({"ms_L0": pj[0], "ms_L8": pj[1], "speedup": pj[0] / pj[1] if pj[1] > 0 else None})
     if pmg is not None:
         pmg.update({"ms": pm[1], "jacobi_ms": pm[0], "speedup": pm[0] / pm[1] if pm[1] > 0 else None,
                     "ms_per_vcycle": pm[2],
@@ -419,7 +446,7 @@ def main():
             "gpu_launches": int(launch_stats["launches"]),
             "e2e": {"value": n_dof_total * args.iters / e2e_s / 1e9, "unit": "GDOF/s",
                     "h2d_bytes_per_step": mesh.n_local * 8, "d2h_bytes_per_step": mesh.n_local * 8},
-            "roofline": roofline, "clocks": clocks, "pmg": pmg,
+            "roofline": roofline, "clocks": clocks, "pmg": pmg, "projection": proj,
             "halo": {"doubles_per_gs": info["halo_doubles"], "neighbors": info["n_neighbors"],
                      "transport": {0: "none", 1: "nccl", 2: "nvlink-p2p"}[info["transport"]]},
         }
