@@ -377,14 +377,47 @@ def main():
         proj = {"sequence": "b_t = b0 + 0.01 t b1, t = 0..11, Jacobi-PCG to 1e-8 (S:385)",
                 "iters_L0": its[0], "iters_L8": its[8]}
     log("projection done")
+    # ---- dealiased advection makef (NEXT #4) on the same mesh: CUDA-event time per apply, L2 flushed
+    mk = None
+    mkv = [0.0]
+    if not args.no_pmg and args.order <= 9:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from makef_bench import makef_cost
+        K = nek.Makef(ctx, mesh.xyz)
+        Uv = [torch.from_numpy(mg.smooth_field(mesh, seed=s)).to(dev) for s in (5, 6, 7)]
+        Fv = [torch.empty_like(Uv[0]) for _ in range(3)]
+        for _ in range(3):
+            K.apply(*Uv, *Fv)
+        barrier(); torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(5):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream); K.apply(*Uv, *Fv); e1.record(stream); e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        mkv = [tot / 5]
+        mb, mf = makef_cost(args.order)
+        mk = {"M": K.M, "bytes_per_element": mb, "flops_per_element": mf, "fp64_peak_tflops": nek.probe_fp64_tflops(local)}
+        K.free()
+        del Uv, Fv
+    log("makef done")
 
     # ---- max over ranks
-    vals = torch.tensor([t_ms, ax_ms, e2e_s] + pm + pj, dtype=torch.float64, device=dev)
+    vals = torch.tensor([t_ms, ax_ms, e2e_s] + pm + pj + mkv, dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     t_ms, ax_ms, e2e_s = [float(v) for v in vals.cpu()[:3]]
     pm = [float(v) for v in vals.cpu()[3:3 + len(pm)]]
-    pj = [float(v) for v in vals.cpu()[3 + len(pm):]]
+    pj = [float(v) for v in vals.cpu()[3 + len(pm):3 + len(pm) + len(pj)]]
+    mkv = [float(v) for v in vals.cpu()[3 + len(pm) + len(pj):]]
+    if mk is not None:
+        ms = mkv[0]
+        gbs = mk["bytes_per_element"] * mesh.E / (ms * 1e-3) / 1e9
+        tfs = mk["flops_per_element"] * mesh.E / (ms * 1e-3) / 1e12
+        mk.update({"ms_per_apply": ms, "gdof_per_s": n_dof_total / (ms * 1e-3) / 1e9, "algorithmic_GBps": gbs,
+                   "algorithmic_TFLOPs": tfs, "fp64_frac": tfs / mk["fp64_peak_tflops"],
+                   "note": "u, v, w in, 9 M^3 lattice factors, 3 outputs per element; flops of the sum-factorised "
+                           "algorithm; FP64 peak = nek_probe_dfma_tflops (register FMA chains, measured here)"})
     if proj is not None:
         proj.update({"ms_L0": pj[0], "ms_L8": pj[1], "speedup": pj[0] / pj[1] if pj[1] > 0 else None})
     if pmg is not None:
@@ -446,7 +479,7 @@ def main():
             "gpu_launches": int(launch_stats["launches"]),
             "e2e": {"value": n_dof_total * args.iters / e2e_s / 1e9, "unit": "GDOF/s",
                     "h2d_bytes_per_step": mesh.n_local * 8, "d2h_bytes_per_step": mesh.n_local * 8},
-            "roofline": roofline, "clocks": clocks, "pmg": pmg, "projection": proj,
+            "roofline": roofline, "clocks": clocks, "pmg": pmg, "projection": proj, "makef": mk,
             "halo": {"doubles_per_gs": info["halo_doubles"], "neighbors": info["n_neighbors"],
                      "transport": {0: "none", 1: "nccl", 2: "nvlink-p2p"}[info["transport"]]},
         }

@@ -232,6 +232,33 @@ int nek_pmg_solve(nek_pmg *pmg, const double *b, double *x, double tol, int maxi
 int nek_pmg_info(const nek_pmg *pmg, nek_pmg_info_t *info);
 int nek_pmg_free(nek_pmg *pmg);
 
+/* ------------------------------------------------- dealiased advection makef */
+/*
+ * The nonlinear advection term of the velocity (P:417-420
+ * "dealiased using N_q=11 quadrature points in each direction", "dealiased
+ * with the 3/2's rule, the working data set per element is 12^3").
+ * DESIGN.md readings M1-M4: per element, component c and GLL node l
+ *   F_c(l) = - sum_q rho_q J_q phi_l(xi_q) (u . grad u_c)(xi_q)
+ * on the M^3 Gauss-Legendre lattice, M = ceil(3(N+1)/2) (N = 7: M = 12), with u and
+ * grad u_c from the order-N interpolant and J, dr/dx from the isoparametric map of `xyz`
+ * (the nek_setup coordinates).  Output is LOCAL (unassembled, unmasked) E-vectors: apply
+ * nek_gs (and a mask) as for any right-hand side.
+ * nek_makef_create: M = 0 or the 3/2-rule value (else NEK_EINVAL); N <= 9 (NEK_EORDER);
+ *   stores 9 M^3 FP64 factors per element (rho J dr_a/dx_b); J <= 0 at a lattice point ->
+ *   NEK_EGEOM.  nek_makef_apply: u, v, w in, fu, fv, fw out (E-vectors, device or host,
+ *   outputs must not alias inputs).  Element-local: no communication for nranks > 1.
+ */
+typedef struct nek_makef nek_makef;
+int nek_makef_create(nek_ctx *ctx, const double *xyz, int M, nek_makef **out, void *stream);
+int nek_makef_apply(nek_makef *mk, const double *u, const double *v, const double *w, double *fu, double *fv,
+                    double *fw, void *stream);
+int nek_makef_lattice(const nek_makef *mk);
+int nek_makef_free(nek_makef *mk);
+
+/* Measurement probe: FP64 FMA throughput of `device` in TFLOP/s (register-only FMA chains,
+ * SURVEY 8(d)); the compute roofline denominator of makef. */
+int nek_probe_dfma_tflops(int device, double *tflops);
+
 /* ----------------------------------------------------------- introspection */
 typedef struct {
     int64_t E;                 /* local elements                                   */

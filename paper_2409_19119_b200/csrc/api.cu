@@ -1263,3 +1263,4 @@ extern "C" int nek_proj_solve(nek_proj *P, double h1, double h2, const double *b
 }
 
 #include "pmg.inc"
+#include "makef.inc"

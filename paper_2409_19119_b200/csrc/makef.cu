@@ -1,0 +1,520 @@
+// makef.cu -- dealiased advection (readings M1-M4).
+//
+// For each element, component c and GLL test node l (reading M1):
+//   F_c(l) = - sum_q rho_q J_q phi_l(xi_q) (u . grad u_c)(xi_q)
+//          = - [(J^T x J^T x J^T) ( sum_a Ut_a  d_a u_c )](l),   Ut_a = sum_b G_ab u_b   (reading M3)
+// on the M^3 Gauss-Legendre lattice (3/2 rule, N = 7 -> M = 12: the paper's "12^3 working set").
+// G_ab = rho J d r_a / d x_b at the fine points is computed once by makef_geom_kernel and streamed
+// (9 M^3 values per element); the velocity stays in HBM at GLL resolution.
+//
+// Kernel design (sm_100a, FP64): one element per CTA iteration, persistent CTAs, every tensor
+// contraction done by a thread owning a whole line of the current stage (i-lines, j-lines or
+// k-columns), the 1-D matrices J (interpolation) and Dq = J D (derivative at the fine points) as
+// compile-time constant-bank operands, line buffers padded to an odd stride.  Per element and
+// component: value/derivative interpolation in 3 stages (2 / 3 / 3 contractions), the pointwise
+// product with the contravariant velocity, and the transposed interpolation back in 3 stages.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "nek_ctx.h"
+
+namespace nekb200 {
+
+constexpr int MK_MAXN = 9;
+__constant__ double c_Jq[MK_MAXN + 1][16 * 10];   // [N][I * (N+1) + i] = h_i(xi^GL_I), default M of N
+__constant__ double c_Dq[MK_MAXN + 1][16 * 10];   // derivative of the interpolant at the GL points
+__constant__ double c_wq[MK_MAXN + 1][16];        // GL weights
+
+constexpr int mk_m(int NQ) { return (3 * NQ + 1) / 2; }   // ceil(3 (N+1) / 2)
+constexpr int odd(int n) { return n | 1; }
+
+template <int NQ>
+struct MK {
+    static constexpr int N = NQ - 1, MQ = mk_m(NQ), P3 = NQ * NQ * NQ, M3 = MQ * MQ * MQ;
+    static constexpr int PN = odd(NQ), PM = odd(MQ);            // padded i strides
+    // buffers (doubles): U3 [3][NQ][NQ][PN]; UT [3][M3] (Ut, then F); A/B [NQ][NQ][PM];
+    // AA/AD/BA [NQ][MQ][PM]; F [M3]; back-projection reuses A/B and AA
+    static constexpr int SZ_U = NQ * NQ * PN, SZ_A = NQ * NQ * PM, SZ_AA = NQ * MQ * PM;
+    static constexpr int SMEM_D = 3 * SZ_U + 3 * M3 + 2 * SZ_A + 3 * SZ_AA + M3;
+    static constexpr int NT = 256;
+    static constexpr int MINB = (SMEM_D * 8 + 1024) * 2 <= 227 * 1024 ? 2 : 1;   // two CTAs per SM when they fit
+};
+
+template <int NQ> __device__ __forceinline__ double Jm(int I, int i) { return c_Jq[NQ - 1][I * NQ + i]; }
+template <int NQ> __device__ __forceinline__ double Dm(int I, int i) { return c_Dq[NQ - 1][I * NQ + i]; }
+
+template <int NQ>
+__global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
+    makef_kernel(int64_t E, const double *__restrict__ G9, const double *__restrict__ u0,
+                 const double *__restrict__ u1, const double *__restrict__ u2, double *__restrict__ f0,
+                 double *__restrict__ f1, double *__restrict__ f2)
+{
+    using C = MK<NQ>;
+    constexpr int MQ = C::MQ, P3 = C::P3, M3 = C::M3, PN = C::PN, PM = C::PM;
+    constexpr int SZ_U = C::SZ_U, SZ_A = C::SZ_A, SZ_AA = C::SZ_AA;
+    extern __shared__ __align__(16) double sm[];
+    double *U3 = sm;                       // [3][NQ][NQ][PN]
+    double *UT = U3 + 3 * SZ_U;            // [3][M3]  (k, j, i) fine-point order, unpadded
+    double *SA = UT + 3 * M3;              // [NQ][NQ][PM]
+    double *SB = SA + SZ_A;
+    double *AA = SB + SZ_A;                // [NQ][MQ][PM]
+    double *AD = AA + SZ_AA;
+    double *BA = AD + SZ_AA;
+    double *F = BA + SZ_AA;                // [M3]
+    const int t = threadIdx.x, nt = blockDim.x;
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        // ---- velocity into shared memory (padded i stride)
+        for (int q = t; q < 3 * P3; q += nt) {
+            const int c = q / P3, p = q - c * P3, i = p % NQ, kj = p / NQ;
+            const double *src = c == 0 ? u0 : c == 1 ? u1 : u2;
+            U3[c * SZ_U + kj * PN + i] = src[e * P3 + p];
+        }
+        __syncthreads();
+        // ---- U at the fine points, 3 components together: i-lines, j-lines, k-columns
+        for (int L = t; L < 3 * NQ * NQ; L += nt) {                  // i: [c][k][j] lines
+            const int c = L / (NQ * NQ), kj = L % (NQ * NQ);
+            double x[NQ];
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) x[m] = U3[c * SZ_U + kj * PN + m];
+            double *o = (c == 0 ? SA : c == 1 ? SB : AA) + kj * PM;  // scratch per component
+#pragma unroll 2
+            for (int I = 0; I < MQ; ++I) {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) s = fma(Jm<NQ>(I, m), x[m], s);
+                o[I] = s;
+            }
+        }
+        __syncthreads();
+        for (int L = t; L < 3 * NQ * MQ; L += nt) {                  // j: [c][k][I] lines
+            const int c = L / (NQ * MQ), r = L % (NQ * MQ), k = r / MQ, I = r % MQ;
+            const double *in = (c == 0 ? SA : c == 1 ? SB : AA);
+            double x[NQ];
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) x[m] = in[(k * NQ + m) * PM + I];
+            double *o = (c == 0 ? AD : c == 1 ? BA : F);              // [k][J][I] stride PM (F: own layout)
+#pragma unroll 2
+            for (int J = 0; J < MQ; ++J) {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) s = fma(Jm<NQ>(J, m), x[m], s);
+                if (c < 2) o[(k * MQ + J) * PM + I] = s;
+                else o[(k * MQ + J) * MQ + I] = s;                     // F holds NQ*MQ*MQ <= M3 values
+            }
+        }
+        __syncthreads();
+        for (int L = t; L < 3 * MQ * MQ; L += nt) {                  // k: [c][J][I] columns -> U
+            const int c = L / (MQ * MQ), JI = L % (MQ * MQ);
+            double x[NQ];
+            if (c < 2) {
+                const double *in = c == 0 ? AD : BA;
+                const int J = JI / MQ, I = JI % MQ;
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) x[m] = in[(m * MQ + J) * PM + I];
+            } else {
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) x[m] = F[m * MQ * MQ + JI];
+            }
+#pragma unroll 2
+            for (int K = 0; K < MQ; ++K) {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) s = fma(Jm<NQ>(K, m), x[m], s);
+                UT[c * M3 + K * MQ * MQ + JI] = s;
+            }
+        }
+        __syncthreads();
+        // ---- contravariant velocity Ut_a = sum_b G_ab U_b (G streamed from HBM), in place
+        const double *Ge = G9 + e * 9 * (int64_t)M3;
+        for (int q = t; q < M3; q += nt) {
+            const double ux = UT[q], uy = UT[M3 + q], uz = UT[2 * M3 + q];
+            double g[9];
+#pragma unroll
+            for (int a = 0; a < 9; ++a) g[a] = __ldcs(Ge + a * M3 + q);
+            UT[q] = g[0] * ux + g[1] * uy + g[2] * uz;
+            UT[M3 + q] = g[3] * ux + g[4] * uy + g[5] * uz;
+            UT[2 * M3 + q] = g[6] * ux + g[7] * uy + g[8] * uz;
+        }
+        __syncthreads();
+        // ---- per component: gradient at the fine points, F = Ut . grad u_c, project back
+        for (int c = 0; c < 3; ++c) {
+            const double *uc = U3 + c * SZ_U;
+            for (int L = t; L < NQ * NQ; L += nt) {                  // i: A = J u, B = Dq u
+                double x[NQ];
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) x[m] = uc[L * PN + m];
+#pragma unroll 2
+                for (int I = 0; I < MQ; ++I) {
+                    double a = 0.0, b = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) { a = fma(Jm<NQ>(I, m), x[m], a); b = fma(Dm<NQ>(I, m), x[m], b); }
+                    SA[L * PM + I] = a;
+                    SB[L * PM + I] = b;
+                }
+            }
+            __syncthreads();
+            for (int L = t; L < 2 * NQ * MQ; L += nt) {              // j: AA, AD from A; BA from B
+                const int which = L / (NQ * MQ), r = L % (NQ * MQ), k = r / MQ, I = r % MQ;
+                const double *in = which == 0 ? SA : SB;
+                double x[NQ];
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) x[m] = in[(k * NQ + m) * PM + I];
+#pragma unroll 2
+                for (int J = 0; J < MQ; ++J) {
+                    if (which == 0) {
+                        double a = 0.0, d = 0.0;
+#pragma unroll
+                        for (int m = 0; m < NQ; ++m) { a = fma(Jm<NQ>(J, m), x[m], a); d = fma(Dm<NQ>(J, m), x[m], d); }
+                        AA[(k * MQ + J) * PM + I] = a;
+                        AD[(k * MQ + J) * PM + I] = d;
+                    } else {
+                        double a = 0.0;
+#pragma unroll
+                        for (int m = 0; m < NQ; ++m) a = fma(Jm<NQ>(J, m), x[m], a);
+                        BA[(k * MQ + J) * PM + I] = a;
+                    }
+                }
+            }
+            __syncthreads();
+            for (int L = t; L < MQ * MQ; L += nt) {                  // k: d_r, d_s, d_t and F
+                const int J = L / MQ, I = L % MQ;
+                double xa[NQ], xd[NQ], xb[NQ];
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) {
+                    xa[m] = AA[(m * MQ + J) * PM + I];
+                    xd[m] = AD[(m * MQ + J) * PM + I];
+                    xb[m] = BA[(m * MQ + J) * PM + I];
+                }
+#pragma unroll 2
+                for (int K = 0; K < MQ; ++K) {
+                    double dr = 0.0, ds = 0.0, dt = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) {
+                        dr = fma(Jm<NQ>(K, m), xb[m], dr);
+                        ds = fma(Jm<NQ>(K, m), xd[m], ds);
+                        dt = fma(Dm<NQ>(K, m), xa[m], dt);
+                    }
+                    const int q = K * MQ * MQ + L;
+                    F[q] = UT[q] * dr + UT[M3 + q] * ds + UT[2 * M3 + q] * dt;
+                }
+            }
+            __syncthreads();
+            for (int L = t; L < MQ * MQ; L += nt) {                  // k^T: P1[k][J][I] into AA
+                double x[MQ];
+#pragma unroll
+                for (int K = 0; K < MQ; ++K) x[K] = F[K * MQ * MQ + L];
+                const int J = L / MQ, I = L % MQ;
+#pragma unroll 2
+                for (int k = 0; k < NQ; ++k) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int K = 0; K < MQ; ++K) s = fma(Jm<NQ>(K, k), x[K], s);
+                    AA[(k * MQ + J) * PM + I] = s;
+                }
+            }
+            __syncthreads();
+            for (int L = t; L < NQ * MQ; L += nt) {                  // j^T: P2[k][j][I] into SA
+                const int k = L / MQ, I = L % MQ;
+                double x[MQ];
+#pragma unroll
+                for (int J = 0; J < MQ; ++J) x[J] = AA[(k * MQ + J) * PM + I];
+#pragma unroll 2
+                for (int j = 0; j < NQ; ++j) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int J = 0; J < MQ; ++J) s = fma(Jm<NQ>(J, j), x[J], s);
+                    SA[(k * NQ + j) * PM + I] = s;
+                }
+            }
+            __syncthreads();
+            double *fo = (c == 0 ? f0 : c == 1 ? f1 : f2) + e * P3;
+            for (int L = t; L < NQ * NQ; L += nt) {                  // i^T: out[k][j][i] = -sum_I J[I][i] P2
+                double x[MQ];
+#pragma unroll
+                for (int I = 0; I < MQ; ++I) x[I] = SA[L * PM + I];
+#pragma unroll 2
+                for (int i = 0; i < NQ; ++i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int I = 0; I < MQ; ++I) s = fma(Jm<NQ>(I, i), x[I], s);
+                    fo[L * NQ + i] = -s;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// G_ab = rho J d r_a / d x_b at the fine points (setup; reading M1).  One element per CTA
+// iteration, the same line-owned sum factorisation as the apply: for each coordinate x_d the three
+// reference derivatives at the fine points (stored as Jacobian entries [3d + a] in G9), then per
+// point the cofactor inverse, rho J and the 9 factors in place.
+template <int NQ>
+__global__ void __launch_bounds__(MK<NQ>::NT)
+    makef_geom_kernel(int64_t E, const double *__restrict__ xyz, int64_t n, double *__restrict__ G9,
+                      unsigned long long *bad)
+{
+    using C = MK<NQ>;
+    constexpr int MQ = C::MQ, P3 = C::P3, M3 = C::M3, PN = C::PN, PM = C::PM;
+    constexpr int SZ_U = C::SZ_U, SZ_A = C::SZ_A, SZ_AA = C::SZ_AA;
+    extern __shared__ __align__(16) double sm[];
+    double *X = sm;                        // [3][NQ][NQ][PN]
+    double *SA = X + 3 * SZ_U, *SB = SA + SZ_A, *AA = SB + SZ_A, *AD = AA + SZ_AA, *BA = AD + SZ_AA;
+    const int t = threadIdx.x, nt = blockDim.x;
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        double *Ge = G9 + e * 9 * (int64_t)M3;
+        for (int q = t; q < 3 * P3; q += nt) {
+            const int d = q / P3, p = q - d * P3;
+            X[d * SZ_U + (p / NQ) * PN + p % NQ] = xyz[d * n + e * P3 + p];
+        }
+        __syncthreads();
+        for (int d = 0; d < 3; ++d) {
+            const double *xd = X + d * SZ_U;
+            for (int L = t; L < NQ * NQ; L += nt) {
+                double x[NQ];
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) x[m] = xd[L * PN + m];
+#pragma unroll 2
+                for (int I = 0; I < MQ; ++I) {
+                    double a = 0.0, b = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) { a = fma(Jm<NQ>(I, m), x[m], a); b = fma(Dm<NQ>(I, m), x[m], b); }
+                    SA[L * PM + I] = a;
+                    SB[L * PM + I] = b;
+                }
+            }
+            __syncthreads();
+            for (int L = t; L < 2 * NQ * MQ; L += nt) {
+                const int which = L / (NQ * MQ), r = L % (NQ * MQ), k = r / MQ, I = r % MQ;
+                const double *in = which == 0 ? SA : SB;
+                double x[NQ];
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) x[m] = in[(k * NQ + m) * PM + I];
+#pragma unroll 2
+                for (int J = 0; J < MQ; ++J) {
+                    double a = 0.0, dd = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) { a = fma(Jm<NQ>(J, m), x[m], a); dd = fma(Dm<NQ>(J, m), x[m], dd); }
+                    if (which == 0) { AA[(k * MQ + J) * PM + I] = a; AD[(k * MQ + J) * PM + I] = dd; }
+                    else BA[(k * MQ + J) * PM + I] = a;
+                }
+            }
+            __syncthreads();
+            for (int L = t; L < MQ * MQ; L += nt) {
+                const int J = L / MQ, I = L % MQ;
+                double xa[NQ], xd2[NQ], xb[NQ];
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) {
+                    xa[m] = AA[(m * MQ + J) * PM + I];
+                    xd2[m] = AD[(m * MQ + J) * PM + I];
+                    xb[m] = BA[(m * MQ + J) * PM + I];
+                }
+#pragma unroll 2
+                for (int K = 0; K < MQ; ++K) {
+                    double dr = 0.0, ds = 0.0, dt = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) {
+                        dr = fma(Jm<NQ>(K, m), xb[m], dr);
+                        ds = fma(Jm<NQ>(K, m), xd2[m], ds);
+                        dt = fma(Dm<NQ>(K, m), xa[m], dt);
+                    }
+                    const int q = K * MQ * MQ + L;
+                    Ge[(3 * d + 0) * M3 + q] = dr;
+                    Ge[(3 * d + 1) * M3 + q] = ds;
+                    Ge[(3 * d + 2) * M3 + q] = dt;
+                }
+            }
+            __syncthreads();
+        }
+        for (int q = t; q < M3; q += nt) {
+            const int I = q % MQ, J = (q / MQ) % MQ, K = q / (MQ * MQ);
+            double Jd[3][3];                                         // [d][a] = d x_d / d r_a
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) Jd[d][a] = Ge[(3 * d + a) * M3 + q];
+            const double c00 = Jd[1][1] * Jd[2][2] - Jd[1][2] * Jd[2][1];
+            const double c01 = Jd[1][2] * Jd[2][0] - Jd[1][0] * Jd[2][2];
+            const double c02 = Jd[1][0] * Jd[2][1] - Jd[1][1] * Jd[2][0];
+            const double c10 = Jd[0][2] * Jd[2][1] - Jd[0][1] * Jd[2][2];
+            const double c11 = Jd[0][0] * Jd[2][2] - Jd[0][2] * Jd[2][0];
+            const double c12 = Jd[0][1] * Jd[2][0] - Jd[0][0] * Jd[2][1];
+            const double c20 = Jd[0][1] * Jd[1][2] - Jd[0][2] * Jd[1][1];
+            const double c21 = Jd[0][2] * Jd[1][0] - Jd[0][0] * Jd[1][2];
+            const double c22 = Jd[0][0] * Jd[1][1] - Jd[0][1] * Jd[1][0];
+            const double det = Jd[0][0] * c00 + Jd[0][1] * c01 + Jd[0][2] * c02;
+            if (!(det > 0.0)) atomicMin(bad, (unsigned long long)(e * M3 + q));
+            // rho J (d r_a / d x_b) = rho cof[b][a]   (inverse = cof^T / J)
+            const double rho = c_wq[NQ - 1][I] * c_wq[NQ - 1][J] * c_wq[NQ - 1][K];
+            const double cof[3][3] = {{c00, c01, c02}, {c10, c11, c12}, {c20, c21, c22}};
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) Ge[(3 * a + b) * M3 + q] = rho * cof[b][a];
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ host side
+// Gauss-Legendre nodes/weights by Newton on P_M (Legendre recurrence), Chebyshev initial guesses
+static void gauss_legendre(int M, double *x, double *w)
+{
+    for (int i = 0; i < M; ++i) {
+        double z = -std::cos(M_PI * (i + 0.75) / (M + 0.5));
+        double dp = 1.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = z;
+            for (int k = 2; k <= M; ++k) {
+                const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+                p0 = p1; p1 = p2;
+            }
+            dp = M * (z * p1 - p0) / (z * z - 1.0);
+            const double dz = p1 / dp;
+            z -= dz;
+            if (std::fabs(dz) < 1e-16) break;
+        }
+        x[i] = z;
+        w[i] = 2.0 / ((1.0 - z * z) * dp * dp);
+    }
+}
+
+int makef_lattice(int N) { return (3 * (N + 1) + 1) / 2; }
+
+cudaError_t makef_upload(int N)
+{
+    const int NQ = N + 1, MQ = makef_lattice(N);
+    std::vector<double> xg(NQ), wg(NQ), D(NQ * NQ), xq(MQ), wq(MQ), J(MQ * NQ), Dq(MQ * NQ), lam(NQ);
+    gll_rule(N, xg.data(), wg.data());
+    deriv_matrix(N, xg.data(), D.data());
+    gauss_legendre(MQ, xq.data(), wq.data());
+    for (int i = 0; i < NQ; ++i) {
+        double p = 1.0;
+        for (int k = 0; k < NQ; ++k)
+            if (k != i) p *= xg[i] - xg[k];
+        lam[i] = 1.0 / p;
+    }
+    for (int I = 0; I < MQ; ++I) {              // barycentric interpolation GLL -> GL (no shared nodes)
+        double den = 0.0;
+        for (int i = 0; i < NQ; ++i) den += lam[i] / (xq[I] - xg[i]);
+        for (int i = 0; i < NQ; ++i) J[I * NQ + i] = lam[i] / (xq[I] - xg[i]) / den;
+    }
+    for (int I = 0; I < MQ; ++I)
+        for (int i = 0; i < NQ; ++i) {
+            double s = 0.0;
+            for (int m = 0; m < NQ; ++m) s += J[I * NQ + m] * D[m * NQ + i];
+            Dq[I * NQ + i] = s;
+        }
+    cudaError_t e;
+    if ((e = cudaMemcpyToSymbol(c_Jq, J.data(), sizeof(double) * J.size(), sizeof(double) * 160 * N)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyToSymbol(c_Dq, Dq.data(), sizeof(double) * Dq.size(), sizeof(double) * 160 * N)) != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(c_wq, wq.data(), sizeof(double) * MQ, sizeof(double) * 16 * N);
+}
+
+template <int NQ>
+static cudaError_t geom_launch(int64_t E, const double *xyz, double *G9, unsigned long long *bad, cudaStream_t s)
+{
+    using C = MK<NQ>;
+    const size_t smem = sizeof(double) * (3 * C::SZ_U + 2 * C::SZ_A + 3 * C::SZ_AA);
+    cudaError_t e = cudaFuncSetAttribute(makef_geom_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)std::min<int64_t>(E, 148 * 2);
+    makef_geom_kernel<NQ><<<grid, C::NT, smem, s>>>(E, xyz, E * C::P3, G9, bad);
+    return cudaGetLastError();
+}
+
+template <int NQ>
+static cudaError_t apply_launch(int64_t E, const double *G9, const double *u0, const double *u1, const double *u2,
+                                double *f0, double *f1, double *f2, cudaStream_t s)
+{
+    using C = MK<NQ>;
+    const size_t smem = sizeof(double) * C::SMEM_D;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(makef_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    int per_sm = (int)((227 * 1024) / (smem + 1024));
+    per_sm = std::max(1, std::min(per_sm, 2048 / C::NT));
+    const int grid = (int)std::min<int64_t>(E, 148 * (int64_t)per_sm);
+    makef_kernel<NQ><<<grid, C::NT, smem, s>>>(E, G9, u0, u1, u2, f0, f1, f2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_makef_geom(int N, int64_t E, const double *xyz, double *G9, unsigned long long *bad, cudaStream_t s)
+{
+    if (E <= 0) return cudaSuccess;
+    switch (N + 1) {
+#define NEK_CASE(NQ) case NQ: return geom_launch<NQ>(E, xyz, G9, bad, s);
+        NEK_CASE(2) NEK_CASE(3) NEK_CASE(4) NEK_CASE(5) NEK_CASE(6) NEK_CASE(7) NEK_CASE(8) NEK_CASE(9) NEK_CASE(10)
+#undef NEK_CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_makef(int N, int64_t E, const double *G9, const double *u0, const double *u1, const double *u2,
+                         double *f0, double *f1, double *f2, cudaStream_t s)
+{
+    if (E <= 0) return cudaSuccess;
+    switch (N + 1) {
+#define NEK_CASE(NQ) case NQ: return apply_launch<NQ>(E, G9, u0, u1, u2, f0, f1, f2, s);
+        NEK_CASE(2) NEK_CASE(3) NEK_CASE(4) NEK_CASE(5) NEK_CASE(6) NEK_CASE(7) NEK_CASE(8) NEK_CASE(9) NEK_CASE(10)
+#undef NEK_CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace nekb200
+
+namespace nekb200 {
+
+// FP64 FMA throughput probe (SURVEY 8(d) "FP64 DFMA peak: an unrolled register-only FMA chain"):
+// 8 independent chains per thread, 1184 CTAs x 256 threads; the roofline denominator of makef.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(int iters, double seed, double *out)
+{
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+    const double m = 0.999999, c = 1e-7;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 12345.678) out[0] = s;   // keep the chains alive
+}
+
+}  // namespace nekb200
+
+extern "C" int nek_probe_dfma_tflops(int device, double *tflops)
+{
+    using namespace nekb200;
+    if (!tflops) return NEK_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return NEK_ENODEV;
+    double *out = nullptr;
+    if (cudaMalloc((void **)&out, sizeof(double)) != cudaSuccess) return NEK_ENOMEM;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    const int grid = 148 * 8, iters = 4096;
+    dfma_probe_kernel<<<grid, 256>>>(64, 1.0, out);          // warm-up
+    cudaEventRecord(a);
+    dfma_probe_kernel<<<grid, 256>>>(iters, 1.0, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return NEK_ECUDA;
+    *tflops = 2.0 * (double)grid * 256 * iters * 16 * 8 / (ms * 1e-3) / 1e12;
+    return NEK_OK;
+}

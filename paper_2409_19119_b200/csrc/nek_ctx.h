@@ -177,6 +177,13 @@ cudaError_t launch_pcg_pupdate(int64_t n, const double *dinv, const double *r, d
 int vec_blocks();
 int upd_blocks();
 
+// makef.cu: dealiased advection (NEXT #4)
+int makef_lattice(int N);
+cudaError_t makef_upload(int N);
+cudaError_t launch_makef_geom(int N, int64_t E, const double *xyz, double *G9, unsigned long long *bad, cudaStream_t s);
+cudaError_t launch_makef(int N, int64_t E, const double *G9, const double *u0, const double *u1, const double *u2,
+                         double *f0, double *f1, double *f2, cudaStream_t s);
+
 // pmg_kernels.cuh
 template <class T>
 cudaError_t launch_prolong_add(int64_t E, int Nc, int Nf, const T *J, const T *ec, T *uf, const int *done,

@@ -106,6 +106,11 @@ _sig = {
     "nek_pmg_solve": ([_P, _P, _P, _D, _I, ctypes.POINTER(_I), ctypes.POINTER(_D), _P, _P], _I),
     "nek_pmg_info": ([_P, ctypes.POINTER(nek_pmg_info_t)], _I),
     "nek_pmg_free": ([_P], _I),
+    "nek_makef_create": ([_P, _P, _I, ctypes.POINTER(_P), _P], _I),
+    "nek_makef_apply": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
+    "nek_makef_lattice": ([_P], _I),
+    "nek_makef_free": ([_P], _I),
+    "nek_probe_dfma_tflops": ([_I, ctypes.POINTER(_D)], _I),
     "nek_plan_create": ([ctypes.POINTER(_P), _I64, _I, _P, _P, _P], _I),
     "nek_plan_surface_gids": ([_P, _P], _I64),
     "nek_plan_set_ranks": ([_P, _I, _I, _P, _P], _I),
@@ -406,6 +411,48 @@ class PMG:
     def free(self):
         if self._h:
             _lib.nek_pmg_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def probe_fp64_tflops(device=0) -> float:
+    """nek_probe_dfma_tflops: measured FP64 FMA throughput (TFLOP/s)."""
+    v = ctypes.c_double(0.0)
+    _check(_lib.nek_probe_dfma_tflops(int(device), ctypes.byref(v)))
+    return v.value
+
+
+class Makef:
+    """nek_makef_*: dealiased advection F_c = -(phi_l, u . grad u_c) on the 3/2-rule Gauss-Legendre
+    lattice.  xyz: the (3, E*(N+1)^3) coordinates given to setup."""
+
+    def __init__(self, ctx: Context, xyz, M=0):
+        self.ctx = ctx
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        if xyz.size != 3 * ctx.n:
+            raise ValueError("xyz must hold 3*E*(N+1)^3 entries")
+        h = ctypes.c_void_p()
+        _check(_lib.nek_makef_create(ctx.handle, _np_ptr(xyz), int(M), ctypes.byref(h), None), ctx.handle)
+        self._h = h
+        self.M = _lib.nek_makef_lattice(h)
+
+    def apply(self, u, v, w, fu, fv, fw):
+        ps, ss = [], []
+        for a, name, wr in ((u, "u", False), (v, "v", False), (w, "w", False), (fu, "fu", True), (fv, "fv", True),
+                            (fw, "fw", True)):
+            p_, s_ = _field_ptr(a, self.ctx.n, name, writable=wr)
+            ps.append(p_); ss.append(s_)
+        _check(_lib.nek_makef_apply(self._h, *ps, _stream_of(*ss)), self.ctx.handle)
+        return fu, fv, fw
+
+    def free(self):
+        if self._h:
+            _lib.nek_makef_free(self._h)
             self._h = None
 
     def __del__(self):
