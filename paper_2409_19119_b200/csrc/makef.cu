@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "nek_ctx.h"
@@ -249,6 +250,179 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
     }
 }
 
+// Variant with the three velocity components merged in every stage (9 barriers per element instead
+// of 26, 192..576 lines per stage): one CTA per SM, the whole 12^3 working set of an element (values,
+// contravariant velocity and the three integrands) resident in shared memory (226 KB at N = 7).
+template <int NQ>
+struct MK3 {
+    using B = MK<NQ>;
+    static constexpr int MQ = B::MQ, M3 = B::M3, SZ_U = B::SZ_U, SZ_A = B::SZ_A, SZ_AA = B::SZ_AA;
+    static constexpr int SMEM_D = 3 * SZ_U + 6 * SZ_A + 9 * SZ_AA + 6 * M3;
+    static constexpr bool FITS = SMEM_D * 8 <= 227 * 1024;
+};
+
+template <int NQ, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    makef3_kernel(int64_t E, const double *__restrict__ G9, const double *__restrict__ u0,
+                  const double *__restrict__ u1, const double *__restrict__ u2, double *__restrict__ f0,
+                  double *__restrict__ f1, double *__restrict__ f2)
+{
+    using C = MK<NQ>;
+    constexpr int MQ = C::MQ, P3 = C::P3, M3 = C::M3, PN = C::PN, PM = C::PM;
+    constexpr int SZ_U = C::SZ_U, SZ_A = C::SZ_A, SZ_AA = C::SZ_AA;
+    extern __shared__ __align__(16) double sm[];
+    double *U3 = sm;                       // [3][NQ][NQ][PN]
+    double *SA = U3 + 3 * SZ_U;            // [3][NQ][NQ][PM]   A, later P2
+    double *SB = SA + 3 * SZ_A;            // [3][NQ][NQ][PM]   B
+    double *AA = SB + 3 * SZ_A;            // [3][NQ][MQ][PM]   AA, later P1
+    double *AD = AA + 3 * SZ_AA;
+    double *BA = AD + 3 * SZ_AA;
+    double *UT = BA + 3 * SZ_AA;           // [3][M3]  U, then Ut
+    double *F = UT + 3 * M3;               // [3][M3]
+    const int t = threadIdx.x;
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        for (int q = t; q < 3 * P3; q += NT) {
+            const int c = q / P3, p = q - c * P3;
+            const double *src = c == 0 ? u0 : c == 1 ? u1 : u2;
+            U3[c * SZ_U + (p / NQ) * PN + p % NQ] = src[e * P3 + p];
+        }
+        __syncthreads();
+        for (int L = t; L < 3 * NQ * NQ; L += NT) {                  // i: A = J u, B = Dq u
+            const int c = L / (NQ * NQ), kj = L % (NQ * NQ);
+            double x[NQ];
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) x[m] = U3[c * SZ_U + kj * PN + m];
+            double *oa = SA + c * SZ_A + kj * PM, *ob = SB + c * SZ_A + kj * PM;
+#pragma unroll 2
+            for (int I = 0; I < MQ; ++I) {
+                double a = 0.0, b = 0.0;
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) { a = fma(Jm<NQ>(I, m), x[m], a); b = fma(Dm<NQ>(I, m), x[m], b); }
+                oa[I] = a;
+                ob[I] = b;
+            }
+        }
+        __syncthreads();
+        for (int L = t; L < 6 * NQ * MQ; L += NT) {                  // j: AA, AD from A; BA from B
+            const int cw = L / (NQ * MQ), r = L % (NQ * MQ), k = r / MQ, I = r % MQ;
+            const int c = cw >> 1, which = cw & 1;
+            const double *in = (which == 0 ? SA : SB) + c * SZ_A;
+            double x[NQ];
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) x[m] = in[(k * NQ + m) * PM + I];
+            if (which == 0) {
+#pragma unroll 2
+                for (int J = 0; J < MQ; ++J) {
+                    double a = 0.0, d = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) { a = fma(Jm<NQ>(J, m), x[m], a); d = fma(Dm<NQ>(J, m), x[m], d); }
+                    AA[c * SZ_AA + (k * MQ + J) * PM + I] = a;
+                    AD[c * SZ_AA + (k * MQ + J) * PM + I] = d;
+                }
+            } else {
+#pragma unroll 2
+                for (int J = 0; J < MQ; ++J) {
+                    double a = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) a = fma(Jm<NQ>(J, m), x[m], a);
+                    BA[c * SZ_AA + (k * MQ + J) * PM + I] = a;
+                }
+            }
+        }
+        __syncthreads();
+        for (int L = t; L < 3 * MQ * MQ; L += NT) {                  // k: U = J AA
+            const int c = L / (MQ * MQ), JI = L % (MQ * MQ), J = JI / MQ, I = JI % MQ;
+            double x[NQ];
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) x[m] = AA[c * SZ_AA + (m * MQ + J) * PM + I];
+#pragma unroll 2
+            for (int K = 0; K < MQ; ++K) {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) s = fma(Jm<NQ>(K, m), x[m], s);
+                UT[c * M3 + K * MQ * MQ + JI] = s;
+            }
+        }
+        __syncthreads();
+        const double *Ge = G9 + e * 9 * (int64_t)M3;                 // Ut = G U, in place
+        for (int q = t; q < M3; q += NT) {
+            const double ux = UT[q], uy = UT[M3 + q], uz = UT[2 * M3 + q];
+            double g[9];
+#pragma unroll
+            for (int a = 0; a < 9; ++a) g[a] = __ldcs(Ge + a * M3 + q);
+            UT[q] = g[0] * ux + g[1] * uy + g[2] * uz;
+            UT[M3 + q] = g[3] * ux + g[4] * uy + g[5] * uz;
+            UT[2 * M3 + q] = g[6] * ux + g[7] * uy + g[8] * uz;
+        }
+        __syncthreads();
+        for (int L = t; L < 3 * MQ * MQ; L += NT) {                  // k: d_r, d_s, d_t and F_c
+            const int c = L / (MQ * MQ), JI = L % (MQ * MQ), J = JI / MQ, I = JI % MQ;
+            double xa[NQ], xd[NQ], xb[NQ];
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) {
+                const int o = c * SZ_AA + (m * MQ + J) * PM + I;
+                xa[m] = AA[o]; xd[m] = AD[o]; xb[m] = BA[o];
+            }
+#pragma unroll 2
+            for (int K = 0; K < MQ; ++K) {
+                double dr = 0.0, ds = 0.0, dt = 0.0;
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) {
+                    dr = fma(Jm<NQ>(K, m), xb[m], dr);
+                    ds = fma(Jm<NQ>(K, m), xd[m], ds);
+                    dt = fma(Dm<NQ>(K, m), xa[m], dt);
+                }
+                const int q = K * MQ * MQ + JI;
+                F[c * M3 + q] = UT[q] * dr + UT[M3 + q] * ds + UT[2 * M3 + q] * dt;
+            }
+        }
+        __syncthreads();
+        for (int L = t; L < 3 * MQ * MQ; L += NT) {                  // k^T: P1 into AA
+            const int c = L / (MQ * MQ), JI = L % (MQ * MQ), J = JI / MQ, I = JI % MQ;
+            double x[MQ];
+#pragma unroll
+            for (int K = 0; K < MQ; ++K) x[K] = F[c * M3 + K * MQ * MQ + JI];
+#pragma unroll 2
+            for (int k = 0; k < NQ; ++k) {
+                double s = 0.0;
+#pragma unroll
+                for (int K = 0; K < MQ; ++K) s = fma(Jm<NQ>(K, k), x[K], s);
+                AA[c * SZ_AA + (k * MQ + J) * PM + I] = s;
+            }
+        }
+        __syncthreads();
+        for (int L = t; L < 3 * NQ * MQ; L += NT) {                  // j^T: P2 into SA
+            const int c = L / (NQ * MQ), r = L % (NQ * MQ), k = r / MQ, I = r % MQ;
+            double x[MQ];
+#pragma unroll
+            for (int J = 0; J < MQ; ++J) x[J] = AA[c * SZ_AA + (k * MQ + J) * PM + I];
+#pragma unroll 2
+            for (int j = 0; j < NQ; ++j) {
+                double s = 0.0;
+#pragma unroll
+                for (int J = 0; J < MQ; ++J) s = fma(Jm<NQ>(J, j), x[J], s);
+                SA[c * SZ_A + (k * NQ + j) * PM + I] = s;
+            }
+        }
+        __syncthreads();
+        for (int L = t; L < 3 * NQ * NQ; L += NT) {                  // i^T: out = -J^T P2
+            const int c = L / (NQ * NQ), kj = L % (NQ * NQ);
+            double x[MQ];
+#pragma unroll
+            for (int I = 0; I < MQ; ++I) x[I] = SA[c * SZ_A + kj * PM + I];
+            double *fo = (c == 0 ? f0 : c == 1 ? f1 : f2) + e * P3 + kj * NQ;
+#pragma unroll 2
+            for (int i = 0; i < NQ; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int I = 0; I < MQ; ++I) s = fma(Jm<NQ>(I, i), x[I], s);
+                fo[i] = -s;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // G_ab = rho J d r_a / d x_b at the fine points (setup; reading M1).  One element per CTA
 // iteration, the same line-owned sum factorisation as the apply: for each coordinate x_d the three
 // reference derivatives at the fine points (stored as Jacobian entries [3d + a] in G9), then per
@@ -427,10 +601,43 @@ static cudaError_t geom_launch(int64_t E, const double *xyz, double *G9, unsigne
     return cudaGetLastError();
 }
 
+template <int NQ, int NT>
+static cudaError_t apply3_launch(int64_t E, const double *G9, const double *u0, const double *u1, const double *u2,
+                                 double *f0, double *f1, double *f2, cudaStream_t s)
+{
+    const size_t smem = sizeof(double) * MK3<NQ>::SMEM_D;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(makef3_kernel<NQ, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int per_sm = std::max(1, std::min((int)((227 * 1024) / (smem + 1024)), 2048 / NT));
+    const int grid = (int)std::min<int64_t>(E, 148 * (int64_t)per_sm);
+    makef3_kernel<NQ, NT><<<grid, NT, smem, s>>>(E, G9, u0, u1, u2, f0, f1, f2);
+    return cudaGetLastError();
+}
+
+static int makef_variant()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *env = getenv("NEK_MAKEF_VARIANT");   // 0: per-component stages, 1: merged (256), 2: merged (384)
+        v = env ? atoi(env) : 1;
+    }
+    return v;
+}
+
 template <int NQ>
 static cudaError_t apply_launch(int64_t E, const double *G9, const double *u0, const double *u1, const double *u2,
                                 double *f0, double *f1, double *f2, cudaStream_t s)
 {
+    if constexpr (MK3<NQ>::FITS) {
+        const int v = makef_variant();
+        if (v == 1) return apply3_launch<NQ, 256>(E, G9, u0, u1, u2, f0, f1, f2, s);
+        if (v == 2) return apply3_launch<NQ, 384>(E, G9, u0, u1, u2, f0, f1, f2, s);
+    }
     using C = MK<NQ>;
     const size_t smem = sizeof(double) * C::SMEM_D;
     static bool attr = false;
