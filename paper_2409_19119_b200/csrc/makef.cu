@@ -345,14 +345,26 @@ __global__ void __launch_bounds__(NT, 1)
         }
         __syncthreads();
         const double *Ge = G9 + e * 9 * (int64_t)M3;                 // Ut = G U, in place
-        for (int q = t; q < M3; q += NT) {
-            const double ux = UT[q], uy = UT[M3 + q], uz = UT[2 * M3 + q];
-            double g[9];
+        for (int q0 = t; q0 < M3; q0 += 4 * NT) {
+            double g[4][9];
 #pragma unroll
-            for (int a = 0; a < 9; ++a) g[a] = __ldcs(Ge + a * M3 + q);
-            UT[q] = g[0] * ux + g[1] * uy + g[2] * uz;
-            UT[M3 + q] = g[3] * ux + g[4] * uy + g[5] * uz;
-            UT[2 * M3 + q] = g[6] * ux + g[7] * uy + g[8] * uz;
+            for (int h = 0; h < 4; ++h) {
+                const int q = q0 + h * NT;
+                if (q < M3) {
+#pragma unroll
+                    for (int a = 0; a < 9; ++a) g[h][a] = __ldcs(Ge + a * M3 + q);
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int q = q0 + h * NT;
+                if (q < M3) {
+                    const double ux = UT[q], uy = UT[M3 + q], uz = UT[2 * M3 + q];
+                    UT[q] = g[h][0] * ux + g[h][1] * uy + g[h][2] * uz;
+                    UT[M3 + q] = g[h][3] * ux + g[h][4] * uy + g[h][5] * uz;
+                    UT[2 * M3 + q] = g[h][6] * ux + g[h][7] * uy + g[h][8] * uz;
+                }
+            }
         }
         __syncthreads();
         for (int L = t; L < 3 * MQ * MQ; L += NT) {                  // k: d_r, d_s, d_t and F_c
@@ -623,8 +635,10 @@ static int makef_variant()
 {
     static int v = -1;
     if (v < 0) {
-        const char *env = getenv("NEK_MAKEF_VARIANT");   // 0: per-component stages, 1: merged (256), 2: merged (384)
-        v = env ? atoi(env) : 1;
+        // 0: per-component stages, two CTAs per SM (default, measured fastest); 1 / 2: components merged
+        // in every stage, one CTA per SM with 256 / 384 threads
+        const char *env = getenv("NEK_MAKEF_VARIANT");
+        v = env ? atoi(env) : 0;
     }
     return v;
 }
