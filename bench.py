@@ -410,6 +410,7 @@ def main():
     pm = [float(v) for v in vals.cpu()[3:3 + len(pm)]]
     pj = [float(v) for v in vals.cpu()[3 + len(pm):3 + len(pm) + len(pj)]]
     mkv = [float(v) for v in vals.cpu()[3 + len(pm) + len(pj):]]
+    n_dof_total = mesh.n_dof * world
     if mk is not None:
         ms = mkv[0]
         gbs = mk["bytes_per_element"] * mesh.E / (ms * 1e-3) / 1e9
@@ -427,7 +428,6 @@ def main():
                              "speedup_vs_fp64_pmg": pm[1] / pm[3] if pm[3] > 0 else None},
                     "note": "time to ||r|| <= 1e-8 ||b|| on the same mesh and right-hand side, CUDA events, "
                             "max over ranks; pMG schedule / Chebyshev degrees as listed (DESIGN.md readings P1-P7)"})
-    n_dof_total = mesh.n_dof * world
     value = n_dof_total * args.iters * args.steps / (t_ms * 1e-3) / 1e9
     ax_gdofs = n_dof_total * reps / (ax_ms * 1e-3) / 1e9
 
