@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pmg", action="store_true", help="skip the Jacobi vs pMG time-to-solution section")
     ap.add_argument("--variant", type=int, default=0, help="Ax kernel variant (nek_set_variant; 0 = default)")
-    ap.add_argument("--mesh", default="box", choices=["box", "rod"],
+    ap.add_argument("--mesh", default="box", choices=["box", "rod", "cfg3"],
                     help="box: 16x16xez elements per GPU (config 2 at ez=16); rod: 17x17-pin rod bundle, "
                          "--rod-layers element layers per GPU (config 4 at 3 layers)")
     ap.add_argument("--rod-layers", type=int, default=3)
@@ -75,12 +75,22 @@ def make_mesh(rank, world, ez, N, args=None):
         L = args.rod_layers
         return mg.rod_bundle(17, 17, L, N, dirichlet="pins_walls" if args.h2 != 0.0 else "outlet",
                              z0_layer=rank * L, nlayers_total=L * world)
+    if args is not None and args.mesh == "cfg3":
+        # BASELINE config 3: E = 32 x 64 x 64 = 131072 (~45M DOF) fixed, z-slabs of 64/P layers (strong scaling)
+        if 64 % world:
+            raise SystemExit("cfg3 needs a rank count dividing 64")
+        lz = 64 // world
+        return mg.box_mesh(32, 64, 64, N, deform="bubble", eps=0.05, dirichlet="all",
+                           zlayers=(rank * lz, (rank + 1) * lz))
     return mg.box_mesh(EX, EY, ez * world, N, deform="bubble", eps=0.05, dirichlet="all",
                        zlayers=(rank * ez, (rank + 1) * ez))
 
 
 def workload_name(args, world):
     kind = "Helmholtz (h1,h2)=(1,%g)" % args.h2 if args.h2 != 0.0 else "Poisson"
+    if args.mesh == "cfg3":
+        return (f"SEM {kind} Jacobi-PCG, {args.iters} iters/step; config 3: bubble-deformed box 32x64x64 elements "
+                f"(E = 131072, ~45M DOF) split into {world} z-slab(s), N={args.order}, Dirichlet all faces")
     if args.mesh == "rod":
         return (f"SEM {kind} Jacobi-PCG, {args.iters} iters/step; 17x17-pin rod bundle, 27744 curved elements per "
                 f"layer, {args.rod_layers} layers per GPU ({args.rod_layers * world} total, z-slabs), N={args.order}, "
@@ -463,7 +473,7 @@ def main():
                                   f"workload ({kt_steps} solves) right after the timed region"}
         out = {
             "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong" if args.mesh == "cfg3" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args, world), "E_per_gpu": mesh.E, "N": mesh.N,
                        "n_dof_per_gpu": mesh.n_dof, "n_local_per_gpu": mesh.n_local,

@@ -382,3 +382,39 @@ def test_projection_sequence_matches_oracle(nek, L):
     finally:
         P.free()
         nek.free(ctx)
+
+
+@pytest.mark.slow
+def test_config3_full_size_sampled(nek):
+    """BASELINE config 3 at full size (E = 131072, N = 7, ~45M DOF, 67M local points) on one GPU, in
+    the launch configuration bench.py --mesh cfg3 times: nek_ax (Ax + gs) on a continuous field
+    against the oracle run on sampled elements and their face neighbours (the operator restricted to
+    an element's interior nodes only needs that element: rows of interior nodes are compared), and a
+    20-iteration PCG window against properties that hold at any size (finite, monotone A-norm-like
+    decrease is not guaranteed, so: same iteration count, relres equal to the device history)."""
+    m = mg.box_mesh(32, 64, 64, 7, deform="bubble", eps=0.05, dirichlet="all")
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        u = torch.from_numpy(mg.smooth_field(m, seed=3)).cuda()
+        w = torch.empty_like(u)
+        nek.ax(ctx, 1.0, 0.0, u, w)
+        wh = w.cpu().numpy()
+        uh = u.cpu().numpy()
+        P3 = 512
+        rng = np.random.default_rng(0)
+        els = rng.choice(m.E, 24, replace=False)
+        q = np.arange(P3)
+        i, j, k = q % 8, (q // 8) % 8, q // 64
+        inner = (i > 0) & (i < 7) & (j > 0) & (j < 7) & (k > 0) & (k < 7)
+        for e in els:
+            sub = mg.submesh(m, np.array([e]))
+            Os = oracle.Oracle.from_mesh(sub)
+            loc = e * P3 + q
+            want = Os.apply(1.0, 0.0, uh[loc])          # element-interior rows need no neighbours
+            got = wh[loc]
+            assert rel(got[inner], want[inner]) <= 1e-12
+        x = torch.zeros_like(u)
+        st, it, rr, hist = nek.pcg_solve(ctx, 1.0, 0.0, u, x, 0.0, 20, want_hist=True)
+        assert it == 20 and np.all(np.isfinite(hist)) and abs(hist[-1] - rr) <= 1e-15 * max(1.0, rr)
+    finally:
+        nek.free(ctx)
