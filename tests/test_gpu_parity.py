@@ -388,18 +388,19 @@ def test_projection_sequence_matches_oracle(nek, L):
 def test_config3_full_size_sampled(nek):
     """BASELINE config 3 at full size (E = 131072, N = 7, ~45M DOF, 67M local points) on one GPU, in
     the launch configuration bench.py --mesh cfg3 times: nek_ax (Ax + gs) on a continuous field
-    against the oracle run on sampled elements and their face neighbours (the operator restricted to
-    an element's interior nodes only needs that element: rows of interior nodes are compared), and a
+    against the oracle run on sampled elements (the operator restricted to an element's interior nodes
+    only needs that element: rows of interior nodes are compared, normwise against ||w||), and a
     20-iteration PCG window against properties that hold at any size (finite, monotone A-norm-like
     decrease is not guaranteed, so: same iteration count, relres equal to the device history)."""
     m = mg.box_mesh(32, 64, 64, 7, deform="bubble", eps=0.05, dirichlet="all")
     ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
     try:
-        u = torch.from_numpy(mg.smooth_field(m, seed=3)).cuda()
+        u = torch.from_numpy(mg.random_evector(m, seed=3)).cuda()     # O(1) entries: no cancellation
         w = torch.empty_like(u)
         nek.ax(ctx, 1.0, 0.0, u, w)
         wh = w.cpu().numpy()
         uh = u.cpu().numpy()
+        wmax = np.abs(wh).max()
         P3 = 512
         rng = np.random.default_rng(0)
         els = rng.choice(m.E, 24, replace=False)
@@ -412,8 +413,9 @@ def test_config3_full_size_sampled(nek):
             loc = e * P3 + q
             want = Os.apply(1.0, 0.0, uh[loc])          # element-interior rows need no neighbours
             got = wh[loc]
-            assert rel(got[inner], want[inner]) <= 1e-12
+            assert np.abs(got[inner] - want[inner]).max() <= 1e-12 * wmax     # normwise (reading 16)
         x = torch.zeros_like(u)
+        u = torch.from_numpy(mg.smooth_field(m, seed=3)).cuda()
         st, it, rr, hist = nek.pcg_solve(ctx, 1.0, 0.0, u, x, 0.0, 20, want_hist=True)
         assert it == 20 and np.all(np.isfinite(hist)) and abs(hist[-1] - rr) <= 1e-15 * max(1.0, rr)
     finally:
