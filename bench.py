@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--order", type=int, default=NORD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pmg", action="store_true", help="skip the Jacobi vs pMG time-to-solution section")
+    ap.add_argument("--no-peaks", action="store_true", help="skip the on-box peak probes")
     ap.add_argument("--variant", type=int, default=0, help="Ax kernel variant (nek_set_variant; 0 = default)")
     ap.add_argument("--mesh", default="box", choices=["box", "rod", "cfg3"],
                     help="box: 16x16xez elements per GPU (config 2 at ez=16); rod: 17x17-pin rod bundle, "
@@ -411,6 +412,48 @@ def main():
         K.free()
         del Uv, Fv
     log("makef done")
+    # ---- peaks measured on this box: FP64 streaming HBM, shared memory, FP64 FMA;
+    # at N > 1 also NCCL allreduce latency of the PCG scalars and pairwise send/recv bandwidth
+    peaks_box = None
+    if not args.no_peaks:
+        hb = nek.probe_hbm_gbps(local, 4 << 30)
+        peaks_box = {"hbm_fp64_GBps": hb, "smem_TBps": nek.probe_smem_tbps(local),
+                     "fp64_fma_TFLOPs": nek.probe_fp64_tflops(local),
+                     "note": "double2 read / write / copy kernels over 4 GiB (best of 5), conflict-free "
+                             "ld.shared.f64, register FMA chains; CUDA events"}
+        if dist:
+            lat = {}
+            for cnt in (1, 2):
+                t = torch.zeros(cnt, dtype=torch.float64, device=dev)
+                for _ in range(20):
+                    dist.all_reduce(t)
+                barrier(); torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(200):
+                    dist.all_reduce(t)
+                e1.record(stream); e1.synchronize()
+                lat[f"{8 * cnt}B_us"] = e0.elapsed_time(e1) * 1e3 / 200
+            bw = {}
+            for nb in (1 << 16, 1 << 20, 1 << 26):
+                buf = torch.zeros(nb // 8, dtype=torch.float64, device=dev)
+                reps = 20
+                barrier(); torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(reps):
+                    if rank == 0:
+                        dist.send(buf, 1)
+                    elif rank == 1:
+                        dist.recv(buf, 0)
+                e1.record(stream); e1.synchronize()
+                ms = e0.elapsed_time(e1)
+                msv = torch.tensor([ms if rank < 2 else 0.0], dtype=torch.float64, device=dev)
+                dist.all_reduce(msv, op=dist.ReduceOp.MAX)
+                bw[f"{nb >> 10}KiB"] = nb * reps / (float(msv) * 1e-3) / 1e9
+            peaks_box["nccl_allreduce_latency"] = lat
+            peaks_box["nccl_sendrecv_GBps_rank0_to_1"] = bw
+    log("peaks done")
 
     # ---- max over ranks
     vals = torch.tensor([t_ms, ax_ms, e2e_s] + pm + pj + mkv, dtype=torch.float64, device=dev)
@@ -491,7 +534,13 @@ def main():
                     "h2d_bytes_per_step": mesh.n_local * 8, "d2h_bytes_per_step": mesh.n_local * 8},
             "roofline": roofline, "clocks": clocks, "pmg": pmg, "projection": proj, "makef": mk,
             "halo": {"doubles_per_gs": info["halo_doubles"], "neighbors": info["n_neighbors"],
-                     "transport": {0: "none", 1: "nccl", 2: "nvlink-p2p"}[info["transport"]]},
+                     "transport": {0: "none", 1: "nccl", 2: "nvlink-p2p"}[info["transport"]],
+                     "GBps": (info["halo_doubles"] * 8 * args.iters / (stats["halo_ms"] / kt_steps * 1e-3) / 1e9
+                              if kt_ms and stats["halo_ms"] > 0 else None),
+                     "ms_per_step": stats["halo_ms"] / kt_steps if kt_ms else None,
+                     "note": "rank 0's interface doubles sent per exchange x iterations / event time of its "
+                             "halo kernels (pack + peer stores, or NCCL send/recv)"},
+            "peaks_box": peaks_box,
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(mesh, 50, args.h2)

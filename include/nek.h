@@ -259,6 +259,15 @@ int nek_makef_free(nek_makef *mk);
  * SURVEY 8(d)); the compute roofline denominator of makef. */
 int nek_probe_dfma_tflops(int device, double *tflops);
 
+/* Measurement probes (SURVEY 8(d) "Peaks to measure on the box"), not on the solver path:
+ * FP64 streaming bandwidth of `device` over `bytes` (>= 1 MiB; split into two buffers): a double2
+ * read-only kernel, a write-only kernel and a read+write copy (copy counts both directions), best of
+ * five after a warm-up, in GB/s; outputs may be NULL.  NEK_EINVAL for bytes < 1 MiB, NEK_ENOMEM if
+ * the buffers do not fit.  nek_probe_smem_tbps: aggregate conflict-free ld.shared.f64 bandwidth in
+ * TB/s (two 1024-thread CTAs per SM). */
+int nek_probe_hbm_gbps(int device, int64_t bytes, double *read_gbps, double *write_gbps, double *copy_gbps);
+int nek_probe_smem_tbps(int device, double *tbps);
+
 /* ----------------------------------------------------------- introspection */
 typedef struct {
     int64_t E;                 /* local elements                                   */

@@ -285,6 +285,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     int st;
     AxLaunch L;
     L.done = done;
+    L.keep = ctx->l2keep;
     if (fused) {
         L.fused = true;
         L.p = ctx->vp; L.x = ctx->vx; L.r = ctx->vr; L.dinv = ctx->vdinv; L.sc = ctx->sc;
@@ -694,7 +695,24 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     }
     // work vectors, reductions, scalars
     for (double **v : {&ctx->vr, &ctx->vp, &ctx->vw, &ctx->vx, &ctx->vdinv, &ctx->vtmp}) CK(dalloc(ctx, v, n));
-    ctx->npart = std::max<int64_t>(ax_partials_needed(1, N, E), 2 * vec_blocks());
+    ctx->npart = std::max<int64_t>(ax_partials_needed(1, N, E), std::max(2 * vec_blocks(), 2 * upd_blocks()));
+    {
+        // L2-resident PCG vectors: when p, r, Dinv, w (and x) plus the gather-scatter lists fit in the
+        // L2 next to the streamed metric factors (evict_first), keep them there (evict_last) across
+        // the kernels of an iteration; NEK_L2KEEP = 0 / 1 / 3 overrides the size rule
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+        const double vec = 8.0 * (double)n, idx = 4.0 * (double)ctx->nperm;
+        int keep = 0;
+        if (4 * vec + idx <= 0.6 * l2) keep = 1;
+        if (5 * vec + idx <= 0.6 * l2) keep = 3;
+        const char *kenv = getenv("NEK_L2KEEP");
+        if (kenv) keep = atoi(kenv);
+        ctx->l2keep = keep;
+        ctx->gsc.keep = keep & 1;
+        const char *senv = getenv("NEK_L2SETASIDE");
+        if (senv) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(senv) << 20);
+    }
     CK(dalloc(ctx, &ctx->part, ctx->npart));
     CK(dalloc(ctx, &ctx->red_loc, RED_N));
     if (ctx->nranks > 1) CK(dalloc(ctx, &ctx->red_all, RED_N * ctx->nranks));
@@ -839,7 +857,7 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, &m, gip));
+                                       ctx->counter + 2, ctx->s_main, &m, gip, ctx->l2keep));
             CK(launch_pcg_fin_p2p(ctx->sc, m, ctx->hist, ctx->s_main));
             ctx->stats.launches += 2; ctx->stats.vec_launches += 2;
         }
@@ -854,7 +872,7 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, nullptr, gip));
+                                       ctx->counter + 2, ctx->s_main, nullptr, gip, ctx->l2keep));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
         if (ctx->nranks > 1) {

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "ax_tma.cuh"
 #include "nek_ctx.h"
@@ -1033,7 +1034,8 @@ __global__ void __launch_bounds__(128, MINB)
                  double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
                  int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done,
                  double *pvec, double *__restrict__ xvec, const double *__restrict__ rvec,
-                 const double *__restrict__ dvec, const PcgScalars *sc, P2PMail mail, unsigned int ctas_total)
+                 const double *__restrict__ dvec, const PcgScalars *sc, P2PMail mail, unsigned int ctas_total,
+                 int keep)
 {
     constexpr int P3 = 512, N = 7;
     if (done && *(volatile const int *)done) return;
@@ -1042,6 +1044,7 @@ __global__ void __launch_bounds__(128, MINB)
     __shared__ uint64_t gfull[2];
     double beta = 0.0, alpha = 0.0;
     if (FUSED) { beta = sc->beta; alpha = sc->alpha; }
+    const uint64_t polv = tma::policy_keep(keep & 1), polx = tma::policy_keep(keep & 2);
     const int t = threadIdx.x, lane = t & 31, wq = t >> 5, q = lane & 3, r = lane >> 2;
     const int64_t nit = (int64_t)blockIdx.x < nelem ? (nelem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (t < 64) S.sD[t] = c_D[N][t];
@@ -1109,17 +1112,17 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
                 const int64_t l = e * P3 + 64 * (kb + kk) + 8 * r + 2 * q;
-                const double2 po = *reinterpret_cast<const double2 *>(pvec + l);
-                const double2 rv = *reinterpret_cast<const double2 *>(rvec + l);
-                const double2 dv = *reinterpret_cast<const double2 *>(dvec + l);
-                double2 xv = *reinterpret_cast<const double2 *>(xvec + l);
+                const double2 po = tma::ld2(pvec + l, polv);
+                const double2 rv = tma::ld2(rvec + l, polv);
+                const double2 dv = tma::ld2(dvec + l, polv);
+                double2 xv = tma::ld2(xvec + l, polx);
                 double2 pn;
                 pn.x = fma(beta, po.x, dv.x * rv.x);
                 pn.y = fma(beta, po.y, dv.y * rv.y);
                 xv.x = fma(alpha, po.x, xv.x);
                 xv.y = fma(alpha, po.y, xv.y);
-                *reinterpret_cast<double2 *>(pvec + l) = pn;
-                *reinterpret_cast<double2 *>(xvec + l) = xv;
+                tma::st2(pvec + l, pn, polv);
+                tma::st2(xvec + l, xv, polx);
                 *reinterpret_cast<double2 *>(&S.sU[par][kb + kk][r][2 * q]) = pn;
                 uk[kk] = pn;
                 if (!TMAG) {
@@ -1250,7 +1253,7 @@ __global__ void __launch_bounds__(128, MINB)
                 if (wd & 1u) v0 = 0.0;
                 if (wd & 2u) v1 = 0.0;
             }
-            *reinterpret_cast<double2 *>(w + l) = make_double2(v0, v1);
+            tma::st2(w + l, make_double2(v0, v1), polv);
             dot = fma(uk[kk].x, v0, dot);
             dot = fma(uk[kk].y, v1, dot);
         }
@@ -1283,12 +1286,12 @@ static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double
         ax_v5_kernel<HELM, true, MINB, L2PF, TMAG><<<(unsigned)grid, 128, dsm, s>>>(L.nelem, L.eoff, L.elist, L.p, G, wJ, mbits, h1, h2, w,
                                                                  L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                  L.done, L.p, L.x, L.r, L.dinv, L.sc, L.mail,
-                                                                 L.ctas_total ? L.ctas_total : (unsigned)grid);
+                                                                 L.ctas_total ? L.ctas_total : (unsigned)grid, L.keep);
     else
         ax_v5_kernel<HELM, false, MINB, L2PF, TMAG><<<(unsigned)grid, 128, dsm, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
                                                                   L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                   L.done, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                                                  L.mail, L.ctas_total ? L.ctas_total : (unsigned)grid);
+                                                                  L.mail, L.ctas_total ? L.ctas_total : (unsigned)grid, L.keep);
     return cudaGetLastError();
 }
 
@@ -1500,6 +1503,7 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
 }
 
 // ---------------------------------------------------------- gather-scatter
+constexpr int GS_PPT_DEFAULT = 8;
 // One thread per run: left fold in canonical order, then broadcast.
 __global__ void gs_local_kernel(int64_t nruns, const int32_t *__restrict__ perm, const int32_t *__restrict__ offs,
                                 double *__restrict__ v, const int *done)
@@ -1526,17 +1530,27 @@ cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *o
 // ascending: the sum order of every run is unchanged (bit-exact with the
 // oracle) but fixed-length runs need no offsets and load their indices as one
 // vector (one dependent load level fewer).
-constexpr int GS_PAIRS_PER_THREAD = 8, GS_QUADS_PER_THREAD = 4;
+// pairs / quads per thread: NEK_GS_PPT = 8 (8 pairs, 4 quads), 4 (4, 2), 2 (2, 1) or 1 (1, 1)
+static int gs_ppt()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NEK_GS_PPT");
+        v = e ? atoi(e) : GS_PPT_DEFAULT;
+        if (v != 1 && v != 2 && v != 4 && v != 8) v = GS_PPT_DEFAULT;
+    }
+    return v;
+}
 
 // Each warp takes a contiguous block of runs of one class and lane l handles
 // runs l, l+32, ... of it, so every warp-wide load touches consecutive runs
 // (first-touch order keeps their copies close in memory).
-template <class T>
+template <class T, int GS_PAIRS_PER_THREAD, int GS_QUADS_PER_THREAD>
 __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n2, const int2 *__restrict__ p2,
                                                 int64_t n4, const int4 *__restrict__ p4, int64_t n8,
                                                 const int4 *__restrict__ p8, int64_t ng,
                                                 const int32_t *__restrict__ pg, const int32_t *__restrict__ og,
-                                                T *__restrict__ v)
+                                                T *__restrict__ v, uint64_t pol)
 {
     const int64_t w2 = (n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD);
     const int64_t w4 = (n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD);
@@ -1546,13 +1560,13 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
         int2 c[GS_PAIRS_PER_THREAD];
         T a[GS_PAIRS_PER_THREAD], b[GS_PAIRS_PER_THREAD];
 #pragma unroll
-        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (r0 + 32 * q < n2) c[q] = p2[r0 + 32 * q];
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (r0 + 32 * q < n2) c[q] = tma::ldi2(p2 + r0 + 32 * q, pol);
 #pragma unroll
         for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
-            if (r0 + 32 * q < n2) { a[q] = v[c[q].x]; b[q] = v[c[q].y]; }
+            if (r0 + 32 * q < n2) { a[q] = tma::ld1(v + c[q].x, pol); b[q] = tma::ld1(v + c[q].y, pol); }
 #pragma unroll
         for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
-            if (r0 + 32 * q < n2) { const T s = a[q] + b[q]; v[c[q].x] = s; v[c[q].y] = s; }
+            if (r0 + 32 * q < n2) { const T s = a[q] + b[q]; tma::st1(v + c[q].x, s, pol); tma::st1(v + c[q].y, s, pol); }
         return;
     }
     wid -= w2;
@@ -1561,15 +1575,19 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
         int4 c[GS_QUADS_PER_THREAD];
         T a[GS_QUADS_PER_THREAD][4];
 #pragma unroll
-        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (r0 + 32 * q < n4) c[q] = p4[r0 + 32 * q];
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (r0 + 32 * q < n4) c[q] = tma::ldi4(p4 + r0 + 32 * q, pol);
 #pragma unroll
         for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
-            if (r0 + 32 * q < n4) { a[q][0] = v[c[q].x]; a[q][1] = v[c[q].y]; a[q][2] = v[c[q].z]; a[q][3] = v[c[q].w]; }
+            if (r0 + 32 * q < n4) {
+                a[q][0] = tma::ld1(v + c[q].x, pol); a[q][1] = tma::ld1(v + c[q].y, pol);
+                a[q][2] = tma::ld1(v + c[q].z, pol); a[q][3] = tma::ld1(v + c[q].w, pol);
+            }
 #pragma unroll
         for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
             if (r0 + 32 * q < n4) {
                 const T s = ((a[q][0] + a[q][1]) + a[q][2]) + a[q][3];
-                v[c[q].x] = s; v[c[q].y] = s; v[c[q].z] = s; v[c[q].w] = s;
+                tma::st1(v + c[q].x, s, pol); tma::st1(v + c[q].y, s, pol);
+                tma::st1(v + c[q].z, s, pol); tma::st1(v + c[q].w, s, pol);
             }
         return;
     }
@@ -1593,38 +1611,39 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
     }
 }
 
-template <class T>
+template <class T, int PPT>
 __global__ void __launch_bounds__(256)
     gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
                       const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
-                      const int32_t *__restrict__ og, T *__restrict__ v, const int *done)
+                      const int32_t *__restrict__ og, T *__restrict__ v, const int *done, int keep)
 {
     if (done && *(volatile const int *)done) return;
-    gs_classes_body((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, n2, p2, n4, p4, n8, p8,
-                    ng, pg, og, v);
+    gs_classes_body<T, PPT, (PPT > 1 ? PPT / 2 : 1)>((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, n2, p2, n4, p4, n8, p8,
+                    ng, pg, og, v, tma::policy_keep(keep));
 }
 
-static int64_t gs_class_warps(const GsClasses &C)
+static int64_t gs_class_warps(const GsClasses &C, int ppt)
 {
-    return (C.n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD) +
-           (C.n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD) + (C.n8 + 31) / 32 + (C.ng + 31) / 32;
+    const int qpt = ppt > 1 ? ppt / 2 : 1;
+    return (C.n2 + 32 * ppt - 1) / (32 * ppt) + (C.n4 + 32 * qpt - 1) / (32 * qpt) + (C.n8 + 31) / 32 +
+           (C.ng + 31) / 32;
 }
 
 // local runs (warps [0, cw)) and, after them, the halo unpack (warps [cw, ...)):
 // one lane per interface run waits for this epoch's halo of every neighbour,
 // folds the contributions in rank order and writes the total to the local copies.
-template <class T>
+template <class T, int PPT>
 __global__ void __launch_bounds__(256)
     gs_classes_unpack_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4,
                              int64_t n8, const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
                              const int32_t *__restrict__ og, int64_t cw, HaloUnpack U, T *__restrict__ v,
-                             const int *done)
+                             const int *done, int C_keep)
 {
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const bool skip = done && *(volatile const int *)done;
     if (wid < cw) {
-        if (!skip) gs_classes_body(wid, lane, n2, p2, n4, p4, n8, p8, ng, pg, og, v);
+        if (!skip) gs_classes_body<T, PPT, (PPT > 1 ? PPT / 2 : 1)>(wid, lane, n2, p2, n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(C_keep));
         return;
     }
     const uint64_t e = *(volatile const uint64_t *)(U.epochs + 2);
@@ -1650,21 +1669,30 @@ template <class T>
 cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, T *v, const int *done,
                                      cudaStream_t s)
 {
-    const int64_t cw = gs_class_warps(C), uw = (U.nifc + 31) / 32;
+    const int ppt = gs_ppt();
+    const int64_t cw = gs_class_warps(C, ppt), uw = (U.nifc + 31) / 32;
     const int64_t warps = cw + std::max<int64_t>(uw, 1);   // at least one waiting warp keeps epochs in step
-    gs_classes_unpack_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
-        C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8, (const int4 *)C.p8, C.ng, C.pg, C.og, cw, U, v,
-        done);
+    const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+#define NEK_GSU(PP)                                                                                                   \
+    gs_classes_unpack_kernel<T, PP><<<grid, 256, 0, s>>>(C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8,     \
+                                                        (const int4 *)C.p8, C.ng, C.pg, C.og, cw, U, v, done, C.keep)
+    if (ppt == 1) NEK_GSU(1); else if (ppt == 2) NEK_GSU(2); else if (ppt == 4) NEK_GSU(4); else NEK_GSU(8);
+#undef NEK_GSU
     return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_gs_classes(const GsClasses &C, T *v, const int *done, cudaStream_t s)
 {
-    const int64_t warps = gs_class_warps(C);
+    const int ppt = gs_ppt();
+    const int64_t warps = gs_class_warps(C, ppt);
     if (warps <= 0) return cudaSuccess;
-    gs_classes_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
-        C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8, (const int4 *)C.p8, C.ng, C.pg, C.og, v, done);
+    const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+#define NEK_GSC(PP)                                                                                                   \
+    gs_classes_kernel<T, PP><<<grid, 256, 0, s>>>(C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8,            \
+                                                 (const int4 *)C.p8, C.ng, C.pg, C.og, v, done, C.keep)
+    if (ppt == 1) NEK_GSC(1); else if (ppt == 2) NEK_GSC(2); else if (ppt == 4) NEK_GSC(4); else NEK_GSC(8);
+#undef NEK_GSC
     return cudaGetLastError();
 }
 
@@ -1798,8 +1826,20 @@ cudaError_t launch_copy_mask(int64_t n, const uint32_t *mbits, const T *src, T *
 // --------------------------------------------------------------------- PCG
 constexpr int VEC_THREADS = 256;
 constexpr int VEC_UNROLL = 4;
+constexpr int UPD_CFG_DEFAULT = 2;
 int vec_blocks() { return 148 * 4; }
-int upd_blocks() { return 148 * 2; }
+// residual-update CTAs per SM: NEK_UPD_CFG = 2 (4 double2 per thread per tile), 4 (4) or 8 (2)
+static int upd_cfg()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NEK_UPD_CFG");
+        v = e ? atoi(e) : UPD_CFG_DEFAULT;
+        if (v != 2 && v != 4 && v != 8) v = UPD_CFG_DEFAULT;
+    }
+    return v;
+}
+int upd_blocks() { return 148 * upd_cfg(); }
 
 // red_all holds [nranks][RED_N]; sums are taken in rank order.
 __device__ __forceinline__ double rank_sum(const double *red_all, int nranks, int slot)
@@ -2055,11 +2095,12 @@ __device__ __forceinline__ void pcg_bookkeep(PcgScalars *sc, double rho1, double
     __threadfence();
 }
 
-__global__ void __launch_bounds__(VEC_THREADS, 2)
+template <int UNR, int MINB>
+__global__ void __launch_bounds__(VEC_THREADS, MINB)
     pcg_update_fused_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                             const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ red_all,
                             int nranks, PcgScalars *sc, double *hist, double *__restrict__ part, double *dst,
-                            unsigned int *counter, P2PMail mail, GsInline gi)
+                            unsigned int *counter, P2PMail mail, GsInline gi, int keep)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ int s_last;
@@ -2079,28 +2120,27 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
         return;
     }
     const double alpha = sc->rho / sigma;
+    const uint64_t pol = tma::policy_keep(keep & 1);
     double a0 = 0.0, a1 = 0.0;
     const int64_t n2 = n >> 1;
-    const double2 *w2 = reinterpret_cast<const double2 *>(w), *d2 = reinterpret_cast<const double2 *>(dinv);
-    double2 *r2 = reinterpret_cast<double2 *>(r);
     const int2 *i2 = reinterpret_cast<const int2 *>(gi.idx);
-    const int64_t tile = (int64_t)VEC_UNROLL * blockDim.x;
+    const int64_t tile = (int64_t)UNR * blockDim.x;
     for (int64_t base = blockIdx.x * tile + threadIdx.x; base < n2; base += (int64_t)gridDim.x * tile) {
-        double2 wv[VEC_UNROLL], dv[VEC_UNROLL], rv[VEC_UNROLL];
-        uint32_t ow[VEC_UNROLL];
-        int2 id[VEC_UNROLL];
+        double2 wv[UNR], dv[UNR], rv[UNR];
+        uint32_t ow[UNR];
+        int2 id[UNR];
 #pragma unroll
-        for (int q = 0; q < VEC_UNROLL; ++q) {
+        for (int q = 0; q < UNR; ++q) {
             const int64_t h = base + (int64_t)q * blockDim.x;
             if (h < n2) {
-                wv[q] = w2[h]; dv[q] = d2[h]; rv[q] = r2[h];
-                ow[q] = __ldg(obits + ((2 * h) >> 5)) >> ((2 * h) & 31);
+                wv[q] = tma::ld2(w + 2 * h, pol); dv[q] = tma::ld2(dinv + 2 * h, pol); rv[q] = tma::ld2(r + 2 * h, pol);
+                ow[q] = tma::ldu(obits + ((2 * h) >> 5), pol) >> ((2 * h) & 31);
                 if (gi.idx) id[q] = i2[h];
             }
         }
         if (gi.idx) {   // the gather-scatter QQ^T of w, on the fly (canonical order, bit-exact)
 #pragma unroll
-            for (int q = 0; q < VEC_UNROLL; ++q) {
+            for (int q = 0; q < UNR; ++q) {
                 const int64_t h = base + (int64_t)q * blockDim.x;
                 if (h < n2) {
                     wv[q].x = w_assembled(id[q].x, wv[q].x, w, gi);
@@ -2109,11 +2149,11 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
             }
         }
 #pragma unroll
-        for (int q = 0; q < VEC_UNROLL; ++q) {
+        for (int q = 0; q < UNR; ++q) {
             const int64_t h = base + (int64_t)q * blockDim.x;
             if (h < n2) {
                 rv[q].x = fma(-alpha, wv[q].x, rv[q].x); rv[q].y = fma(-alpha, wv[q].y, rv[q].y);
-                r2[h] = rv[q];
+                tma::st2(r + 2 * h, rv[q], pol);
                 if (ow[q] & 1u) { a0 = fma(rv[q].x, dv[q].x * rv[q].x, a0); a1 = fma(rv[q].x, rv[q].x, a1); }
                 if (ow[q] & 2u) { a0 = fma(rv[q].y, dv[q].y * rv[q].y, a0); a1 = fma(rv[q].y, rv[q].y, a1); }
             }
@@ -2155,14 +2195,25 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail, const GsInline *gi)
+                                    const P2PMail *mail, const GsInline *gi, int keep)
 {
     P2PMail m;
     if (mail) m = *mail;
     GsInline g;
     if (gi) g = *gi;
-    pcg_update_fused_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist, part, dst,
-                                                         counter, m, g);
+    switch (nblk / 148) {
+    case 8:
+        pcg_update_fused_kernel<2, 8><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
+                                                                   part, dst, counter, m, g, keep);
+        break;
+    case 4:
+        pcg_update_fused_kernel<4, 4><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
+                                                                   part, dst, counter, m, g, keep);
+        break;
+    default:
+        pcg_update_fused_kernel<4, 2><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
+                                                                   part, dst, counter, m, g, keep);
+    }
     return cudaGetLastError();
 }
 

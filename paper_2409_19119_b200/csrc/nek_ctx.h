@@ -90,6 +90,7 @@ struct AxLaunch {
     double *p = nullptr, *x = nullptr;
     const double *r = nullptr, *dinv = nullptr;
     const PcgScalars *sc = nullptr;
+    int keep = 0;                        // L2-resident mode: bit 0 p, r, Dinv, w; bit 1 also x
 };
 cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
                       const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch);
@@ -104,6 +105,7 @@ int ax_gstride_f(int N);
 struct GsClasses {
     int64_t n2 = 0, n4 = 0, n8 = 0, ng = 0;
     const int32_t *p2 = nullptr, *p4 = nullptr, *p8 = nullptr, *pg = nullptr, *og = nullptr;
+    int keep = 0;                        // L2 evict_last on the index lists and values (L2-resident mode)
 };
 template <class T> cudaError_t launch_gs_classes(const GsClasses &C, T *v, const int *done, cudaStream_t s);
 cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst, const int *done, cudaStream_t s);
@@ -130,7 +132,7 @@ cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *ob
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail = nullptr, const GsInline *gi = nullptr);
+                                    const P2PMail *mail = nullptr, const GsInline *gi = nullptr, int keep = 0);
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
 // local gather-scatter and (P2P) the halo unpack in one launch
 struct HaloUnpack {
@@ -227,6 +229,7 @@ struct nek_ctx {
     int32_t *gs_p2 = nullptr, *gs_p4 = nullptr, *gs_p8 = nullptr, *gs_pg = nullptr, *gs_og = nullptr;
     int32_t *gsi_idx = nullptr, *gsi_perm = nullptr, *gsi_offs = nullptr;   // GsInline tables
     bool gs_inline = false;
+    int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
     bool concurrent_bnd = false;
     bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts         // NEK_CONCURRENT_BND=1: boundary Ax + send on s_hi beside the interior
     nekb200::GsClasses gsc;

@@ -1,0 +1,143 @@
+// probes.cu -- measurement probes of SURVEY 8(d) ("Peaks to measure on the box"):
+// FP64 streaming read / write / copy bandwidth of HBM over >= 4 GB and the
+// shared-memory ld.shared.f64 bandwidth.  They give the roofline denominators
+// next to MEASURED_PEAKS.json (torch copy) and the nominal 8 TB/s of BJ; they are
+// not on the solver path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "nek.h"
+
+namespace nekb200 {
+
+constexpr int PROBE_THREADS = 256;
+
+__global__ void __launch_bounds__(PROBE_THREADS) probe_read_kernel(const double2 *__restrict__ a, int64_t n2,
+                                                                   double *out)
+{
+    double s0 = 0.0, s1 = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        const double2 v0 = __ldcs(a + i), v1 = __ldcs(a + i + stride), v2 = __ldcs(a + i + 2 * stride),
+                      v3 = __ldcs(a + i + 3 * stride);
+        s0 += (v0.x + v1.x) + (v2.x + v3.x);
+        s1 += (v0.y + v1.y) + (v2.y + v3.y);
+    }
+    for (; i < n2; i += stride) { const double2 v = __ldcs(a + i); s0 += v.x; s1 += v.y; }
+    if (s0 + s1 == 1.2345e300) out[0] = s0;   // keep the loads alive
+}
+
+__global__ void __launch_bounds__(PROBE_THREADS) probe_copy_kernel(const double2 *__restrict__ a,
+                                                                   double2 *__restrict__ b, int64_t n2)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        const double2 v0 = __ldcs(a + i), v1 = __ldcs(a + i + stride), v2 = __ldcs(a + i + 2 * stride),
+                      v3 = __ldcs(a + i + 3 * stride);
+        __stcs(b + i, v0); __stcs(b + i + stride, v1); __stcs(b + i + 2 * stride, v2); __stcs(b + i + 3 * stride, v3);
+    }
+    for (; i < n2; i += stride) __stcs(b + i, __ldcs(a + i));
+}
+
+__global__ void __launch_bounds__(PROBE_THREADS) probe_write_kernel(double2 *__restrict__ b, int64_t n2, double v)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride)
+        __stcs(b + i, make_double2(v, v));
+}
+
+// every warp reads 32 consecutive doubles (two wavefronts, conflict free) per load
+__global__ void __launch_bounds__(1024) probe_smem_kernel(int iters, double *out)
+{
+    __shared__ double buf[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) buf[i] = i * 1e-3;
+    __syncthreads();
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int it = 0; it < iters; ++it) {
+        const int base = ((w * 8 + it) & 31) * 256 + lane;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s[k] += buf[(base + 32 * k) & 4095];
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += s[k];
+    if (t == 1.2345e300) out[0] = t;
+}
+
+static int sm_count(int device)
+{
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return sms;
+}
+
+}  // namespace nekb200
+
+extern "C" int nek_probe_hbm_gbps(int device, int64_t bytes, double *read_gbps, double *write_gbps,
+                                  double *copy_gbps)
+{
+    using namespace nekb200;
+    if (bytes < (1 << 20)) return NEK_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return NEK_ENODEV;
+    const int64_t n2 = bytes / 2 / 16;   // two buffers of bytes/2 each, double2 elements
+    double2 *a = nullptr, *b = nullptr;
+    double *out = nullptr;
+    if (cudaMalloc((void **)&a, n2 * 16) != cudaSuccess) return NEK_ENOMEM;
+    if (cudaMalloc((void **)&b, n2 * 16) != cudaSuccess) { cudaFree(a); return NEK_ENOMEM; }
+    cudaMalloc((void **)&out, sizeof(double));
+    cudaMemset(a, 0, n2 * 16);
+    const int grid = sm_count(device) * 8;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best[3] = {1e30f, 1e30f, 1e30f};
+    for (int rep = 0; rep < 6; ++rep) {
+        for (int k = 0; k < 3; ++k) {
+            cudaEventRecord(e0);
+            if (k == 0) probe_read_kernel<<<grid, PROBE_THREADS>>>(a, n2, out);
+            else if (k == 1) probe_write_kernel<<<grid, PROBE_THREADS>>>(b, n2, 1.0);
+            else probe_copy_kernel<<<grid, PROBE_THREADS>>>(a, b, n2);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0) best[k] = std::min(best[k], ms);   // rep 0 is the warm-up
+        }
+    }
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    cudaFree(a); cudaFree(b); cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess) return NEK_ECUDA;
+    const double bytes1 = (double)n2 * 16;
+    if (read_gbps) *read_gbps = bytes1 / (best[0] * 1e-3) / 1e9;
+    if (write_gbps) *write_gbps = bytes1 / (best[1] * 1e-3) / 1e9;
+    if (copy_gbps) *copy_gbps = 2 * bytes1 / (best[2] * 1e-3) / 1e9;
+    return NEK_OK;
+}
+
+extern "C" int nek_probe_smem_tbps(int device, double *tbps)
+{
+    using namespace nekb200;
+    if (!tbps) return NEK_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return NEK_ENODEV;
+    double *out = nullptr;
+    if (cudaMalloc((void **)&out, sizeof(double)) != cudaSuccess) return NEK_ENOMEM;
+    const int grid = sm_count(device) * 2, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    probe_smem_kernel<<<grid, 1024>>>(64, out);
+    cudaEventRecord(e0);
+    probe_smem_kernel<<<grid, 1024>>>(iters, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return NEK_ECUDA;
+    *tbps = (double)grid * 1024 * iters * 8 * 8 / (ms * 1e-3) / 1e12;
+    return NEK_OK;
+}

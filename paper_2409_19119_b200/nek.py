@@ -111,6 +111,8 @@ _sig = {
     "nek_makef_lattice": ([_P], _I),
     "nek_makef_free": ([_P], _I),
     "nek_probe_dfma_tflops": ([_I, ctypes.POINTER(_D)], _I),
+    "nek_probe_hbm_gbps": ([_I, _I64, ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_D)], _I),
+    "nek_probe_smem_tbps": ([_I, ctypes.POINTER(_D)], _I),
     "nek_plan_create": ([ctypes.POINTER(_P), _I64, _I, _P, _P, _P], _I),
     "nek_plan_surface_gids": ([_P, _P], _I64),
     "nek_plan_set_ranks": ([_P, _I, _I, _P, _P], _I),
@@ -424,6 +426,20 @@ def probe_fp64_tflops(device=0) -> float:
     """nek_probe_dfma_tflops: measured FP64 FMA throughput (TFLOP/s)."""
     v = ctypes.c_double(0.0)
     _check(_lib.nek_probe_dfma_tflops(int(device), ctypes.byref(v)))
+    return v.value
+
+
+def probe_hbm_gbps(device=0, nbytes=4 << 30) -> dict:
+    """nek_probe_hbm_gbps: FP64 (double2) streaming read / write / copy bandwidth over `nbytes`."""
+    r, w, c = ctypes.c_double(0.0), ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(_lib.nek_probe_hbm_gbps(int(device), int(nbytes), ctypes.byref(r), ctypes.byref(w), ctypes.byref(c)))
+    return {"read": r.value, "write": w.value, "copy": c.value}
+
+
+def probe_smem_tbps(device=0) -> float:
+    """nek_probe_smem_tbps: aggregate ld.shared.f64 bandwidth (TB/s)."""
+    v = ctypes.c_double(0.0)
+    _check(_lib.nek_probe_smem_tbps(int(device), ctypes.byref(v)))
     return v.value
 
 
