@@ -523,7 +523,9 @@ def main():
                        "pcg_iters_per_step": args.iters, "h1": 1.0, "h2": args.h2,
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
                        "parallelism": f"dp{world} (element z-slabs, NCCL halo + allgather reductions)",
-                       "timing": "CUDA graph of 10 PCG iterations per replay, device time by CUDA events"},
+                       "timing": "CUDA graph of 10 PCG iterations per replay, device time by CUDA events",
+                       "l2_resident": {"keep": info["l2_keep"], "setaside_bytes": info["l2_setaside"],
+                                       "setaside_max": info["l2_setaside_max"]}},
             "pcg_iter_per_s": args.iters * args.steps / (t_ms * 1e-3),
             "ax_gs": {"gdof_per_s": ax_gdofs, "ms_per_apply": ax_ms / reps,
                       "algorithmic_GBps": (ax_bytes_per_elem * mesh.E * world / P3 * P3 + 0) * reps / (ax_ms * 1e-3) / 1e9},

@@ -286,7 +286,9 @@ typedef struct {
     int64_t device_bytes;      /* device memory held by the context                */
     double  geom_min_jac;      /* min J over local nodes                           */
     int32_t transport;         /* 0 = single GPU, 1 = NCCL, 2 = NVLink peer memory (CUDA IPC) */
-    int32_t pad_;
+    int32_t l2_keep;           /* L2-resident PCG vectors: bit 0 p, r, Dinv, w, gs lists; bit 1 x  */
+    int64_t l2_setaside;       /* persisting-L2 bytes in effect (device-wide limit)               */
+    int64_t l2_setaside_max;   /* cudaDevAttrMaxPersistingL2CacheSize                            */
 } nek_info_t;
 
 int nek_get_info(const nek_ctx *ctx, nek_info_t *info);

@@ -361,6 +361,22 @@ static int exchange_slots(nek_ctx *ctx, int channel)
     return NEK_OK;
 }
 
+// Single-GPU nek_ax / nek_gs run straight on the caller's stream (no event hand-off to s_main
+// and back, which costs a few microseconds per call); restored on scope exit.
+struct OnCallerStream {
+    nek_ctx *ctx;
+    cudaStream_t saved;
+    bool on;
+    OnCallerStream(nek_ctx *c, void *stream) : ctx(c), saved(c->s_main), on(c->nranks == 1 && !c->timing)
+    {
+        if (on) ctx->s_main = (cudaStream_t)stream;
+    }
+    ~OnCallerStream()
+    {
+        if (on) ctx->s_main = saved;
+    }
+};
+
 static void enter(nek_ctx *ctx, void *stream)
 {
     cudaEventRecord(ctx->ev_in, (cudaStream_t)stream);
@@ -710,8 +726,23 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         if (kenv) keep = atoi(kenv);
         ctx->l2keep = keep;
         ctx->gsc.keep = keep & 1;
-        const char *senv = getenv("NEK_L2SETASIDE");
-        if (senv) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(senv) << 20);
+        // evict_last lines live in the persisting L2 set-aside: size it for the kept vectors (device-wide
+        // limit, only ever raised; clamped to cudaDevAttrMaxPersistingL2CacheSize); NEK_L2SETASIDE = MiB
+        if (keep) {
+            int maxp = 0;
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+            double want = ((keep & 2) ? 5 : 4) * vec + idx;
+            const char *senv = getenv("NEK_L2SETASIDE");
+            if (senv) want = (double)atoll(senv) * (1 << 20);
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t req = (size_t)std::min<double>(want, (double)maxp);
+            if (req > cur && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, req) != cudaSuccess)
+                cudaGetLastError();
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            ctx->l2_setaside = (int64_t)cur;
+            ctx->l2_setaside_max = maxp;
+        }
     }
     CK(dalloc(ctx, &ctx->part, ctx->npart));
     CK(dalloc(ctx, &ctx->red_loc, RED_N));
@@ -799,7 +830,8 @@ int nek_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, void 
     CK(cudaSetDevice(ctx->device));
     const bool du = is_device_ptr(u), dw = is_device_ptr(w);
     int st;
-    enter(ctx, stream);
+    OnCallerStream on_caller(ctx, stream);
+    if (!on_caller.on) enter(ctx, stream);
     const double *ud = u;
     double *wd = w;
     if (!du || !dw) { if ((st = ensure_stage(ctx)) != NEK_OK) return st; }
@@ -810,7 +842,7 @@ int nek_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, void 
         CK(cudaMemcpyAsync(w, wd, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
         CK(cudaStreamSynchronize(ctx->s_main));
     }
-    leave(ctx, stream);
+    if (!on_caller.on) leave(ctx, stream);
     return NEK_OK;
 }
 
@@ -821,7 +853,8 @@ int nek_gs(nek_ctx *ctx, double *v, void *stream)
     CK(cudaSetDevice(ctx->device));
     const bool dv = is_device_ptr(v);
     int st;
-    enter(ctx, stream);
+    OnCallerStream on_caller(ctx, stream);
+    if (!on_caller.on) enter(ctx, stream);
     double *vd = v;
     if (!dv) {
         if ((st = ensure_stage(ctx)) != NEK_OK) return st;
@@ -833,7 +866,7 @@ int nek_gs(nek_ctx *ctx, double *v, void *stream)
         CK(cudaMemcpyAsync(v, vd, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
         CK(cudaStreamSynchronize(ctx->s_main));
     }
-    leave(ctx, stream);
+    if (!on_caller.on) leave(ctx, stream);
     return NEK_OK;
 }
 
@@ -1033,6 +1066,7 @@ int nek_get_info(const nek_ctx *ctx, nek_info_t *info)
     info->n_neighbors = (int64_t)ctx->neighbors.size(); info->halo_doubles = ctx->nslots;
     info->n_boundary_elems = ctx->n_boundary; info->device_bytes = ctx->device_bytes; info->geom_min_jac = ctx->min_jac;
     info->transport = ctx->nranks == 1 ? 0 : (ctx->p2p ? 2 : 1);
+    info->l2_keep = ctx->l2keep; info->l2_setaside = ctx->l2_setaside; info->l2_setaside_max = ctx->l2_setaside_max;
     return NEK_OK;
 }
 

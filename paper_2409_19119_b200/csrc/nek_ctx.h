@@ -230,6 +230,7 @@ struct nek_ctx {
     int32_t *gsi_idx = nullptr, *gsi_perm = nullptr, *gsi_offs = nullptr;   // GsInline tables
     bool gs_inline = false;
     int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
+    int64_t l2_setaside = 0, l2_setaside_max = 0;   // persisting L2 bytes granted / allowed
     bool concurrent_bnd = false;
     bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts         // NEK_CONCURRENT_BND=1: boundary Ax + send on s_hi beside the interior
     nekb200::GsClasses gsc;

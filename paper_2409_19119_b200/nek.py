@@ -51,7 +51,8 @@ class nek_info_t(ctypes.Structure):
                 ("n_runs", ctypes.c_int64), ("n_perm", ctypes.c_int64), ("n_ifc_runs", ctypes.c_int64),
                 ("n_ifc_perm", ctypes.c_int64), ("n_neighbors", ctypes.c_int64), ("halo_doubles", ctypes.c_int64),
                 ("n_boundary_elems", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
-                ("geom_min_jac", ctypes.c_double), ("transport", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+                ("geom_min_jac", ctypes.c_double), ("transport", ctypes.c_int32), ("l2_keep", ctypes.c_int32),
+                ("l2_setaside", ctypes.c_int64), ("l2_setaside_max", ctypes.c_int64)]
 
 
 class nek_stats_t(ctypes.Structure):
