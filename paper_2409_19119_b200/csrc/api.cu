@@ -1037,6 +1037,16 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
         CK(launch_pcg_xfinal(ctx->n, ctx->sc, ctx->vp, ctx->vx, ctx->s_main));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
+    if (ctx->l2keep) {      // release the L2-resident vectors (evict_last -> evict_normal)
+        L2Ranges R;
+        const int64_t vb = 8 * ctx->n;
+        R.add(ctx->vp, vb); R.add(ctx->vr, vb); R.add(ctx->vw, vb); R.add(ctx->vdinv, vb);
+        if (ctx->l2keep & 2) R.add(ctx->vx, vb);
+        R.add(ctx->gsc.p2, 8 * ctx->gsc.n2); R.add(ctx->gsc.p4, 16 * ctx->gsc.n4);
+        R.add(ctx->obits, 4 * ((ctx->n + 31) / 32));
+        CK(launch_l2_demote(R, ctx->s_main));
+        ctx->stats.launches += 1;
+    }
     CK(cudaMemcpyAsync(H, ctx->sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, ctx->s_main));
     if (dx) CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->s_main));
     else CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));

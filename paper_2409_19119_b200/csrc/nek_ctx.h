@@ -134,6 +134,17 @@ cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const doub
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
                                     const P2PMail *mail = nullptr, const GsInline *gi = nullptr, int keep = 0);
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
+// device ranges whose L2 lines are demoted from evict_last after an L2-resident solve
+struct L2Ranges {
+    const void *ptr[10] = {};
+    int64_t bytes[10] = {};
+    int count = 0;
+    void add(const void *p, int64_t b)
+    {
+        if (p && b > 0 && count < 10) { ptr[count] = p; bytes[count] = b; ++count; }
+    }
+};
+cudaError_t launch_l2_demote(const L2Ranges &R, cudaStream_t s);
 // local gather-scatter and (P2P) the halo unpack in one launch
 struct HaloUnpack {
     int64_t nifc = 0;
