@@ -279,6 +279,8 @@ static int gs_full(nek_ctx *ctx, T *v, const int *done)
 // w = M QQ^T (h1 K_L + h2 B_L) M u.  With dot: this rank's <M u, A_L M u> into
 // red_loc[RED_SIGMA] (then allgathered across ranks into red_all).  fused: the
 // PCG direction / deferred x update is applied in the Ax prologue (u == vp).
+static bool use_fold(const nek_ctx *ctx) { return ctx->fold && ctx->p2p && ax_has_fold(ctx->variant, ctx->N); }
+
 static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, bool dot, const int *done,
                     bool fused = false, bool skip_local_gs = false)
 {
@@ -302,6 +304,8 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     const int64_t g1 = ax_grid(ctx->variant, ctx->N, nb), g2 = ax_grid(ctx->variant, ctx->N, ni);
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
     L.elist = ctx->elist;
+    const bool fold = push && use_fold(ctx);      // (rho', rr) pulled and booked by the Ax itself
+    if (fold) { L.fold = 1 | (nb > 0 ? 2 : 0); L.hist = ctx->hist; }
     if (ax_has_fused(ctx->variant, ctx->N) && ctx->p2p && !ctx->concurrent_bnd) {
         // Boundary elements, then the halo send, then the interior elements, in stream order: the
         // NVLink transfer overlaps the interior work and the send never waits for SM
@@ -312,6 +316,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
         L.nelem = ni; L.eoff = nb; L.part_off = g1;
+        if (fold) L.fold = 1 | (nb > 0 ? 0 : 2);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
     } else if (ax_has_fused(ctx->variant, ctx->N)) {
         // Boundary elements and the halo send on the high-priority stream, interior elements on
@@ -325,6 +330,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         if ((st = halo_start(ctx, w, done, ctx->s_hi)) != NEK_OK) return st;
         CK(cudaEventRecord(ctx->ev_bnd, ctx->s_hi));
         L.nelem = ni; L.eoff = nb; L.part_off = g1;
+        if (fold) L.fold = 1 | (nb > 0 ? 0 : 2);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_bnd, 0));
     } else {
@@ -360,6 +366,28 @@ static int exchange_slots(nek_ctx *ctx, int channel)
     NK(ncclAllGather(ctx->red_loc, ctx->red_all, RED_N, ncclDouble, ctx->nccl, ctx->s_main));
     return NEK_OK;
 }
+
+// The persisting-L2 carve-out of an L2-resident solve, raised on entry and restored when the solve
+// returns (after its final stream synchronisation).
+struct L2SetAside {
+    size_t prev = 0;
+    bool on = false;
+    explicit L2SetAside(nek_ctx *ctx)
+    {
+        if (!ctx->l2keep || ctx->l2_setaside <= 0) return;
+        if (cudaDeviceGetLimit(&prev, cudaLimitPersistingL2CacheSize) != cudaSuccess) { cudaGetLastError(); return; }
+        if ((size_t)ctx->l2_setaside <= prev) return;
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)ctx->l2_setaside) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        on = true;
+    }
+    ~L2SetAside()
+    {
+        if (on && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev) != cudaSuccess) cudaGetLastError();
+    }
+};
 
 // Single-GPU nek_ax / nek_gs run straight on the caller's stream (no event hand-off to s_main
 // and back, which costs a few microseconds per call); restored on scope exit.
@@ -683,6 +711,8 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         if (!env || std::strcmp(env, "0") != 0) {
             st = setup_p2p(ctx);
             if (st != NEK_OK) return st;
+            const char *fenv = getenv("NEK_FOLD");
+            ctx->fold = ctx->p2p && !(fenv && std::strcmp(fenv, "0") == 0);
         }
     }
 
@@ -726,21 +756,17 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         if (kenv) keep = atoi(kenv);
         ctx->l2keep = keep;
         ctx->gsc.keep = keep & 1;
-        // evict_last lines live in the persisting L2 set-aside: size it for the kept vectors (device-wide
-        // limit, only ever raised; clamped to cudaDevAttrMaxPersistingL2CacheSize); NEK_L2SETASIDE = MiB
+        // evict_last lines live in the persisting L2 set-aside: sized for the kept vectors (clamped to
+        // cudaDevAttrMaxPersistingL2CacheSize; NEK_L2SETASIDE = MiB) and granted only for the duration
+        // of a solve -- the carve-out halves the write bandwidth of everything else (measured: 3.0 vs
+        // 5.9 TB/s for a streaming write, nek_ax and the pMG V-cycle 11-15% slower)
         if (keep) {
             int maxp = 0;
             cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
             double want = ((keep & 2) ? 5 : 4) * vec + idx;
             const char *senv = getenv("NEK_L2SETASIDE");
             if (senv) want = (double)atoll(senv) * (1 << 20);
-            size_t cur = 0;
-            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-            const size_t req = (size_t)std::min<double>(want, (double)maxp);
-            if (req > cur && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, req) != cudaSuccess)
-                cudaGetLastError();
-            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-            ctx->l2_setaside = (int64_t)cur;
+            ctx->l2_setaside = (int64_t)std::min<double>(want, (double)maxp);
             ctx->l2_setaside_max = maxp;
         }
     }
@@ -890,9 +916,12 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, &m, gip, ctx->l2keep));
-            CK(launch_pcg_fin_p2p(ctx->sc, m, ctx->hist, ctx->s_main));
-            ctx->stats.launches += 2; ctx->stats.vec_launches += 2;
+                                       ctx->counter + 2, ctx->s_main, &m, gip, ctx->l2keep, use_fold(ctx) ? 1 : 0));
+            ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
+            if (!use_fold(ctx)) {   // folded: the next Ax pulls (rho', rr) and does this bookkeeping
+                CK(launch_pcg_fin_p2p(ctx->sc, m, ctx->hist, ctx->s_main));
+                ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
+            }
         }
         return NEK_OK;
     }
@@ -958,6 +987,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
         CK(cudaMemcpyAsync(ctx->stage_in, b, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->s_main));
         bd = ctx->stage_in;
     }
+    L2SetAside l2scope(ctx);
     PcgScalars *H = ctx->sc_host;
     std::memset(H, 0, sizeof(*H));
     H->tol = tol; H->maxit = maxit;
@@ -1032,6 +1062,10 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
             CK(cudaStreamSynchronize(ctx->s_main));
             if (H->done) break;
         }
+    }
+    if (use_fused(ctx) && use_fold(ctx)) {   // bookkeeping of the last update (no Ax followed it)
+        CK(launch_pcg_fold_finish(ctx->sc, mail_of(ctx), ctx->hist, ctx->s_main));
+        ctx->stats.launches += 1;
     }
     if (use_fused(ctx)) {   // the deferred x += alpha p of the last iteration
         CK(launch_pcg_xfinal(ctx->n, ctx->sc, ctx->vp, ctx->vx, ctx->s_main));

@@ -1071,8 +1071,8 @@ __global__ void __launch_bounds__(128, MINB)
                  double h1, double h2, double *__restrict__ w, double *__restrict__ part, int64_t part_off,
                  int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done,
                  double *pvec, double *__restrict__ xvec, const double *__restrict__ rvec,
-                 const double *__restrict__ dvec, const PcgScalars *sc, P2PMail mail, unsigned int ctas_total,
-                 int keep)
+                 const double *__restrict__ dvec, PcgScalars *sc, P2PMail mail, unsigned int ctas_total,
+                 int keep, int fold, double *hist)
 {
     constexpr int P3 = 512, N = 7;
     pdl_trigger();
@@ -1123,7 +1123,41 @@ __global__ void __launch_bounds__(128, MINB)
         }
         return;
     }
-    if (FUSED) { beta = sc->beta; alpha = sc->alpha; }
+    if (FUSED) {
+        beta = sc->beta; alpha = sc->alpha;
+        if ((fold & 1) && *(volatile const int *)&sc->fold_ready) {
+            // folded bookkeeping: (rho', rr) of the last update from every rank (mailbox channel 1),
+            // beta = rho' / rho, convergence / maxit; one CTA records it (no separate fin kernel)
+            __shared__ double s_m[3];
+            __shared__ int s_stop;
+            if (t == 0) {
+                mail_pull(mail, 1, s_m);
+                const double rho1 = s_m[0], rr = s_m[1], rho = sc->rho, bb = sc->bb;
+                const int it = sc->iter;
+                const bool conv = sqrt(rr) <= sc->tol * bb, stop = conv || it >= sc->maxit;
+                if ((fold & 2) && blockIdx.x == 0) {
+                    sc->rr = rr;
+                    if (hist) hist[it] = sqrt(rr) / bb;
+                    sc->beta = rho1 / rho;
+                    sc->rho_next = rho1;
+                    if (conv) { sc->status = NEK_OK; sc->done = 1; }
+                    else if (stop) { sc->status = NEK_MAXIT; sc->done = 1; }
+                    __threadfence();
+                }
+                s_m[2] = rho1 / rho;
+                s_stop = stop;
+            }
+            __syncthreads();
+            if (s_stop) {
+                if (TMAG) {
+                    if (nit > 0) tma::mbar_wait(&gfull[0], 0);
+                    if (nit > 1) tma::mbar_wait(&gfull[1], 0);
+                }
+                return;
+            }
+            beta = s_m[2];
+        }
+    }
     const int kb = 2 * wq;                       // this warp's first k-slab
     double dot = 0.0;
     int64_t e_next = nit > 0 ? elem_at(0) : 0;
@@ -1330,13 +1364,14 @@ static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double
     if (L.fused)
         return launch_k(pdl_enabled(), ax_v5_kernel<HELM, true, MINB, L2PF, TMAG>, (unsigned)grid, 128, dsm, s, L.nelem,
                         L.eoff, L.elist, (const double *)L.p, G, wJ, mbits, h1, h2, w, L.part, L.part_off, L.fin_total,
-                        L.dst, L.counter, L.done, L.p, L.x, L.r, L.dinv, L.sc, L.mail,
-                        L.ctas_total ? L.ctas_total : (unsigned)grid, L.keep);
+                        L.dst, L.counter, L.done, L.p, L.x, L.r, L.dinv, const_cast<PcgScalars *>(L.sc), L.mail,
+                        L.ctas_total ? L.ctas_total : (unsigned)grid, L.keep, L.fold, L.hist);
     else
         ax_v5_kernel<HELM, false, MINB, L2PF, TMAG><<<(unsigned)grid, 128, dsm, s>>>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w,
                                                                   L.part, L.part_off, L.fin_total, L.dst, L.counter,
                                                                   L.done, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                                                  L.mail, L.ctas_total ? L.ctas_total : (unsigned)grid, L.keep);
+                                                                  L.mail, L.ctas_total ? L.ctas_total : (unsigned)grid, L.keep,
+                                                                  0, nullptr);
     return cudaGetLastError();
 }
 
@@ -1361,6 +1396,12 @@ static int v6_epb(int N)
 #undef NEK_CASE
     }
     return 1;
+}
+
+// the folded P2P bookkeeping (AxLaunch::fold) is implemented by the N = 7 kernel v5
+bool ax_has_fold(int variant, int N)
+{
+    return N == 7 && (variant == 0 || variant == 8 || variant == 9 || variant == 10);
 }
 
 bool ax_has_fused(int variant, int N)
@@ -1973,6 +2014,8 @@ __global__ void pcg_init_fin_kernel(PcgScalars *sc, const double *red_all, int n
     sc->done = 0;
     sc->alpha = 0.0;
     sc->beta = 0.0;
+    sc->rho_next = rho;
+    sc->fold_ready = 0;
     if (hist) hist[0] = rr > 0.0 ? 1.0 : 0.0;
     if (!(rr > 0.0)) { sc->done = 1; sc->status = NEK_OK; }              // b = 0 -> x = 0, 0 iterations
     else if (sc->tol >= 1.0) { sc->done = 1; sc->status = NEK_OK; }      // ||r0|| <= tol ||b||
@@ -2159,7 +2202,7 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     pcg_update_fused_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                             const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ red_all,
                             int nranks, PcgScalars *sc, double *hist, double *__restrict__ part, double *dst,
-                            unsigned int *counter, P2PMail mail, GsInline gi, int keep)
+                            unsigned int *counter, P2PMail mail, GsInline gi, int keep, int fold)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ int s_last;
@@ -2180,7 +2223,7 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
         if (blockIdx.x == 0 && threadIdx.x == 0) { sc->status = NEK_ENOTSPD; sc->alpha = 0.0; sc->done = 1; }
         return;
     }
-    const double alpha = sc->rho / sigma;
+    const double alpha = (fold ? sc->rho_next : sc->rho) / sigma;
     const uint64_t pol = tma::policy_keep(keep & 1);
     double a0 = 0.0, a1 = 0.0;
     const int64_t n2 = n >> 1;
@@ -2247,7 +2290,16 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
         if (threadIdx.x == 0) {
             *counter = 0u;
             if (nranks == 1) pcg_bookkeep(sc, b0, b1, alpha, hist);
-            else if (mail.nranks > 1) mail_push(mail, 1, b0, b1, 0.0);   // to every rank (channel 1)
+            else if (mail.nranks > 1) {
+                if (fold) {                      // the next Ax pulls (rho', rr) and does the bookkeeping
+                    sc->alpha = alpha;
+                    sc->iter += 1;
+                    sc->rho = sc->rho_next;
+                    sc->fold_ready = 1;
+                    __threadfence();
+                }
+                mail_push(mail, 1, b0, b1, 0.0);   // to every rank (channel 1)
+            }
             else { dst[0] = b0; dst[1] = b1; }
         }
     }
@@ -2383,13 +2435,13 @@ static bool upd_tma()
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail, const GsInline *gi, int keep)
+                                    const P2PMail *mail, const GsInline *gi, int keep, int fold)
 {
     P2PMail m;
     if (mail) m = *mail;
     GsInline g;
     if (gi) g = *gi;
-    if (!g.idx && upd_tma()) {
+    if (!g.idx && upd_tma() && !fold) {
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(pcg_update_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UPT_SMEM);
@@ -2402,15 +2454,15 @@ cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const doub
     switch (nblk / 148) {
     case 8:
         return launch_k(pdl_enabled(), pcg_update_fused_kernel<2, 8>, nblk, VEC_THREADS, 0, s, n, obits, dinv, w, r,
-                        red_all, nranks, sc, hist, part, dst, counter, m, g, keep);
+                        red_all, nranks, sc, hist, part, dst, counter, m, g, keep, fold);
         break;
     case 4:
         return launch_k(pdl_enabled(), pcg_update_fused_kernel<4, 4>, nblk, VEC_THREADS, 0, s, n, obits, dinv, w, r,
-                        red_all, nranks, sc, hist, part, dst, counter, m, g, keep);
+                        red_all, nranks, sc, hist, part, dst, counter, m, g, keep, fold);
         break;
     default:
         return launch_k(pdl_enabled(), pcg_update_fused_kernel<4, 2>, nblk, VEC_THREADS, 0, s, n, obits, dinv, w, r,
-                        red_all, nranks, sc, hist, part, dst, counter, m, g, keep);
+                        red_all, nranks, sc, hist, part, dst, counter, m, g, keep, fold);
     }
     return cudaGetLastError();
 }
@@ -2422,6 +2474,28 @@ __global__ void pcg_fin_p2p_kernel(PcgScalars *sc, P2PMail mail, double *hist)
     double v[3];
     mail_pull(mail, 1, v);
     pcg_bookkeep(sc, v[0], v[1], sc->rho / sc->sigma, hist);
+}
+
+// folded path, after the last update of a solve: the bookkeeping its (rho', rr) would get from the next Ax
+__global__ void pcg_fold_finish_kernel(PcgScalars *sc, P2PMail mail, double *hist)
+{
+    if (sc->done || !sc->fold_ready) return;
+    double v[3];
+    mail_pull(mail, 1, v);
+    const double rr = v[1], bb = sc->bb;
+    const int it = sc->iter;
+    sc->rr = rr;
+    if (hist) hist[it] = sqrt(rr) / bb;
+    sc->beta = v[0] / sc->rho;
+    sc->rho_next = v[0];
+    if (sqrt(rr) <= sc->tol * bb) { sc->status = NEK_OK; sc->done = 1; }
+    else if (it >= sc->maxit) { sc->status = NEK_MAXIT; sc->done = 1; }
+}
+
+cudaError_t launch_pcg_fold_finish(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s)
+{
+    pcg_fold_finish_kernel<<<1, 1, 0, s>>>(sc, mail, hist);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s)

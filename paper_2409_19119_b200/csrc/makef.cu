@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "ax_tma.cuh"
 #include "nek_ctx.h"
 
 namespace nekb200 {
@@ -30,6 +31,9 @@ __constant__ double c_Jq[MK_MAXN + 1][16 * 10];   // [N][I * (N+1) + i] = h_i(xi
 __constant__ double c_Dq[MK_MAXN + 1][16 * 10];   // derivative of the interpolant at the GL points
 __constant__ double c_wq[MK_MAXN + 1][16];        // GL weights
 
+#ifndef MK_PF_G
+#define MK_PF_G 1   // bulk L2 prefetch of the next element's lattice factors
+#endif
 constexpr int mk_m(int NQ) { return (3 * NQ + 1) / 2; }   // ceil(3 (N+1) / 2)
 constexpr int odd(int n) { return n | 1; }
 
@@ -68,6 +72,9 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
     double *F = BA + SZ_AA;                // [M3]
     const int t = threadIdx.x, nt = blockDim.x;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        // the next element's lattice factors into L2 while this one computes (read in the Ut stage)
+        if (MK_PF_G && t == 0 && e + gridDim.x < E && (9 * M3 * 8) % 16 == 0)
+            tma::prefetch_l2(G9 + (e + gridDim.x) * 9 * (int64_t)M3, 9 * M3 * 8);
         // ---- velocity into shared memory (padded i stride)
         for (int q = t; q < 3 * P3; q += nt) {
             const int c = q / P3, p = q - c * P3, i = p % NQ, kj = p / NQ;
@@ -281,6 +288,8 @@ __global__ void __launch_bounds__(NT, 1)
     double *F = UT + 3 * M3;               // [3][M3]
     const int t = threadIdx.x;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        if (MK_PF_G && t == 0 && e + gridDim.x < E && (9 * M3 * 8) % 16 == 0)
+            tma::prefetch_l2(G9 + (e + gridDim.x) * 9 * (int64_t)M3, 9 * M3 * 8);
         for (int q = t; q < 3 * P3; q += NT) {
             const int c = q / P3, p = q - c * P3;
             const double *src = c == 0 ? u0 : c == 1 ? u1 : u2;

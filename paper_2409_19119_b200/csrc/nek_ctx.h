@@ -25,6 +25,9 @@ struct PcgScalars {
     double sigma;      // global <p, A p> of the current iteration (P2P path)
     double alpha;      // alpha of the last update whose x += alpha p is still pending (fused path)
     double beta;       // beta for the next direction update (fused path)
+    double rho_next;   // folded P2P path: rho of the current iteration (set by the Ax bookkeeping CTA)
+    int fold_ready;    // folded P2P path: 1 once an update has pushed (rho', rr) for the next Ax to pull
+    int pad_;
 };
 
 // NVLink peer mailbox of a rank: [channel][epoch parity][rank][4] doubles, slot 3 = epoch.
@@ -91,10 +94,15 @@ struct AxLaunch {
     const double *r = nullptr, *dinv = nullptr;
     const PcgScalars *sc = nullptr;
     int keep = 0;                        // L2-resident mode: bit 0 p, r, Dinv, w; bit 1 also x
+    // folded P2P bookkeeping (fused Ax v5 only): bit 0 = pull (rho', rr) of the last update from the
+    // mailbox at entry and take beta from it; bit 1 = this launch's CTA 0 also does the bookkeeping
+    int fold = 0;
+    double *hist = nullptr;
 };
 cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
                       const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch);
 int64_t ax_grid(int variant, int N, int64_t nelem);      // partial slots one launch writes
+bool ax_has_fold(int variant, int N);
 int ax_partials_needed(int variant, int N, int64_t E);
 // FP32 operator (v6, N <= 9): Gf is [E][ax_gstride_f(N)] (6 planes, padded to 16 bytes per element)
 cudaError_t launch_ax_f(int N, int64_t E, const float *u, const float *Gf, const float *wJf, const uint32_t *mbits,
@@ -132,7 +140,10 @@ cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *ob
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail = nullptr, const GsInline *gi = nullptr, int keep = 0);
+                                    const P2PMail *mail = nullptr, const GsInline *gi = nullptr, int keep = 0,
+                                    int fold = 0);
+// folded P2P path: the bookkeeping of the last pushed (rho', rr) when no Ax followed it
+cudaError_t launch_pcg_fold_finish(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
 // device ranges whose L2 lines are demoted from evict_last after an L2-resident solve
 struct L2Ranges {
@@ -241,6 +252,7 @@ struct nek_ctx {
     int32_t *gsi_idx = nullptr, *gsi_perm = nullptr, *gsi_offs = nullptr;   // GsInline tables
     bool gs_inline = false;
     int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
+    bool fold = false;                              // P2P: bookkeeping folded into the next Ax (no fin kernel)
     int64_t l2_setaside = 0, l2_setaside_max = 0;   // persisting L2 bytes granted / allowed
     bool concurrent_bnd = false;
     bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts         // NEK_CONCURRENT_BND=1: boundary Ax + send on s_hi beside the interior
