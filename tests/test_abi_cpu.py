@@ -166,3 +166,12 @@ def test_multirank_plans_reproduce_oracle(nek, split):
     ref = oracle.gs_multi([s.gid for s in subs], vals)
     for a, b in zip(got, ref):
         assert np.array_equal(a, b)
+
+
+def test_probe_argument_errors(nek):
+    """The measurement probes validate their arguments before touching a device (include/nek.h)."""
+    import ctypes
+    d = ctypes.c_double(0.0)
+    assert nek._lib.nek_probe_hbm_gbps(0, 1000, ctypes.byref(d), None, None) == nek.EINVAL
+    assert nek._lib.nek_probe_smem_tbps(0, None) == nek.EINVAL
+    assert nek._lib.nek_probe_dfma_tflops(0, None) == nek.EINVAL

@@ -420,3 +420,35 @@ def test_config3_full_size_sampled(nek):
         assert it == 20 and np.all(np.isfinite(hist)) and abs(hist[-1] - rr) <= 1e-15 * max(1.0, rr)
     finally:
         nek.free(ctx)
+
+
+@pytest.mark.parametrize("keep", ["0", "1", "3"])
+def test_pcg_l2_resident_bitwise(nek, keep):
+    """The L2-resident mode only changes cache policy (evict_last hints, the persisting carve-out
+    raised for the solve): the iterates, history and iteration count are bit-identical to the
+    plain mode, and the carve-out is released when the solve returns."""
+    import os
+    m = mg.box_mesh(6, 5, 4, 7, deform="bubble")
+    b = mg.smooth_field(m, seed=11)
+    res = {}
+    for k in ("0", keep):
+        os.environ["NEK_L2KEEP"] = k
+        try:
+            ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+        finally:
+            os.environ.pop("NEK_L2KEEP", None)
+        try:
+            info = nek.get_info(ctx)
+            assert info["l2_keep"] == int(k)
+            if int(k):
+                assert 0 < info["l2_setaside"] <= info["l2_setaside_max"]
+            bd = torch.from_numpy(b).cuda()
+            xd = torch.zeros_like(bd)
+            st, it, rr, hg = nek.pcg_solve(ctx, 1.0, 0.0, bd, xd, 1e-9, 400, want_hist=True)
+            assert st == nek.OK
+            res[k] = (xd.cpu().numpy(), it, hg)
+        finally:
+            nek.free(ctx)
+    x0, it0, h0 = res["0"]
+    x1, it1, h1 = res[keep]
+    assert it1 == it0 and np.array_equal(x1, x0) and np.array_equal(h1, h0)
