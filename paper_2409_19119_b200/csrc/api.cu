@@ -711,8 +711,11 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         if (!env || std::strcmp(env, "0") != 0) {
             st = setup_p2p(ctx);
             if (st != NEK_OK) return st;
+            // folded bookkeeping: +2% at 2 GPUs (config 2 per GPU) and parity-clean in tools/mgpu_check.py,
+            // but a sequence of projection solves (bench --gpus 2, NEXT #2 section) times out in a peer
+            // exchange with it, cause not yet found -- opt-in only (NEK_FOLD=1)
             const char *fenv = getenv("NEK_FOLD");
-            ctx->fold = ctx->p2p && !(fenv && std::strcmp(fenv, "0") == 0);
+            ctx->fold = ctx->p2p && fenv && std::strcmp(fenv, "1") == 0;
         }
     }
 
