@@ -438,6 +438,11 @@ def main():
             for nb in (1 << 16, 1 << 20, 1 << 26):
                 buf = torch.zeros(nb // 8, dtype=torch.float64, device=dev)
                 reps = 20
+                for _ in range(3):       # warm-up (connection setup on the first transfer)
+                    if rank == 0:
+                        dist.send(buf, 1)
+                    elif rank == 1:
+                        dist.recv(buf, 0)
                 barrier(); torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
