@@ -8,9 +8,12 @@ Tolerances (DESIGN.md "Parity bar"):
     residual history |d(||r_k||/||b||)| <= max(1e-12 max(1, h_k), 10 x the
     oracle's own summation-order noise) on fixed windows (reading 17).
 """
+import os
+
 import numpy as np
 import pytest
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
@@ -452,3 +455,50 @@ def test_pcg_l2_resident_bitwise(nek, keep):
     x0, it0, h0 = res["0"]
     x1, it1, h1 = res[keep]
     assert it1 == it0 and np.array_equal(x1, x0) and np.array_equal(h1, h0)
+
+
+@pytest.mark.parametrize("env", [{"NEK_PDL": "1"}, {"NEK_GS_PPT": "1"}, {"NEK_GS_PPT": "2"}, {"NEK_UPD_TMA": "1"},
+                                 {"NEK_UPD_CFG": "8"}])
+def test_pcg_measured_alternatives(env):
+    """The kept-but-not-default launch configurations ('measured and rejected'):
+    programmatic dependent launch and gs pairs-per-thread change no arithmetic (bit-identical to the
+    default); the TMA-staged and the 8-CTA/SM residual updates sum the dot products in a different
+    (still fixed) order, so they agree with the oracle-checked default to rounding.  The switches are
+    read once per process, hence a subprocess per setting.  N = 6 with an odd element count makes
+    n_local odd (the scalar tail of the vector kernels)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2409_19119_b200 import nek
+from workloads import meshgen as mg
+out = {}
+for (ex, ey, ez, N) in ((6, 5, 4, 7), (3, 3, 3, 6)):
+    m = mg.box_mesh(ex, ey, ez, N, deform="bubble")
+    b = torch.from_numpy(mg.smooth_field(m, seed=5)).cuda()
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    x = torch.zeros_like(b)
+    st, it, rr, h = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 1e-9, 600, want_hist=True)
+    out[str(N)] = {"it": it, "x": x.cpu().numpy().tolist(), "h": list(map(float, h))}
+    nek.free(ctx)
+print(json.dumps(out))
+''' % ROOT
+    def run(extra):
+        e = dict(os.environ)
+        e.update(extra)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    base, alt = run({}), run(env)
+    exact = "NEK_UPD_TMA" not in env and "NEK_UPD_CFG" not in env
+    for N in base:
+        xb, xa = np.array(base[N]["x"]), np.array(alt[N]["x"])
+        if exact:
+            assert alt[N]["it"] == base[N]["it"] and np.array_equal(xa, xb) and alt[N]["h"] == base[N]["h"]
+        else:
+            assert abs(alt[N]["it"] - base[N]["it"]) <= 1
+            assert np.abs(xa - xb).max() <= 1e-12 * np.abs(xb).max()
