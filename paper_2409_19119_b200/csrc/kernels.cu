@@ -1116,6 +1116,7 @@ __global__ void __launch_bounds__(128, MINB)
         }
     }
     pdl_wait();                                  // predecessor's outputs (p, r, scalars) complete
+    if (FUSED) { beta = sc->beta; alpha = sc->alpha; }   // issued beside the done load, not after it
     if (done && *(volatile const int *)done) {
         if (TMAG) {                              // drain the metric copies already in flight
             if (nit > 0) tma::mbar_wait(&gfull[0], 0);
@@ -1124,7 +1125,6 @@ __global__ void __launch_bounds__(128, MINB)
         return;
     }
     if (FUSED) {
-        beta = sc->beta; alpha = sc->alpha;
         if ((fold & 1) && *(volatile const int *)&sc->fold_ready) {
             // folded bookkeeping: (rho', rr) of the last update from every rank (mailbox channel 1),
             // beta = rho' / rho, convergence / maxit; one CTA records it (no separate fin kernel)
@@ -2209,6 +2209,28 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     __shared__ double s_sig[3];
     pdl_trigger();
     pdl_wait();
+    const uint64_t pol = tma::policy_keep(keep & 1);
+    const int64_t n2 = n >> 1;
+    const int2 *i2 = reinterpret_cast<const int2 *>(gi.idx);
+    const int64_t tile = (int64_t)UNR * blockDim.x;
+    int64_t base = blockIdx.x * tile + threadIdx.x;
+    double2 wv[UNR], dv[UNR], rv[UNR];
+    uint32_t ow[UNR];
+    int2 id[UNR];
+    auto load = [&](int64_t b0) {
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+            const int64_t h = b0 + (int64_t)q * blockDim.x;
+            if (h < n2) {
+                wv[q] = tma::ld2(w + 2 * h, pol); dv[q] = tma::ld2(dinv + 2 * h, pol); rv[q] = tma::ld2(r + 2 * h, pol);
+                ow[q] = tma::ldu(obits + ((2 * h) >> 5), pol) >> ((2 * h) & 31);
+                if (gi.idx) id[q] = i2[h];
+            }
+        }
+    };
+    // the first tile's streams are issued before the dependent scalar reads (done, sigma, rho), so
+    // their latencies overlap; w, r, Dinv are complete (stream order) whatever the scalars say
+    load(base);
     if (*(volatile int *)&sc->done) return;
     double sigma;
     if (mail.nranks > 1) {                       // sigma of every rank from the mailbox (channel 0)
@@ -2224,24 +2246,9 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
         return;
     }
     const double alpha = (fold ? sc->rho_next : sc->rho) / sigma;
-    const uint64_t pol = tma::policy_keep(keep & 1);
     double a0 = 0.0, a1 = 0.0;
-    const int64_t n2 = n >> 1;
-    const int2 *i2 = reinterpret_cast<const int2 *>(gi.idx);
-    const int64_t tile = (int64_t)UNR * blockDim.x;
-    for (int64_t base = blockIdx.x * tile + threadIdx.x; base < n2; base += (int64_t)gridDim.x * tile) {
-        double2 wv[UNR], dv[UNR], rv[UNR];
-        uint32_t ow[UNR];
-        int2 id[UNR];
-#pragma unroll
-        for (int q = 0; q < UNR; ++q) {
-            const int64_t h = base + (int64_t)q * blockDim.x;
-            if (h < n2) {
-                wv[q] = tma::ld2(w + 2 * h, pol); dv[q] = tma::ld2(dinv + 2 * h, pol); rv[q] = tma::ld2(r + 2 * h, pol);
-                ow[q] = tma::ldu(obits + ((2 * h) >> 5), pol) >> ((2 * h) & 31);
-                if (gi.idx) id[q] = i2[h];
-            }
-        }
+    for (bool first = true; base < n2; base += (int64_t)gridDim.x * tile, first = false) {
+        if (!first) load(base);
         if (gi.idx) {   // the gather-scatter QQ^T of w, on the fly (canonical order, bit-exact)
 #pragma unroll
             for (int q = 0; q < UNR; ++q) {

@@ -1,0 +1,3 @@
+bash tools/ab_var.sh
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/t_pytest.log 2>&1; tail -4 gpurun_out/t_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
