@@ -161,7 +161,33 @@ def cpu_baseline(mesh, iters, h2=0.0):
     O.pcg(1.0, h2, b, 0.0, iters, dinv=d)
     dt = time.perf_counter() - t0
     return {"value": mesh.n_dof * iters / dt / 1e9, "unit": "GDOF/s", "cores": 1, "kind": "oracle",
-            "sample": f"{iters} Jacobi-PCG iterations (incl. init) on the N=1 workload mesh, plain C oracle, 1 thread"}
+            "sample": f"{iters} Jacobi-PCG iterations (incl. init) on the N=1 workload mesh, plain C oracle, 1 thread",
+            "host": host_info()}
+
+
+def host_info():
+    """CPU model, cores available and a one-thread STREAM-triad figure of the host (SURVEY 8(d):
+    the CPU's own roofline for the oracle baseline)."""
+    import numpy as np
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    n = 1 << 25                                   # 3 x 256 MiB
+    a, b, c = np.zeros(n), np.ones(n), np.full(n, 2.0)
+    best = 1e9
+    for _ in range(3):
+        t0 = time.perf_counter()
+        np.multiply(c, 3.0, out=a)
+        np.add(a, b, out=a)                       # a = b + 3 c (two passes: 5 streams of 8 B)
+        best = min(best, time.perf_counter() - t0)
+    return {"cpu_model": model, "cores_available": len(os.sched_getaffinity(0)),
+            "triad_1thread_GBps": 5 * 8 * n / best / 1e9,
+            "triad_note": "numpy a = c*3; a += b (5 x 8 B per element moved), best of 3, one thread"}
 
 
 def run_reference(args):
