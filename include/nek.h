@@ -324,7 +324,8 @@ int nek_get_stats(nek_ctx *ctx, nek_stats_t *stats, int reset);
  *   0  default: N = 7 -> v5 (DMMA k-slabs, fused PCG prologue); N <= 9 otherwise -> v6
  *      (TMA-staged metric ring, line-wise contractions, fused prologue); N >= 10 -> v0
  *   1  v0 (any N, (i,j)-thread columns)       11  v6 at any N <= 9 (N = 7 included)
- *   2..10  N = 7 experiments (v1..v5 configurations); other N -> v0 */
+ *   2..10, 12  N = 7 experiments (v1..v5 configurations; 12 = v5 at 4 CTAs
+ *      per SM whatever the size); other N -> v0 */
 int nek_set_variant(nek_ctx *ctx, int ax_variant);
 
 /* --------------------------------------------- host-only planning (no GPU) */

@@ -1401,16 +1401,18 @@ static int v6_epb(int N)
 // the folded P2P bookkeeping (AxLaunch::fold) is implemented by the N = 7 kernel v5
 bool ax_has_fold(int variant, int N)
 {
-    return N == 7 && (variant == 0 || variant == 8 || variant == 9 || variant == 10);
+    return N == 7 && (variant == 0 || variant == 8 || variant == 9 || variant == 10 || variant == 12);
 }
 
 bool ax_has_fused(int variant, int N)
 {
-    return ((variant == 0 || variant == 8 || variant == 9 || variant == 10) && N == 7) || use_v6(variant, N);
+    return ((variant == 0 || variant == 8 || variant == 9 || variant == 10 || variant == 12) && N == 7) ||
+           use_v6(variant, N);
 }
 
 // variant (N = 7): 0 = default (v5, DMMA, k-slabs, 4 CTAs/SM), 8 = v5 at 3 CTAs/SM,
-// 9 = v5 + L2 bulk prefetch of the next element, 10 = v5 + TMA ring for G (3 CTAs/SM), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
+// 9 = v5 + L2 bulk prefetch of the next element, 10 = v5 + TMA ring for G (3 CTAs/SM), 12 = v5 at 4 CTAs/SM
+// (the large-problem default, at any size), 1 = v0 (any N), 2 = v1, 3 = v2 with 2 k-groups,
 // 4 = v2 with 4 k-groups, 5 = v3 with 2 k-groups, 6 = v3 with 1 k-group, 7 = v4 (DMMA, j-slabs)
 constexpr int V5_SMALL_ELEMS_PER_CTA = 16;
 static int per_sm_of(int variant)
@@ -1420,6 +1422,7 @@ static int per_sm_of(int variant)
     case 8: return 3;
     case 9: return 4;
     case 10: return 3;
+    case 12: return 4;
     case 7: return 3;
     case 6: return 6;
     case 2: return 3;
@@ -1519,9 +1522,12 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         return h2 != 0.0 ? ax_v2_launch<true, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                          : ax_v2_launch<false, 2>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
     }
-    if (N == 7 && (variant == 0 || variant == 8 || variant == 9 || variant == 10)) {
+    if (N == 7 && (variant == 0 || variant == 8 || variant == 9 || variant == 10 || variant == 12)) {
         if (nlaunch) ++*nlaunch;
         const int64_t grid = ax_grid(variant, N, L.nelem);
+        if (variant == 12)
+            return h2 != 0.0 ? ax_v5_launch<true, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                             : ax_v5_launch<false, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
         if (variant == 9)
             return h2 != 0.0 ? ax_v5_launch<true, 4, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 4, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
@@ -1529,8 +1535,13 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
             return h2 != 0.0 ? ax_v5_launch<true, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
         if (variant == 0) {
-            // few elements per CTA (the pipeline never fills): TMA-staged metric prefetch at 3 CTAs/SM;
-            // otherwise register streaming at 4 CTAs/SM (measured 98% of the copy peak at scale)
+            // few elements per CTA (the pipeline never fills): TMA-staged metric prefetch at 3 CTAs/SM --
+            // except for the fused PCG launch with L2-resident vectors, where register streaming at
+            // 3 CTAs/SM measured better (config 2: 22.6 vs 22.2 GDOF/s; nek_ax keeps the TMA ring,
+            // 32.4 vs 29.4); otherwise register streaming at 4 CTAs/SM (98% of the copy peak at scale)
+            if (L.nelem <= (int64_t)V5_SMALL_ELEMS_PER_CTA * 4 * 148 && L.fused && L.keep)
+                return h2 != 0.0 ? ax_v5_launch<true, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
+                                 : ax_v5_launch<false, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
             if (L.nelem <= (int64_t)V5_SMALL_ELEMS_PER_CTA * 4 * 148)
                 return h2 != 0.0 ? ax_v5_launch<true, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                                  : ax_v5_launch<false, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);

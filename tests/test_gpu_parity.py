@@ -249,7 +249,7 @@ def test_config2_full_size(nek):
         nek.free(ctx)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 def test_ax_all_variants_N7(nek, variant):
     """Every Ax kernel variant (nek_set_variant) against the oracle, Poisson and Helmholtz."""
     m = mg.box_mesh(3, 4, 5, 7, deform="bubble")
