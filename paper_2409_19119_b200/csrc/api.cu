@@ -165,7 +165,8 @@ static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w,
     if (!strm) strm = ctx->s_main;
     Scope sc(ctx, CLS_AX, strm);
     int nl = 0;
-    CK(launch_ax(ctx->variant, ctx->N, L, u, ctx->G, ctx->wJ, ctx->mbits, h1, h2, w, strm, &nl));
+    CK(launch_ax(ax_effective_variant(ctx->variant, ctx->N, L.fused, L.keep), ctx->N, L, u, ctx->G, ctx->wJ,
+                 ctx->mbits, h1, h2, w, strm, &nl));
     ctx->stats.ax_launches += L.nelem > 0;
     ctx->stats.launches += nl;
     ctx->stats.ax_elements += L.nelem;
@@ -288,6 +289,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     AxLaunch L;
     L.done = done;
     L.keep = ctx->l2keep;
+    const int var = ax_effective_variant(ctx->variant, ctx->N, fused, ctx->l2keep);   // the kernel do_ax launches
     if (fused) {
         L.fused = true;
         L.p = ctx->vp; L.x = ctx->vx; L.r = ctx->vr; L.dinv = ctx->vdinv; L.sc = ctx->sc;
@@ -296,12 +298,12 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     L.dst = ctx->red_loc + RED_SIGMA;
     if (ctx->nranks == 1) {
         L.nelem = ctx->E;
-        if (dot) { L.part = ctx->part; L.fin_total = ax_grid(ctx->variant, ctx->N, ctx->E); }
+        if (dot) { L.part = ctx->part; L.fin_total = ax_grid(var, ctx->N, ctx->E); }
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         return skip_local_gs ? NEK_OK : do_gs_local(ctx, w, done);
     }
     const int64_t nb = ctx->n_boundary, ni = ctx->E - ctx->n_boundary;
-    const int64_t g1 = ax_grid(ctx->variant, ctx->N, nb), g2 = ax_grid(ctx->variant, ctx->N, ni);
+    const int64_t g1 = ax_grid(var, ctx->N, nb), g2 = ax_grid(var, ctx->N, ni);
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
     L.elist = ctx->elist;
     const bool fold = push && use_fold(ctx);      // (rho', rr) pulled and booked by the Ax itself

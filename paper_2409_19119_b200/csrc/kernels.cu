@@ -155,6 +155,35 @@ __device__ __forceinline__ void mail_pull(const P2PMail &M, int channel, double 
     sum3[0] = a0; sum3[1] = a1; sum3[2] = a2;
 }
 
+// The same with the per-rank waits in parallel: called by all 32 lanes of one warp; lane q < nranks
+// acquires rank q's slot, lane 0 folds the values in rank order (the bits of mail_pull).  nranks <= 32.
+__device__ __forceinline__ void mail_pull_warp(const P2PMail &M, int channel, double *sum3)
+{
+    const int lane = threadIdx.x & 31;
+    if (M.nranks > 32) {
+        if (lane == 0) mail_pull(M, channel, sum3);
+        return;
+    }
+    const uint64_t e = *(volatile uint64_t *)&M.epochs[channel];
+    const size_t base = ((size_t)channel * 2 + (e & 1)) * M.nranks;
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    if (lane < M.nranks) {
+        const double *src = M.mbox + (base + lane) * 4;
+        wait_epoch(reinterpret_cast<const uint64_t *>(src + 3), e, M.err);
+        b0 = ((volatile const double *)src)[0];
+        b1 = ((volatile const double *)src)[1];
+        b2 = ((volatile const double *)src)[2];
+    }
+    double a0 = __shfl_sync(0xffffffffu, b0, 0), a1 = __shfl_sync(0xffffffffu, b1, 0),
+           a2 = __shfl_sync(0xffffffffu, b2, 0);
+    for (int q = 1; q < M.nranks; ++q) {
+        const double c0 = __shfl_sync(0xffffffffu, b0, q), c1 = __shfl_sync(0xffffffffu, b1, q),
+                     c2 = __shfl_sync(0xffffffffu, b2, q);
+        a0 += c0; a1 += c1; a2 += c2;
+    }
+    if (lane == 0) { sum3[0] = a0; sum3[1] = a1; sum3[2] = a2; }
+}
+
 // Fixed-order block sum for any blockDim.x <= 1024 (smem tree); sred needs blockDim.x entries.
 __device__ __forceinline__ double block_sum_any(double v, double *sred)
 {
@@ -1398,6 +1427,14 @@ static int v6_epb(int N)
     return 1;
 }
 
+// The fused PCG launch with L2-resident vectors: register streaming at 4 CTAs/SM (variant 12) beats the
+// TMA metric ring at any size (config 2: 23.8 vs 22.6 GDOF/s, Ax 89% vs 83% of the copy peak by
+// algorithmic bytes); nek_ax and the unfused launches keep the default (TMA ring: 32.4 vs 27.7).
+int ax_effective_variant(int variant, int N, bool fused, int keep)
+{
+    return (variant == 0 && N == 7 && fused && keep) ? 12 : variant;
+}
+
 // the folded P2P bookkeeping (AxLaunch::fold) is implemented by the N = 7 kernel v5
 bool ax_has_fold(int variant, int N)
 {
@@ -1535,13 +1572,9 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
             return h2 != 0.0 ? ax_v5_launch<true, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
         if (variant == 0) {
-            // few elements per CTA (the pipeline never fills): TMA-staged metric prefetch at 3 CTAs/SM --
-            // except for the fused PCG launch with L2-resident vectors, where register streaming at
-            // 3 CTAs/SM measured better (config 2: 22.6 vs 22.2 GDOF/s; nek_ax keeps the TMA ring,
-            // 32.4 vs 29.4); otherwise register streaming at 4 CTAs/SM (98% of the copy peak at scale)
-            if (L.nelem <= (int64_t)V5_SMALL_ELEMS_PER_CTA * 4 * 148 && L.fused && L.keep)
-                return h2 != 0.0 ? ax_v5_launch<true, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
-                                 : ax_v5_launch<false, 3>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
+            // few elements per CTA (the pipeline never fills): TMA-staged metric prefetch at 3 CTAs/SM
+            // (the fused PCG launch with L2-resident vectors runs variant 12 instead, see
+            // ax_effective_variant); otherwise register streaming at 4 CTAs/SM (98% of the copy peak at scale)
             if (L.nelem <= (int64_t)V5_SMALL_ELEMS_PER_CTA * 4 * 148)
                 return h2 != 0.0 ? ax_v5_launch<true, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                                  : ax_v5_launch<false, 3, false, true>(L, u, G, wJ, mbits, h1, h2, w, grid, s);
@@ -2245,7 +2278,7 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     if (*(volatile int *)&sc->done) return;
     double sigma;
     if (mail.nranks > 1) {                       // sigma of every rank from the mailbox (channel 0)
-        if (threadIdx.x == 0) mail_pull(mail, 0, s_sig);
+        if (threadIdx.x < 32) mail_pull_warp(mail, 0, s_sig);
         __syncthreads();
         sigma = s_sig[0];
         if (blockIdx.x == 0 && threadIdx.x == 0) sc->sigma = sigma;
@@ -2488,10 +2521,11 @@ cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const doub
 // P2P: pull <r, Dinv r> and <r, r> of every rank (channel 1) and do the bookkeeping
 __global__ void pcg_fin_p2p_kernel(PcgScalars *sc, P2PMail mail, double *hist)
 {
+    __shared__ double v[3];
     if (sc->done) return;
-    double v[3];
-    mail_pull(mail, 1, v);
-    pcg_bookkeep(sc, v[0], v[1], sc->rho / sc->sigma, hist);
+    mail_pull_warp(mail, 1, v);
+    __syncwarp();
+    if (threadIdx.x == 0) pcg_bookkeep(sc, v[0], v[1], sc->rho / sc->sigma, hist);
 }
 
 // folded path, after the last update of a solve: the bookkeeping its (rho', rr) would get from the next Ax
@@ -2518,7 +2552,7 @@ cudaError_t launch_pcg_fold_finish(PcgScalars *sc, const P2PMail &mail, double *
 
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s)
 {
-    pcg_fin_p2p_kernel<<<1, 1, 0, s>>>(sc, mail, hist);
+    pcg_fin_p2p_kernel<<<1, 32, 0, s>>>(sc, mail, hist);
     return cudaGetLastError();
 }
 

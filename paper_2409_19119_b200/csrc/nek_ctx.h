@@ -103,6 +103,7 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
                       const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch);
 int64_t ax_grid(int variant, int N, int64_t nelem);      // partial slots one launch writes
 bool ax_has_fold(int variant, int N);
+int ax_effective_variant(int variant, int N, bool fused, int keep);
 int ax_partials_needed(int variant, int N, int64_t E);
 // FP32 operator (v6, N <= 9): Gf is [E][ax_gstride_f(N)] (6 planes, padded to 16 bytes per element)
 cudaError_t launch_ax_f(int N, int64_t E, const float *u, const float *Gf, const float *wJf, const uint32_t *mbits,
