@@ -303,7 +303,16 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         return skip_local_gs ? NEK_OK : do_gs_local(ctx, w, done);
     }
     const int64_t nb = ctx->n_boundary, ni = ctx->E - ctx->n_boundary;
-    const int64_t g1 = ax_grid(var, ctx->N, nb), g2 = ax_grid(var, ctx->N, ni);
+    int64_t g1 = ax_grid(var, ctx->N, nb), g2 = ax_grid(var, ctx->N, ni);
+    // concurrent boundary / interior launches, v5: split one wave of CTAs between them (the boundary
+    // CTAs take ~4 elements each) so no interior CTA starts late and the halo pack finds the slots the
+    // boundary CTAs free (NEK_BND_SPLIT=0: each launch sized on its own)
+    const bool split = ctx->concurrent_bnd && ctx->bnd_split && ax_has_fold(var, ctx->N) && nb > 0 && ni > 0;
+    if (split) {
+        const int64_t wave = ax_grid(var, ctx->N, ctx->E);
+        g1 = std::min<int64_t>(nb, std::max<int64_t>(1, std::min<int64_t>((nb + 3) / 4, wave / 4)));
+        g2 = std::min<int64_t>(ni, std::max<int64_t>(1, wave - g1));
+    }
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
     L.elist = ctx->elist;
     const bool fold = push && use_fold(ctx);      // (rho', rr) pulled and booked by the Ax itself
@@ -328,10 +337,12 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         if (dot) { L.part = ctx->part; L.fin_total = g1 + g2; L.ctas_total = (unsigned)(g1 + g2); }
         if (push) L.mail = mail_of(ctx);
         L.nelem = nb; L.eoff = 0; L.part_off = 0;
+        if (split) L.grid = g1;
         if ((st = do_ax(ctx, h1, h2, u, w, L, ctx->s_hi)) != NEK_OK) return st;
         if ((st = halo_start(ctx, w, done, ctx->s_hi)) != NEK_OK) return st;
         CK(cudaEventRecord(ctx->ev_bnd, ctx->s_hi));
         L.nelem = ni; L.eoff = nb; L.part_off = g1;
+        if (split) L.grid = g2;
         if (fold) L.fold = 1 | (nb > 0 ? 0 : 2);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_bnd, 0));
@@ -685,6 +696,8 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         // ones the send must not queue behind the persistent interior grid (measured)
         const char *cenv = getenv("NEK_CONCURRENT_BND");
         ctx->concurrent_bnd = cenv ? std::strcmp(cenv, "1") == 0 : E < 16384;
+        const char *senv = getenv("NEK_BND_SPLIT");
+        ctx->bnd_split = !(senv && std::strcmp(senv, "0") == 0);
         const char *genv = getenv("NEK_GS_INLINE");
         ctx->gs_inline = genv && std::strcmp(genv, "1") == 0;
     }

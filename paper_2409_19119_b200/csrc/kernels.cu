@@ -1561,7 +1561,7 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
     }
     if (N == 7 && (variant == 0 || variant == 8 || variant == 9 || variant == 10 || variant == 12)) {
         if (nlaunch) ++*nlaunch;
-        const int64_t grid = ax_grid(variant, N, L.nelem);
+        const int64_t grid = L.grid > 0 ? std::min<int64_t>(L.grid, L.nelem) : ax_grid(variant, N, L.nelem);
         if (variant == 12)
             return h2 != 0.0 ? ax_v5_launch<true, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s)
                              : ax_v5_launch<false, 4>(L, u, G, wJ, mbits, h1, h2, w, grid, s);

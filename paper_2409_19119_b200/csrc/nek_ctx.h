@@ -98,6 +98,7 @@ struct AxLaunch {
     // mailbox at entry and take beta from it; bit 1 = this launch's CTA 0 also does the bookkeeping
     int fold = 0;
     double *hist = nullptr;
+    int64_t grid = 0;                    // > 0: CTAs of this launch (v5), else ax_grid
 };
 cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
                       const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch);
@@ -254,6 +255,7 @@ struct nek_ctx {
     bool gs_inline = false;
     int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
     bool fold = false;                              // P2P: bookkeeping folded into the next Ax (no fin kernel)
+    bool bnd_split = true;                          // concurrent boundary/interior Ax share one wave of CTAs
     int64_t l2_setaside = 0, l2_setaside_max = 0;   // persisting L2 bytes granted / allowed
     bool concurrent_bnd = false;
     bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts         // NEK_CONCURRENT_BND=1: boundary Ax + send on s_hi beside the interior
