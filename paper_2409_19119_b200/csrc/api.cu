@@ -201,7 +201,8 @@ static int halo_start(nek_ctx *ctx, const T *v, const int *done, cudaStream_t st
         CK(launch_gs_pack_p2p_fused<T>(ctx->ifc_perm, ctx->ifc_offs, v, as<T>(ctx->ifc_partial), ctx->nslots,
                                        ctx->send_run, ctx->d_slot_nbr, ctx->d_peer_recv, ctx->d_remote_off,
                                        ctx->d_send_offs, ctx->d_remote_half, (int)ctx->neighbors.size(), ctx->rank,
-                                       ctx->d_peer_hflags, ctx->epochs, ctx->counter + 3, done, strm));
+                                       ctx->d_peer_hflags, ctx->epochs, ctx->counter + 3, done, strm,
+                                       reinterpret_cast<const int4 *>(ctx->pack4)));
         ctx->stats.launches += 1;
         ctx->stats.halo_launches += 1;
         return NEK_OK;
@@ -705,6 +706,15 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     CK(upload(ctx, &ctx->ifc_perm, p->ifc_perm));
     CK(upload(ctx, &ctx->ifc_offs, to32(p->ifc_offs)));
     CK(upload(ctx, &ctx->send_run, p->send_run));
+    {   // per send slot, the local copies of its run in canonical order (the P2P pack's gather list)
+        std::vector<int32_t> p4(4 * p->send_run.size(), -1);
+        for (size_t q = 0; q < p->send_run.size(); ++q) {
+            const int64_t r = p->send_run[q], a = p->ifc_offs[r], b = p->ifc_offs[r + 1];
+            if (b - a > 4) { p4[4 * q] = -2; continue; }
+            for (int64_t c = a; c < b; ++c) p4[4 * q + (c - a)] = p->ifc_perm[c];
+        }
+        CK(upload(ctx, &ctx->pack4, p4));
+    }
     CK(upload(ctx, &ctx->coffs, to32(p->contrib_offs)));
     CK(upload(ctx, &ctx->contrib, p->contrib));
     ctx->nslots = (int64_t)p->send_run.size();
@@ -833,7 +843,8 @@ int nek_free(nek_ctx *ctx)
     if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
     for (auto &t : ctx->graph_timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (void *p : {(void *)ctx->G, (void *)ctx->wJ, (void *)ctx->perm, (void *)ctx->offs, (void *)ctx->ifc_perm,
-                    (void *)ctx->ifc_offs, (void *)ctx->send_run, (void *)ctx->coffs, (void *)ctx->contrib,
+                    (void *)ctx->ifc_offs, (void *)ctx->send_run, (void *)ctx->pack4, (void *)ctx->coffs,
+                    (void *)ctx->contrib,
                     (void *)ctx->ifc_partial, (void *)ctx->sendbuf, (void *)ctx->recvbuf, (void *)ctx->elist,
                     (void *)ctx->mbits, (void *)ctx->obits, (void *)ctx->vr, (void *)ctx->vp, (void *)ctx->vw,
                     (void *)ctx->vx, (void *)ctx->vdinv, (void *)ctx->vtmp, (void *)ctx->stage_in,

@@ -2662,7 +2662,7 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
                                          const int64_t *__restrict__ remote_off, const int64_t *__restrict__ send_offs,
                                          const int64_t *__restrict__ remote_half, int nnbr, int me,
                                          uint64_t *const *peer_hflags, uint64_t *epochs, unsigned int *counter,
-                                         const int *done)
+                                         const int *done, const int4 *__restrict__ pack4)
 {
     __shared__ int s_last;
     const uint64_t e = epochs[2] + 1;
@@ -2671,9 +2671,18 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
         for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < nslots;
              sidx += (int64_t)gridDim.x * blockDim.x) {
             const int run = send_run[sidx];
-            const int o0 = offs[run], o1 = offs[run + 1];
-            T s = v[perm[o0]];
-            for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
+            T s;
+            const int4 c4 = pack4 ? pack4[sidx] : make_int4(-2, -1, -1, -1);
+            if (c4.x >= 0) {                     // <= 4 local copies, listed per slot (one dependent level)
+                s = v[c4.x];
+                if (c4.y >= 0) s += v[c4.y];
+                if (c4.z >= 0) s += v[c4.z];
+                if (c4.w >= 0) s += v[c4.w];
+            } else {
+                const int o0 = offs[run], o1 = offs[run + 1];
+                s = v[perm[o0]];
+                for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
+            }
             partial[run] = s;
             const int k = slot_nbr[sidx];
             reinterpret_cast<T *>(peer_recv[k])[par * remote_half[k] + remote_off[k] + (sidx - send_offs[k])] = s;
@@ -2698,13 +2707,14 @@ cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, c
                                      int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
                                      double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
                                      const int64_t *remote_half, int nnbr, int me, uint64_t *const *peer_hflags,
-                                     uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s)
+                                     uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s,
+                                     const int4 *pack4)
 {
-    // latency-bound gathers (slot -> run -> copies -> values): many small CTAs in flight
+    // latency-bound gathers (slot -> copies -> values with pack4, else slot -> run -> copies -> values)
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + 127) / 128, 148 * 16));
     gs_pack_p2p_fused_kernel<<<blocks, 128, 0, s>>>(nslots, perm, offs, v, partial, send_run, slot_nbr, peer_recv,
                                                     remote_off, send_offs, remote_half, nnbr, me, peer_hflags, epochs,
-                                                    counter, done);
+                                                    counter, done, pack4);
     return cudaGetLastError();
 }
 
@@ -2795,7 +2805,7 @@ cudaError_t launch_axpby(int64_t n, double alpha, const double *x, double beta, 
                                                      const int32_t *, const int32_t *, double *const *,         \
                                                      const int64_t *, const int64_t *, const int64_t *, int, int, \
                                                      uint64_t *const *, uint64_t *, unsigned int *, const int *, \
-                                                     cudaStream_t);
+                                                     cudaStream_t, const int4 *);
 NEK_GS_INST(double)
 NEK_GS_INST(float)
 #undef NEK_GS_INST

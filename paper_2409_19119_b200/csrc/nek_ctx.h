@@ -190,7 +190,8 @@ cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, c
                                      int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
                                      double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
                                      const int64_t *remote_half, int nnbr, int me, uint64_t *const *peer_hflags,
-                                     uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s);
+                                     uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s,
+                                     const int4 *pack4 = nullptr);
 
 cudaError_t launch_pcg_init_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_update(int64_t n, const uint32_t *obits, const double *dinv, const double *p,
@@ -261,6 +262,7 @@ struct nek_ctx {
     bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts         // NEK_CONCURRENT_BND=1: boundary Ax + send on s_hi beside the interior
     nekb200::GsClasses gsc;
     int32_t *ifc_perm = nullptr, *ifc_offs = nullptr, *send_run = nullptr, *coffs = nullptr, *contrib = nullptr;
+    int32_t *pack4 = nullptr;   // [nslots][4] local copies of each send slot's run (-1 pad; x = -2: > 4 copies)
     int64_t nifc = 0, nifc_perm = 0, nslots = 0;
     std::vector<int32_t> neighbors;
     std::vector<int64_t> send_offs;
