@@ -75,6 +75,33 @@ typedef struct {
     unsigned char nccl_id[128];
 } nek_comm;
 
+/*
+ * Loopback group: P virtual ranks in ONE process on ONE GPU (SURVEY 4 "loopback comm backend";
+ * SPEC S:196/S:235 runs its ranks under one scheduler), so the multi-rank path -- the halo exchange
+ * of interface partial sums (unit-depth exchange), its overlap with interior-element work
+ * and the rank-ordered reductions -- runs and is testable on a single GPU.
+ *   nek_loopback_create  nranks in [1, 64]; transport 0 = the peer-memory kernels of the NVLink
+ *                        path (halo pack into the neighbour's receive buffer, flag/epoch waits,
+ *                        mailbox reductions), 1 = the NCCL-path kernels (pack / unpack around a
+ *                        staged copy).  Returns NEK_OK / NEK_EINVAL / NEK_ENOMEM.
+ *   nek_loopback_comm    fills *comm for `rank` (rank, nranks and a tag in nccl_id that names
+ *                        the group); pass it to nek_setup like an NCCL communicator.
+ *   nek_loopback_abort   makes every pending and later group barrier fail (NEK_ENCCL), e.g.
+ *                        when one rank's thread stops early.
+ *   nek_loopback_free    after every context of the group has been freed.
+ * Each rank is driven by its own host thread, making the same calls as a one-process-per-GPU
+ * rank would.  Inside the library every step that consumes another rank's data waits (stream
+ * events swapped through the group) for that rank's producer, so no kernel spins on a rank that
+ * has not launched; PCG iterations are launched directly rather than from a CUDA graph.
+ * Barriers time out after NEK_LOOPBACK_TIMEOUT_S seconds (default 60).  The group object is
+ * owned by the caller and must outlive its contexts.
+ */
+typedef struct nek_loopback nek_loopback;
+int nek_loopback_create(int nranks, int transport, nek_loopback **out);
+int nek_loopback_comm(nek_loopback *lb, int rank, nek_comm *comm);
+int nek_loopback_abort(nek_loopback *lb);
+int nek_loopback_free(nek_loopback *lb);
+
 int nek_version(void);                 /* returns NEK_ABI_VERSION */
 const char *nek_last_error(void);      /* message of the last failure without a context (thread-local) */
 
@@ -139,6 +166,15 @@ int nek_gs(nek_ctx *ctx, double *v, void *stream);
  * Returns NEK_OK (converged; also b = 0 -> x = 0, iters = 0), NEK_MAXIT,
  * NEK_ENOTSPD (x holds the last iterate), or an error.  The call synchronises
  * `stream` (convergence is polled from the device every few iterations).
+ * L2 residency: when the PCG vectors fit in the L2 (nek_info_t.l2_keep), the
+ * call raises the DEVICE-WIDE persisting-L2 limit (cudaLimitPersistingL2CacheSize)
+ * for its duration and restores the previous value before returning; kernels of
+ * other contexts running concurrently on the device see a smaller normal L2.
+ * Multi-rank: a peer wait that times out (NEK_P2P_TIMEOUT_MS, default 10 s)
+ * returns NEK_ENCCL; the error is sticky -- every later call on the context
+ * returns NEK_ENCCL and the context must be rebuilt.  nek_ax / nek_gs on device
+ * pointers report such a timeout at the next call (their results hold NaN in the
+ * affected entries instead of stale data).
  */
 int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x, double tol,
                   int maxit, int *iters, double *relres, double *hist, void *stream);
@@ -320,12 +356,13 @@ typedef struct {
 int nek_set_timing(nek_ctx *ctx, int on);
 int nek_get_stats(nek_ctx *ctx, nek_stats_t *stats, int reset);
 
-/* Ax kernel variant selection (0 = default).  For experiments and tests.
- *   0  default: N = 7 -> v5 (DMMA k-slabs, fused PCG prologue); N <= 9 otherwise -> v6
- *      (TMA-staged metric ring, line-wise contractions, fused prologue); N >= 10 -> v0
+/* Ax kernel variant selection (0 = default).  For experiments and tests; other values -> NEK_EINVAL.
+ *   0  default: N = 7 -> v5 (DMMA k-slabs, fused PCG prologue; TMA metric ring at 3 CTAs/SM for
+ *      launches of <= 16 elements per CTA, register streaming at 4 CTAs/SM otherwise); N <= 9
+ *      otherwise -> v6 (TMA-staged metric ring, line-wise contractions, fused prologue); N >= 10 -> v0
  *   1  v0 (any N, (i,j)-thread columns)       11  v6 at any N <= 9 (N = 7 included)
- *   2..10, 12  N = 7 experiments (v1..v5 configurations; 12 = v5 at 4 CTAs
- *      per SM whatever the size); other N -> v0 */
+ *   8  v5 register streaming at 3 CTAs/SM      10  v5 TMA metric ring at 3 CTAs/SM
+ *   12 v5 register streaming at 4 CTAs/SM (any size); for N != 7, 8/10/12 run v0 */
 int nek_set_variant(nek_ctx *ctx, int ax_variant);
 
 /* --------------------------------------------- host-only planning (no GPU) */

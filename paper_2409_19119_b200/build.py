@@ -41,22 +41,49 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(args):
+    cmd, src = args
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return src, r.returncode, r.stdout + r.stderr
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel (one nvcc per translation unit), then link."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     inc, lib = nccl_paths()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    objdir = os.path.join(PKG, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    common = [nvcc, *ARCH, "-lineinfo", "-O3", "-std=c++17", "--expt-relaxed-constexpr",
+              "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
+    if verbose:
+        common += ["-Xptxas", "-v"]
+    jobs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + f".{os.getpid()}.o")
+        objs.append(obj)
+        jobs.append(([*common, "-c", src, "-o", obj], src))
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(_compile, jobs))
+    failed = [(src, out) for src, rc, out in results if rc != 0]
+    if failed:
+        for src, out in failed:
+            sys.stderr.write(f"--- {src}\n{out}")
+        raise RuntimeError("nvcc build of libnek.so failed: " + ", ".join(os.path.basename(s) for s, _ in failed))
+    if verbose:
+        for src, _, out in results:
+            sys.stderr.write(f"--- {src}\n{out}")
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc, *ARCH, "-lineinfo", "-O3", "-std=c++17", "--expt-relaxed-constexpr",
-           "-Xcompiler", "-fPIC,-O3", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
-           *sources(), "-L", lib, "-l:libnccl.so.2", f"-Xlinker", f"-rpath={lib}", "-o", tmp]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    link = [nvcc, *ARCH, "-shared", *objs, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}", "-o", tmp]
+    r = subprocess.run(link, capture_output=True, text=True)
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc build of libnek.so failed")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc link of libnek.so failed")
     os.replace(tmp, LIB)
     return LIB
 

@@ -158,6 +158,75 @@ static void harvest_timers(nek_ctx *ctx)
     P.pending.clear();
 }
 
+// ------------------------------------------------------------ collectives
+// One process per GPU: NCCL at setup and for the staged (NCCL) transport; peer memory (CUDA IPC) for
+// the NVLink transport.  Loopback group (P virtual ranks on one GPU, loopback.h): host allgathers
+// through the group, stage-serialised device copies, sibling pointers instead of IPC handles.
+static int lb_fail(nek_ctx *ctx)
+{
+    return fail(ctx, NEK_ENCCL, "loopback group barrier failed (a rank stopped or timed out)");
+}
+
+// every rank's `bytes` host bytes into all[nranks * bytes] (rank order); synchronous
+static int coll_allgather_host(nek_ctx *ctx, const void *mine, size_t bytes, void *all)
+{
+    if (ctx->nranks == 1) { std::memcpy(all, mine, bytes); return NEK_OK; }
+    if (ctx->lb) return ctx->lb->allgather(ctx->rank, mine, bytes, all) ? NEK_OK : lb_fail(ctx);
+    const size_t b = std::max<size_t>(bytes, 1);
+    unsigned char *d = nullptr;
+    CK(cudaMalloc(&d, b * (ctx->nranks + 1)));
+    if (bytes) CK(cudaMemcpy(d + b * ctx->nranks, mine, bytes, cudaMemcpyHostToDevice));
+    NK(ncclAllGather(d + b * ctx->nranks, d, b, ncclUint8, ctx->nccl, ctx->s_main));
+    CK(cudaStreamSynchronize(ctx->s_main));
+    for (int q = 0; q < ctx->nranks && bytes; ++q)
+        CK(cudaMemcpy(static_cast<char *>(all) + q * bytes, d + q * b, bytes, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return NEK_OK;
+}
+
+// loopback only: `strm` waits for the work every other rank issued before this point (each rank
+// records an event, the ranks swap events through the group; two events alternate so a fast rank's
+// next record never replaces one a slow rank has still to wait on)
+static int lb_stage_sync(nek_ctx *ctx, cudaStream_t strm)
+{
+    if (!ctx->lb || ctx->nranks == 1) return NEK_OK;
+    cudaEvent_t mine = ctx->ev_lb[ctx->lb_seq++ & 1];
+    CK(cudaEventRecord(mine, strm));
+    std::vector<cudaEvent_t> ev(ctx->nranks);
+    if (!ctx->lb->allgather(ctx->rank, &mine, sizeof(mine), ev.data())) return lb_fail(ctx);
+    for (int q = 0; q < ctx->nranks; ++q)
+        if (q != ctx->rank) CK(cudaStreamWaitEvent(strm, ev[q], 0));
+    return NEK_OK;
+}
+
+// every rank's `bytes` device bytes at `send` into recv[nranks * bytes] (rank order), stream-ordered
+static int coll_allgather_dev(nek_ctx *ctx, const void *send, void *recv, size_t bytes, cudaStream_t strm)
+{
+    if (ctx->nranks == 1) {
+        CK(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, strm));
+        return NEK_OK;
+    }
+    if (!ctx->lb) {
+        NK(ncclAllGather(send, recv, bytes, ncclUint8, ctx->nccl, strm));
+        return NEK_OK;
+    }
+    std::vector<const void *> src(ctx->nranks);
+    if (!ctx->lb->allgather(ctx->rank, &send, sizeof(send), src.data())) return lb_fail(ctx);
+    int st;
+    if ((st = lb_stage_sync(ctx, strm)) != NEK_OK) return st;   // every sender's producer has run
+    for (int q = 0; q < ctx->nranks; ++q)
+        CK(cudaMemcpyAsync(static_cast<char *>(recv) + q * bytes, src[q], bytes, cudaMemcpyDeviceToDevice, strm));
+    return lb_stage_sync(ctx, strm);   // no rank rewrites its send buffer before every rank has copied it
+}
+
+// a peer wait timed out earlier in this context (sticky: the exchange epochs are out of step)
+static int check_peer(nek_ctx *ctx)
+{
+    if (ctx->p2p_err_host && *(volatile int *)ctx->p2p_err_host)
+        return fail(ctx, NEK_ENCCL, "peer exchange timed out (a rank stopped participating); rebuild the context");
+    return NEK_OK;
+}
+
 // ------------------------------------------------------------ building blocks
 static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, const AxLaunch &L,
                  cudaStream_t strm = nullptr)
@@ -165,8 +234,8 @@ static int do_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w,
     if (!strm) strm = ctx->s_main;
     Scope sc(ctx, CLS_AX, strm);
     int nl = 0;
-    CK(launch_ax(ax_effective_variant(ctx->variant, ctx->N, L.fused, L.keep), ctx->N, L, u, ctx->G, ctx->wJ,
-                 ctx->mbits, h1, h2, w, strm, &nl));
+    const int var = L.variant >= 0 ? L.variant : ax_effective_variant(ctx->variant, ctx->N, L.fused, L.keep);
+    CK(launch_ax(var, ctx->N, L, u, ctx->G, ctx->wJ, ctx->mbits, h1, h2, w, strm, &nl));
     ctx->stats.ax_launches += L.nelem > 0;
     ctx->stats.launches += nl;
     ctx->stats.ax_elements += L.nelem;
@@ -181,7 +250,7 @@ static P2PMail mail_of(const nek_ctx *ctx)
 {
     P2PMail m;
     m.mbox = ctx->mbox; m.peer_mbox = ctx->d_peer_mbox; m.epochs = ctx->epochs; m.err = ctx->p2p_err;
-    m.me = ctx->rank; m.nranks = ctx->nranks;
+    m.me = ctx->rank; m.nranks = ctx->nranks; m.timeout_ns = ctx->p2p_timeout_ns;
     return m;
 }
 
@@ -213,6 +282,20 @@ static int halo_start(nek_ctx *ctx, const T *v, const int *done, cudaStream_t st
                                  ctx->send_run, as<T>(ctx->sendbuf), done, strm));
         ctx->stats.launches += (ctx->nifc > 0) + (ctx->nslots > 0);
         ctx->stats.halo_launches += 1;
+    }
+    if (ctx->lb) {   // staged loopback: the NCCL send/recv pairs become device copies from the neighbours
+        int st;
+        if ((st = lb_stage_sync(ctx, strm)) != NEK_OK) return st;
+        for (size_t k = 0; k < ctx->neighbors.size(); ++k) {
+            const size_t cnt = (size_t)(ctx->send_offs[k + 1] - ctx->send_offs[k]);
+            if (cnt)
+                CK(cudaMemcpyAsync(as<T>(ctx->recvbuf) + ctx->send_offs[k],
+                                   reinterpret_cast<const T *>(ctx->lb_halo_src[k]), cnt * sizeof(T),
+                                   cudaMemcpyDeviceToDevice, strm));
+        }
+        if ((st = lb_stage_sync(ctx, strm)) != NEK_OK) return st;
+        CK(cudaEventRecord(ctx->ev_join, strm));
+        return NEK_OK;
     }
     CK(cudaEventRecord(ctx->ev_fork, strm));
     CK(cudaStreamWaitEvent(ctx->s_comm, ctx->ev_fork, 0));
@@ -254,12 +337,14 @@ static int do_gs_local(nek_ctx *ctx, T *v, const int *done)
 template <class T>
 static int gs_local_and_unpack_p2p(nek_ctx *ctx, T *v, const int *done, bool skip_local = false)
 {
+    int st;
+    if ((st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;   // loopback: the neighbours' packs ran
     Scope sc(ctx, CLS_GS);
     HaloUnpack U;
     U.nifc = ctx->nifc; U.perm = ctx->ifc_perm; U.offs = ctx->ifc_offs; U.coffs = ctx->coffs;
     U.contrib = ctx->contrib; U.nbr = ctx->d_nbr; U.partial = ctx->ifc_partial; U.recv = ctx->recv2;
     U.half = std::max<int64_t>(ctx->nslots, 1); U.hflags = ctx->hflags; U.epochs = ctx->epochs; U.nnbr = (int)ctx->neighbors.size();
-    U.err = ctx->p2p_err;
+    U.err = ctx->p2p_err; U.timeout_ns = ctx->p2p_timeout_ns;
     CK(launch_gs_classes_unpack<T>(skip_local ? GsClasses() : ctx->gsc, U, v, done, ctx->s_main));
     ctx->stats.gs_launches += 1;
     ctx->stats.launches += 1;
@@ -281,16 +366,14 @@ static int gs_full(nek_ctx *ctx, T *v, const int *done)
 // w = M QQ^T (h1 K_L + h2 B_L) M u.  With dot: this rank's <M u, A_L M u> into
 // red_loc[RED_SIGMA] (then allgathered across ranks into red_all).  fused: the
 // PCG direction / deferred x update is applied in the Ax prologue (u == vp).
-static bool use_fold(const nek_ctx *ctx) { return ctx->fold && ctx->p2p && ax_has_fold(ctx->variant, ctx->N); }
-
 static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, bool dot, const int *done,
-                    bool fused = false, bool skip_local_gs = false)
+                    bool fused = false)
 {
     int st;
     AxLaunch L;
     L.done = done;
     L.keep = ctx->l2keep;
-    const int var = ax_effective_variant(ctx->variant, ctx->N, fused, ctx->l2keep);   // the kernel do_ax launches
+    int var = ax_effective_variant(ctx->variant, ctx->N, fused, ctx->l2keep);   // the kernel do_ax launches
     if (fused) {
         L.fused = true;
         L.p = ctx->vp; L.x = ctx->vx; L.r = ctx->vr; L.dinv = ctx->vdinv; L.sc = ctx->sc;
@@ -301,14 +384,20 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         L.nelem = ctx->E;
         if (dot) { L.part = ctx->part; L.fin_total = ax_grid(var, ctx->N, ctx->E); }
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
-        return skip_local_gs ? NEK_OK : do_gs_local(ctx, w, done);
+        return do_gs_local(ctx, w, done);
     }
     const int64_t nb = ctx->n_boundary, ni = ctx->E - ctx->n_boundary;
+    // concurrent boundary / interior launches of the N = 7 kernel: split one wave of CTAs between them
+    // (the boundary CTAs take ~4 elements each) so no interior CTA starts late and the halo pack finds
+    // the slots the boundary CTAs free (NEK_BND_SPLIT=0: each launch sized on its own).  Both launches
+    // run the v5 configuration the whole partition would get, so the wave is the one they occupy.
+    const bool split = ctx->concurrent_bnd && ctx->bnd_split && ctx->N == 7 &&
+                       (var == 0 || var == 8 || var == 10 || var == 12) && nb > 0 && ni > 0;
+    if (split) {
+        var = ax_concrete_variant(var, ctx->N, ctx->E);
+        L.variant = var;
+    }
     int64_t g1 = ax_grid(var, ctx->N, nb), g2 = ax_grid(var, ctx->N, ni);
-    // concurrent boundary / interior launches, v5: split one wave of CTAs between them (the boundary
-    // CTAs take ~4 elements each) so no interior CTA starts late and the halo pack finds the slots the
-    // boundary CTAs free (NEK_BND_SPLIT=0: each launch sized on its own)
-    const bool split = ctx->concurrent_bnd && ctx->bnd_split && ax_has_fold(var, ctx->N) && nb > 0 && ni > 0;
     if (split) {
         const int64_t wave = ax_grid(var, ctx->N, ctx->E);
         g1 = std::min<int64_t>(nb, std::max<int64_t>(1, std::min<int64_t>((nb + 3) / 4, wave / 4)));
@@ -316,8 +405,6 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     }
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
     L.elist = ctx->elist;
-    const bool fold = push && use_fold(ctx);      // (rho', rr) pulled and booked by the Ax itself
-    if (fold) { L.fold = 1 | (nb > 0 ? 2 : 0); L.hist = ctx->hist; }
     if (ax_has_fused(ctx->variant, ctx->N) && ctx->p2p && !ctx->concurrent_bnd) {
         // Boundary elements, then the halo send, then the interior elements, in stream order: the
         // NVLink transfer overlaps the interior work and the send never waits for SM
@@ -328,7 +415,6 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
         L.nelem = ni; L.eoff = nb; L.part_off = g1;
-        if (fold) L.fold = 1 | (nb > 0 ? 0 : 2);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
     } else if (ax_has_fused(ctx->variant, ctx->N)) {
         // Boundary elements and the halo send on the high-priority stream, interior elements on
@@ -344,7 +430,6 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         CK(cudaEventRecord(ctx->ev_bnd, ctx->s_hi));
         L.nelem = ni; L.eoff = nb; L.part_off = g1;
         if (split) L.grid = g2;
-        if (fold) L.fold = 1 | (nb > 0 ? 0 : 2);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_bnd, 0));
     } else {
@@ -361,8 +446,8 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
             if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         }
     }
-    if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, w, done, skip_local_gs);
-    if (!skip_local_gs && (st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
+    if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, w, done);
+    if ((st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
     return halo_finish(ctx, w, done);
 }
 
@@ -372,17 +457,24 @@ static int exchange_slots(nek_ctx *ctx, int channel)
 {
     if (ctx->nranks == 1) return NEK_OK;
     if (ctx->p2p) {
-        CK(launch_red_exchange(channel, ctx->rank, ctx->nranks, ctx->red_loc, ctx->red_all, ctx->mbox,
-                               ctx->d_peer_mbox, ctx->epochs, ctx->p2p_err, ctx->s_main));
+        const P2PMail m = mail_of(ctx);
+        if (ctx->lb) {   // loopback: every rank's push before any rank's pull
+            int st;
+            CK(launch_red_exchange(channel, m, ctx->red_loc, ctx->red_all, 1, ctx->s_main));
+            if ((st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;
+            CK(launch_red_exchange(channel, m, ctx->red_loc, ctx->red_all, 2, ctx->s_main));
+            ctx->stats.launches += 2;
+            return NEK_OK;
+        }
+        CK(launch_red_exchange(channel, m, ctx->red_loc, ctx->red_all, 3, ctx->s_main));
         ctx->stats.launches += 1;
         return NEK_OK;
     }
-    NK(ncclAllGather(ctx->red_loc, ctx->red_all, RED_N, ncclDouble, ctx->nccl, ctx->s_main));
-    return NEK_OK;
+    return coll_allgather_dev(ctx, ctx->red_loc, ctx->red_all, sizeof(double) * RED_N, ctx->s_main);
 }
 
 // The persisting-L2 carve-out of an L2-resident solve, raised on entry and restored when the solve
-// returns (after its final stream synchronisation).
+// returns (after its final stream synchronisation).  It is a device-wide limit (include/nek.h).
 struct L2SetAside {
     size_t prev = 0;
     bool on = false;
@@ -453,73 +545,93 @@ static int ensure_dinv(nek_ctx *ctx, double h1, double h2)
     return NEK_OK;
 }
 
+// Peer mappings of the mailbox, the halo receive buffer and the halo flags.  Each rank publishes one
+// record -- CUDA IPC handles (one process per GPU) or raw device pointers (loopback group) of those
+// buffers and of its staged send buffer, where each rank's data lands in its receive buffer, and its
+// receive-buffer half size -- then opens its peers' allocations.  Any IPC failure leaves ctx->p2p
+// false on every rank (the NCCL transport stays in use).
+struct PeerRec {
+    cudaIpcMemHandle_t h[3];
+    void *raw[4];   // mbox, recv2, hflags, sendbuf (loopback)
+    int64_t half;
+};
 
-// Exchange CUDA IPC handles of the mailbox, the halo receive buffer and the halo
-// flags (one NCCL allgather), plus where each rank's data lands in each
-// neighbour's receive buffer, then open the peers' allocations.  Any failure
-// leaves ctx->p2p false (the NCCL path stays in use).
-static int setup_p2p(nek_ctx *ctx)
+static int setup_p2p(nek_ctx *ctx, bool want_p2p)
 {
     const int P = ctx->nranks, me = ctx->rank;
     const int nn = (int)ctx->neighbors.size();
-    CK(dalloc(ctx, &ctx->mbox, (int64_t)2 * 2 * P * 4));
-    CK(cudaMemset(ctx->mbox, 0, sizeof(double) * 2 * 2 * P * 4));
-    CK(dalloc(ctx, &ctx->hflags, P));
-    CK(cudaMemset(ctx->hflags, 0, sizeof(uint64_t) * P));
-    CK(dalloc(ctx, &ctx->recv2, 2 * std::max<int64_t>(ctx->nslots, 1)));
-    CK(dalloc(ctx, &ctx->epochs, 4));
-    CK(cudaMemset(ctx->epochs, 0, sizeof(uint64_t) * 4));
-    CK(dalloc(ctx, &ctx->p2p_err, 1));
-    CK(cudaMemset(ctx->p2p_err, 0, sizeof(int)));
-    // per-rank record: 3 IPC handles, offsets of every rank's data in MY receive buffer (-1: not a
-    // neighbour), and my receive-buffer half size (the buffer is double-buffered by epoch parity)
-    const size_t rec_bytes = sizeof(cudaIpcMemHandle_t) * 3 + sizeof(int64_t) * (P + 1);
-    std::vector<unsigned char> mine(rec_bytes, 0), all(rec_bytes * P, 0);
-    cudaIpcMemHandle_t h[3];
-    if (cudaIpcGetMemHandle(&h[0], ctx->mbox) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->recv2) != cudaSuccess ||
-        cudaIpcGetMemHandle(&h[2], ctx->hflags) != cudaSuccess) {
-        cudaGetLastError();
-        return NEK_OK;   // no IPC: stay on NCCL
+    CK(cudaHostAlloc((void **)&ctx->p2p_err_host, sizeof(int), cudaHostAllocMapped));
+    *ctx->p2p_err_host = 0;
+    CK(cudaHostGetDevicePointer((void **)&ctx->p2p_err, ctx->p2p_err_host, 0));
+    if (const char *e = getenv("NEK_P2P_TIMEOUT_MS")) ctx->p2p_timeout_ns = (uint64_t)std::max(1.0, atof(e)) * 1000000ull;
+    if (want_p2p) {
+        CK(dalloc(ctx, &ctx->mbox, (int64_t)2 * 2 * P * 4));
+        CK(cudaMemset(ctx->mbox, 0, sizeof(double) * 2 * 2 * P * 4));
+        CK(dalloc(ctx, &ctx->hflags, P));
+        CK(cudaMemset(ctx->hflags, 0, sizeof(uint64_t) * P));
+        CK(dalloc(ctx, &ctx->recv2, 2 * std::max<int64_t>(ctx->nslots, 1)));
+        CK(dalloc(ctx, &ctx->epochs, 4));
+        CK(cudaMemset(ctx->epochs, 0, sizeof(uint64_t) * 4));
     }
-    std::memcpy(mine.data(), h, sizeof(h));
+    // record: PeerRec, then the offsets of every rank's data in MY receive buffer (-1: not a neighbour)
+    const size_t rec_bytes = sizeof(PeerRec) + sizeof(int64_t) * P;
+    std::vector<unsigned char> mine(rec_bytes, 0), all(rec_bytes * P, 0);
+    PeerRec R;
+    std::memset(&R, 0, sizeof(R));
+    R.raw[0] = ctx->mbox; R.raw[1] = ctx->recv2; R.raw[2] = ctx->hflags; R.raw[3] = ctx->sendbuf;
+    R.half = std::max<int64_t>(ctx->nslots, 1);
+    bool ok = true;
+    if (want_p2p && !ctx->lb &&
+        (cudaIpcGetMemHandle(&R.h[0], ctx->mbox) != cudaSuccess || cudaIpcGetMemHandle(&R.h[1], ctx->recv2) != cudaSuccess ||
+         cudaIpcGetMemHandle(&R.h[2], ctx->hflags) != cudaSuccess)) {
+        cudaGetLastError();
+        ok = false;   // no IPC: stay on NCCL (every rank must agree, below)
+    }
+    std::memcpy(mine.data(), &R, sizeof(R));
     std::vector<int64_t> offs(P, -1);   // where neighbour q's data lands in MY receive buffer
     for (int k = 0; k < nn; ++k) offs[ctx->neighbors[k]] = ctx->send_offs[k];
-    std::memcpy(mine.data() + sizeof(h), offs.data(), sizeof(int64_t) * P);
-    const int64_t my_half = std::max<int64_t>(ctx->nslots, 1);
-    std::memcpy(mine.data() + sizeof(h) + sizeof(int64_t) * P, &my_half, sizeof(int64_t));
-    unsigned char *dbuf = nullptr;
-    CK(cudaMalloc(&dbuf, rec_bytes * (P + 1)));
-    CK(cudaMemcpy(dbuf + rec_bytes * P, mine.data(), rec_bytes, cudaMemcpyHostToDevice));
-    NK(ncclAllGather(dbuf + rec_bytes * P, dbuf, rec_bytes, ncclUint8, ctx->nccl, ctx->s_main));
-    CK(cudaStreamSynchronize(ctx->s_main));
-    CK(cudaMemcpy(all.data(), dbuf, rec_bytes * P, cudaMemcpyDeviceToHost));
-    cudaFree(dbuf);
+    std::memcpy(mine.data() + sizeof(R), offs.data(), sizeof(int64_t) * P);
+    int st;
+    if ((st = coll_allgather_host(ctx, mine.data(), rec_bytes, all.data())) != NEK_OK) return st;
+    auto rec = [&](int q) { PeerRec r; std::memcpy(&r, all.data() + rec_bytes * q, sizeof(r)); return r; };
+    auto off_of = [&](int q, int p) {
+        int64_t o;
+        std::memcpy(&o, all.data() + rec_bytes * q + sizeof(PeerRec) + sizeof(int64_t) * p, sizeof(o));
+        return o;
+    };
+    if (!want_p2p) {   // staged loopback: where each neighbour keeps the slots it sends to this rank
+        ctx->lb_halo_src.assign(nn, nullptr);
+        for (int k = 0; k < nn; ++k) {
+            const int q = ctx->neighbors[k];
+            ctx->lb_halo_src[k] = static_cast<const double *>(rec(q).raw[3]) + off_of(q, me);
+        }
+        return NEK_OK;
+    }
     std::vector<double *> pm(P, nullptr), pr(P, nullptr);
     std::vector<uint64_t *> pf(P, nullptr);
-    bool ok = true;
     for (int q = 0; q < P && ok; ++q) {
         if (q == me) { pm[q] = ctx->mbox; continue; }
-        cudaIpcMemHandle_t hq[3];
-        std::memcpy(hq, all.data() + rec_bytes * q, sizeof(hq));
+        const PeerRec r = rec(q);
+        const bool nbr = std::find(ctx->neighbors.begin(), ctx->neighbors.end(), q) != ctx->neighbors.end();
+        if (ctx->lb) {   // same process, same device: the sibling's pointers as they are
+            pm[q] = (double *)r.raw[0];
+            if (nbr) { pr[q] = (double *)r.raw[1]; pf[q] = (uint64_t *)r.raw[2]; }
+            continue;
+        }
         void *p = nullptr;
-        if (cudaIpcOpenMemHandle(&p, hq[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
+        if (cudaIpcOpenMemHandle(&p, r.h[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
         ctx->ipc_opened.push_back(p); pm[q] = (double *)p;
-        bool nbr = std::find(ctx->neighbors.begin(), ctx->neighbors.end(), q) != ctx->neighbors.end();
         if (!nbr) continue;
-        if (cudaIpcOpenMemHandle(&p, hq[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
+        if (cudaIpcOpenMemHandle(&p, r.h[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
         ctx->ipc_opened.push_back(p); pr[q] = (double *)p;
-        if (cudaIpcOpenMemHandle(&p, hq[2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
+        if (cudaIpcOpenMemHandle(&p, r.h[2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = false; break; }
         ctx->ipc_opened.push_back(p); pf[q] = (uint64_t *)p;
     }
     // every rank must agree on the transport
     int okv = ok ? 1 : 0;
-    int *dok = nullptr;
-    CK(cudaMalloc(&dok, sizeof(int)));
-    CK(cudaMemcpy(dok, &okv, sizeof(int), cudaMemcpyHostToDevice));
-    NK(ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, ctx->nccl, ctx->s_main));
-    CK(cudaStreamSynchronize(ctx->s_main));
-    CK(cudaMemcpy(&okv, dok, sizeof(int), cudaMemcpyDeviceToHost));
-    cudaFree(dok);
+    std::vector<int> oks(P);
+    if ((st = coll_allgather_host(ctx, &okv, sizeof(int), oks.data())) != NEK_OK) return st;
+    for (int q = 0; q < P; ++q) okv &= oks[q];
     if (!okv) {
         cudaGetLastError();
         for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -534,11 +646,8 @@ static int setup_p2p(nek_ctx *ctx)
         const int q = ctx->neighbors[k];
         nrecv[k] = pr[q];
         nflag[k] = pf[q];
-        int64_t o, hq;
-        std::memcpy(&o, all.data() + rec_bytes * q + sizeof(h) + sizeof(int64_t) * me, sizeof(int64_t));
-        std::memcpy(&hq, all.data() + rec_bytes * q + sizeof(h) + sizeof(int64_t) * P, sizeof(int64_t));
-        roff[k] = o;
-        rhalf[k] = hq;   // the neighbour's half size, not ours
+        roff[k] = off_of(q, me);
+        rhalf[k] = rec(q).half;   // the neighbour's half size, not ours
     }
     std::vector<int32_t> slot_nbr(ctx->nslots), nbr32(ctx->neighbors.begin(), ctx->neighbors.end());
     for (int k = 0; k < nn; ++k)
@@ -593,7 +702,11 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     ctx->E = E; ctx->N = N; ctx->Nq = N + 1; ctx->P3 = ctx->Nq * ctx->Nq * ctx->Nq; ctx->n = E * ctx->P3;
     ctx->rank = comm && comm->nranks > 1 ? comm->rank : 0;
     ctx->nranks = comm && comm->nranks > 1 ? comm->nranks : 1;
-    if (parent) { ctx->rank = parent->rank; ctx->nranks = parent->nranks; }
+    if (ctx->nranks > 1 && !parent) {
+        ctx->lb = loop_group_of(comm->nccl_id);
+        if (ctx->lb && ctx->lb->nranks != ctx->nranks) return fail(ctx, NEK_EINVAL, "loopback group size != nranks");
+    }
+    if (parent) { ctx->rank = parent->rank; ctx->nranks = parent->nranks; ctx->lb = parent->lb; }
 
     // host planning (local maps + validation)
     nek_plan *p = nullptr;
@@ -611,7 +724,8 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CK(cudaStreamCreateWithPriority(&ctx->s_hi, cudaStreamNonBlocking, hi));
     }
-    for (cudaEvent_t *e : {&ctx->ev_in, &ctx->ev_out, &ctx->ev_fork, &ctx->ev_join, &ctx->ev_fork2, &ctx->ev_bnd})
+    for (cudaEvent_t *e : {&ctx->ev_in, &ctx->ev_out, &ctx->ev_fork, &ctx->ev_join, &ctx->ev_fork2, &ctx->ev_bnd,
+                           &ctx->ev_lb[0], &ctx->ev_lb[1]})
         CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     enter(ctx, stream);
 
@@ -619,7 +733,7 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         if (parent) {
             ctx->nccl = parent->nccl;
             ctx->owns_nccl = false;
-        } else {
+        } else if (!ctx->lb) {
             ncclUniqueId uid;
             std::memcpy(&uid, comm->nccl_id, 128);
             NK(ncclCommInitRank(&ctx->nccl, ctx->nranks, uid, ctx->rank));
@@ -628,23 +742,13 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         int64_t ns = nek_plan_surface_gids(p, nullptr);
         std::vector<int64_t> mine(ns);
         nek_plan_surface_gids(p, mine.data());
-        int64_t *dcnt = nullptr, *dall = nullptr, *dmine = nullptr;
-        CK(cudaMalloc(&dcnt, sizeof(int64_t) * (ctx->nranks + 1)));
-        CK(cudaMemcpy(dcnt + ctx->nranks, &ns, sizeof(int64_t), cudaMemcpyHostToDevice));
-        NK(ncclAllGather(dcnt + ctx->nranks, dcnt, 1, ncclInt64, ctx->nccl, ctx->s_main));
         std::vector<int64_t> counts(ctx->nranks);
-        CK(cudaMemcpyAsync(counts.data(), dcnt, sizeof(int64_t) * ctx->nranks, cudaMemcpyDeviceToHost, ctx->s_main));
-        CK(cudaStreamSynchronize(ctx->s_main));
+        if ((st = coll_allgather_host(ctx, &ns, sizeof(int64_t), counts.data())) != NEK_OK) return st;
         int64_t mx = 1;
         for (auto c : counts) mx = std::max(mx, c);
-        CK(cudaMalloc(&dmine, sizeof(int64_t) * mx));
-        CK(cudaMalloc(&dall, sizeof(int64_t) * mx * ctx->nranks));
-        if (ns) CK(cudaMemcpy(dmine, mine.data(), sizeof(int64_t) * ns, cudaMemcpyHostToDevice));
-        NK(ncclAllGather(dmine, dall, (size_t)mx, ncclInt64, ctx->nccl, ctx->s_main));
+        mine.resize(mx, -1);
         std::vector<int64_t> all((size_t)mx * ctx->nranks);
-        CK(cudaMemcpyAsync(all.data(), dall, sizeof(int64_t) * all.size(), cudaMemcpyDeviceToHost, ctx->s_main));
-        CK(cudaStreamSynchronize(ctx->s_main));
-        cudaFree(dcnt); cudaFree(dall); cudaFree(dmine);
+        if ((st = coll_allgather_host(ctx, mine.data(), sizeof(int64_t) * mx, all.data())) != NEK_OK) return st;
         std::vector<const int64_t *> lists(ctx->nranks);
         for (int q = 0; q < ctx->nranks; ++q) lists[q] = all.data() + (size_t)q * mx;
         st = nek_plan_set_ranks(p, ctx->rank, ctx->nranks, counts.data(), lists.data());
@@ -676,22 +780,6 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         ctx->gsc.ng = (int64_t)og.size() - 1;
         ctx->gsc.p2 = ctx->gs_p2; ctx->gsc.p4 = ctx->gs_p4; ctx->gsc.p8 = ctx->gs_p8;
         ctx->gsc.pg = ctx->gs_pg; ctx->gsc.og = ctx->gs_og;
-        // inline tables for the residual update: pair partner, or a generic run id
-        std::vector<int32_t> idx(ctx->n, -1), gp, go(1, 0);
-        for (int64_t r = 0; r < ctx->nruns; ++r) {
-            const int64_t a0 = p->offs[r], len = p->offs[r + 1] - a0;
-            if (len == 2) {
-                idx[p->perm[a0]] = p->perm[a0 + 1];
-                idx[p->perm[a0 + 1]] = p->perm[a0];
-            } else {
-                const int32_t gr = (int32_t)go.size() - 1;
-                for (int64_t c = 0; c < len; ++c) { gp.push_back(p->perm[a0 + c]); idx[p->perm[a0 + c]] = -(gr + 2); }
-                go.push_back((int32_t)gp.size());
-            }
-        }
-        CK(upload(ctx, &ctx->gsi_idx, idx)); CK(upload(ctx, &ctx->gsi_perm, gp)); CK(upload(ctx, &ctx->gsi_offs, go));
-        // off by default: measured slower (the partner gathers are dependent loads inside a
-        // streaming kernel, and miss L2 at scale); NEK_GS_INLINE=1 turns it on
         // boundary Ax + halo send beside the interior Ax (concurrent streams) pays off for small
         // per-rank problems, where the boundary launch alone would leave most SMs idle; for large
         // ones the send must not queue behind the persistent interior grid (measured)
@@ -699,8 +787,6 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         ctx->concurrent_bnd = cenv ? std::strcmp(cenv, "1") == 0 : E < 16384;
         const char *senv = getenv("NEK_BND_SPLIT");
         ctx->bnd_split = !(senv && std::strcmp(senv, "0") == 0);
-        const char *genv = getenv("NEK_GS_INLINE");
-        ctx->gs_inline = genv && std::strcmp(genv, "1") == 0;
     }
     ctx->nifc = (int64_t)p->ifc_offs.size() - 1; ctx->nifc_perm = (int64_t)p->ifc_perm.size();
     CK(upload(ctx, &ctx->ifc_perm, p->ifc_perm));
@@ -730,18 +816,12 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     ctx->n_masked = 0;
     for (auto m : p->mask) ctx->n_masked += m;
 
-    // NVLink peer-memory path: map the peers' mailbox / halo buffers (CUDA IPC)
+    // NVLink peer-memory path: map the peers' mailbox / halo buffers (CUDA IPC, or the siblings' own
+    // pointers in a loopback group); NEK_P2P=0 or a staged loopback group keeps the NCCL-path kernels
     if (ctx->nranks > 1) {
         const char *env = getenv("NEK_P2P");
-        if (!env || std::strcmp(env, "0") != 0) {
-            st = setup_p2p(ctx);
-            if (st != NEK_OK) return st;
-            // folded bookkeeping: +2% at 2 GPUs (config 2 per GPU) and parity-clean in tools/mgpu_check.py,
-            // but a sequence of projection solves (bench --gpus 2, NEXT #2 section) times out in a peer
-            // exchange with it, cause not yet found -- opt-in only (NEK_FOLD=1)
-            const char *fenv = getenv("NEK_FOLD");
-            ctx->fold = ctx->p2p && fenv && std::strcmp(fenv, "1") == 0;
-        }
+        const bool want = !(env && std::strcmp(env, "0") == 0) && !(ctx->lb && ctx->lb->transport == 1);
+        if ((st = setup_p2p(ctx, want)) != NEK_OK) return st;
     }
 
     // geometry
@@ -828,6 +908,7 @@ int nek_setup(nek_ctx **out, int64_t E, int N, const double *xyz, const int64_t 
     }
     if (st != NEK_OK) {
         g_last_error = ctx->err;
+        if (ctx->lb) ctx->lb->abort();   // the other ranks' collectives fail instead of waiting
         nek_free(ctx);
         return st;
     }
@@ -839,7 +920,11 @@ int nek_free(nek_ctx *ctx)
 {
     if (!ctx) return NEK_OK;
     cudaSetDevice(ctx->device);
-    if (ctx->s_main) cudaStreamSynchronize(ctx->s_main);
+    for (cudaStream_t st : {ctx->s_main, ctx->s_hi, ctx->s_comm})
+        if (st) cudaStreamSynchronize(st);
+    // loopback: no rank releases buffers its siblings may still write into (their kernels are done once
+    // every rank has synchronised; a failed setup aborted the group first, so this returns at once)
+    if (ctx->lb) ctx->lb->barrier();
     if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
     for (auto &t : ctx->graph_timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (void *p : {(void *)ctx->G, (void *)ctx->wJ, (void *)ctx->perm, (void *)ctx->offs, (void *)ctx->ifc_perm,
@@ -850,12 +935,12 @@ int nek_free(nek_ctx *ctx)
                     (void *)ctx->vx, (void *)ctx->vdinv, (void *)ctx->vtmp, (void *)ctx->stage_in,
                     (void *)ctx->stage_out, (void *)ctx->part, (void *)ctx->red_loc, (void *)ctx->sc,
                     (void *)ctx->counter, (void *)ctx->hist, (void *)ctx->gs_p2, (void *)ctx->gs_p4,
-                    (void *)ctx->gs_p8, (void *)ctx->gs_pg, (void *)ctx->gs_og, (void *)ctx->gsi_idx,
-                    (void *)ctx->gsi_perm, (void *)ctx->gsi_offs})
+                    (void *)ctx->gs_p8, (void *)ctx->gs_pg, (void *)ctx->gs_og})
         if (p) cudaFree(p);
     if (ctx->red_all && ctx->red_all != ctx->red_loc) cudaFree(ctx->red_all);
     for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
-    for (void *p : {(void *)ctx->mbox, (void *)ctx->d_peer_mbox, (void *)ctx->epochs, (void *)ctx->p2p_err,
+    if (ctx->p2p_err_host) cudaFreeHost(ctx->p2p_err_host);
+    for (void *p : {(void *)ctx->mbox, (void *)ctx->d_peer_mbox, (void *)ctx->epochs,
                     (void *)ctx->recv2, (void *)ctx->d_peer_recv, (void *)ctx->d_remote_off, (void *)ctx->d_send_offs,
                     (void *)ctx->d_remote_half,
                     (void *)ctx->d_slot_nbr, (void *)ctx->d_nbr, (void *)ctx->hflags, (void *)ctx->d_peer_hflags})
@@ -865,7 +950,8 @@ int nek_free(nek_ctx *ctx)
     for (auto &t : P.pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : P.free_ev) cudaEventDestroy(e);
     P.pending.clear(); P.free_ev.clear();
-    for (cudaEvent_t e : {ctx->ev_in, ctx->ev_out, ctx->ev_fork, ctx->ev_join, ctx->ev_fork2, ctx->ev_bnd})
+    for (cudaEvent_t e : {ctx->ev_in, ctx->ev_out, ctx->ev_fork, ctx->ev_join, ctx->ev_fork2, ctx->ev_bnd,
+                          ctx->ev_lb[0], ctx->ev_lb[1]})
         if (e) cudaEventDestroy(e);
     if (ctx->nccl && ctx->owns_nccl) ncclCommDestroy(ctx->nccl);
     if (ctx->owns_streams) {
@@ -885,6 +971,7 @@ int nek_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, void 
     CK(cudaSetDevice(ctx->device));
     const bool du = is_device_ptr(u), dw = is_device_ptr(w);
     int st;
+    if ((st = check_peer(ctx)) != NEK_OK) return st;
     OnCallerStream on_caller(ctx, stream);
     if (!on_caller.on) enter(ctx, stream);
     const double *ud = u;
@@ -896,6 +983,7 @@ int nek_ax(nek_ctx *ctx, double h1, double h2, const double *u, double *w, void 
     if (!dw) {
         CK(cudaMemcpyAsync(w, wd, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
         CK(cudaStreamSynchronize(ctx->s_main));
+        if ((st = check_peer(ctx)) != NEK_OK) return st;   // device-pointer calls report it at the next call
     }
     if (!on_caller.on) leave(ctx, stream);
     return NEK_OK;
@@ -908,6 +996,7 @@ int nek_gs(nek_ctx *ctx, double *v, void *stream)
     CK(cudaSetDevice(ctx->device));
     const bool dv = is_device_ptr(v);
     int st;
+    if ((st = check_peer(ctx)) != NEK_OK) return st;
     OnCallerStream on_caller(ctx, stream);
     if (!on_caller.on) enter(ctx, stream);
     double *vd = v;
@@ -920,6 +1009,7 @@ int nek_gs(nek_ctx *ctx, double *v, void *stream)
     if (!dv) {
         CK(cudaMemcpyAsync(v, vd, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, ctx->s_main));
         CK(cudaStreamSynchronize(ctx->s_main));
+        if ((st = check_peer(ctx)) != NEK_OK) return st;
     }
     if (!on_caller.on) leave(ctx, stream);
     return NEK_OK;
@@ -933,37 +1023,36 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
     int st;
     const int *done = &ctx->sc->done;
     const int nb = vec_blocks();
-    GsInline gi;
-    if (ctx->gs_inline) { gi.idx = ctx->gsi_idx; gi.perm = ctx->gsi_perm; gi.offs = ctx->gsi_offs; }
-    const GsInline *gip = ctx->gs_inline ? &gi : nullptr;
     if (use_fused(ctx) && ctx->p2p) {
         // sigma pushed by the Ax kernel, pulled by the update kernel; (rho', rr) pushed by the
         // update kernel, pulled by the bookkeeping kernel: no separate exchange launches
-        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true, ctx->gs_inline)) != NEK_OK) return st;
+        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
         const P2PMail m = mail_of(ctx);
+        if ((st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;   // loopback: every rank pushed sigma
         {
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, &m, gip, ctx->l2keep, use_fold(ctx) ? 1 : 0));
+                                       ctx->counter + 2, ctx->s_main, &m, ctx->l2keep));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
-            if (!use_fold(ctx)) {   // folded: the next Ax pulls (rho', rr) and does this bookkeeping
-                CK(launch_pcg_fin_p2p(ctx->sc, m, ctx->hist, ctx->s_main));
-                ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
-            }
+        }
+        if ((st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;   // loopback: every rank pushed (rho', rr)
+        {
+            Scope sc(ctx, CLS_VEC);
+            CK(launch_pcg_fin_p2p(ctx->sc, m, ctx->hist, ctx->s_main));
+            ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
         return NEK_OK;
     }
     if (use_fused(ctx)) {
-        // Ax prologue: p = Dinv r + beta p, x += alpha p (deferred); then w = A p, sigma; the local
-        // gather-scatter of w happens inside the residual update
-        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true, ctx->gs_inline)) != NEK_OK) return st;
+        // Ax prologue: p = Dinv r + beta p, x += alpha p (deferred); then w = A p, sigma
+        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
         if ((st = exchange_slots(ctx, 0)) != NEK_OK) return st;
         {
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, nullptr, gip, ctx->l2keep));
+                                       ctx->counter + 2, ctx->s_main, nullptr, ctx->l2keep));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
         if (ctx->nranks > 1) {
@@ -999,6 +1088,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     if (!b || !x || maxit < 0 || !(tol >= 0.0)) return fail(ctx, NEK_EINVAL, "bad b/x/maxit/tol");
     CK(cudaSetDevice(ctx->device));
     int st;
+    if ((st = check_peer(ctx)) != NEK_OK) return st;
     enter(ctx, stream);
     if ((st = ensure_dinv(ctx, h1, h2)) != NEK_OK) return st;
     if (ctx->hist_cap < maxit + 1) {
@@ -1034,7 +1124,9 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
 
     const int C = std::max(1, std::min(maxit, 10));
     const char *genv = getenv("NEK_NO_GRAPH");
-    const bool use_graph = !(genv && std::strcmp(genv, "0") != 0);
+    // loopback: the stage syncs swap events between host threads at every exchange, so the iterations
+    // are launched directly (a captured graph would freeze one set of cross-rank waits)
+    const bool use_graph = !(genv && std::strcmp(genv, "0") != 0) && !ctx->lb;
     if (use_graph && (!ctx->graph || ctx->graph_iters != C || ctx->graph_h1 != h1 || ctx->graph_h2 != h2 ||
                       ctx->graph_timing != ctx->timing)) {
         if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
@@ -1092,10 +1184,6 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
             if (H->done) break;
         }
     }
-    if (use_fused(ctx) && use_fold(ctx)) {   // bookkeeping of the last update (no Ax followed it)
-        CK(launch_pcg_fold_finish(ctx->sc, mail_of(ctx), ctx->hist, ctx->s_main));
-        ctx->stats.launches += 1;
-    }
     if (use_fused(ctx)) {   // the deferred x += alpha p of the last iteration
         CK(launch_pcg_xfinal(ctx->n, ctx->sc, ctx->vp, ctx->vx, ctx->s_main));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
@@ -1117,11 +1205,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     if (hist && H->iter >= 0)
         CK(cudaMemcpy(hist, ctx->hist, sizeof(double) * (H->iter + 1), cudaMemcpyDeviceToHost));
     if (ctx->timing) harvest_timers(ctx);
-    if (ctx->p2p) {
-        int perr = 0;
-        CK(cudaMemcpy(&perr, ctx->p2p_err, sizeof(int), cudaMemcpyDeviceToHost));
-        if (perr) return fail(ctx, NEK_ENCCL, "peer exchange timed out (a rank stopped participating)");
-    }
+    if ((st = check_peer(ctx)) != NEK_OK) return st;
     if (iters) *iters = H->iter;
     if (relres) *relres = H->bb > 0 ? std::sqrt(H->rr) / H->bb : 0.0;
     leave(ctx, stream);
@@ -1198,7 +1282,7 @@ int nek_get_stats(nek_ctx *ctx, nek_stats_t *stats, int reset)
 
 int nek_set_variant(nek_ctx *ctx, int v)
 {
-    if (!ctx || v < 0) return NEK_EINVAL;
+    if (!ctx || !ax_variant_valid(v)) return fail(ctx, NEK_EINVAL, "unknown Ax variant " + std::to_string(v));
     ctx->variant = v;
     if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
     return NEK_OK;
@@ -1215,7 +1299,7 @@ struct nek_proj {
     double *X = nullptr, *B = nullptr;          // [L][n]
     double *xbar = nullptr, *db = nullptr, *dx = nullptr, *v = nullptr, *av = nullptr, *bm = nullptr;
     double *coef = nullptr, *part = nullptr, *gath = nullptr;
-    int nblk = 296;
+    int nblk = 0;
 };
 
 // global owner-copy dot products <V_i, y> for i < l, returned on the host (rank-ordered across ranks)
@@ -1236,8 +1320,10 @@ static int proj_dots(nek_proj *P, int l, const double *V, const double *y, doubl
     if (ctx->nranks > 1) {
         CK(cudaMemcpyAsync(P->gath + (size_t)ctx->nranks * PROJ_MAX_VECTORS, out, sizeof(double) * l,
                            cudaMemcpyHostToDevice, ctx->s_main));
-        NK(ncclAllGather(P->gath + (size_t)ctx->nranks * PROJ_MAX_VECTORS, P->gath, (size_t)l, ncclDouble, ctx->nccl,
-                         ctx->s_main));
+        int st;
+        if ((st = coll_allgather_dev(ctx, P->gath + (size_t)ctx->nranks * PROJ_MAX_VECTORS, P->gath,
+                                     sizeof(double) * l, ctx->s_main)) != NEK_OK)
+            return st;
         std::vector<double> all((size_t)ctx->nranks * l);
         CK(cudaMemcpyAsync(all.data(), P->gath, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, ctx->s_main));
         CK(cudaStreamSynchronize(ctx->s_main));
@@ -1259,6 +1345,7 @@ extern "C" int nek_proj_create(nek_ctx *ctx, int max_vectors, nek_proj **out)
     nek_proj *P = new (std::nothrow) nek_proj();
     if (!P) return fail(ctx, NEK_ENOMEM, "host allocation failed");
     P->ctx = ctx; P->L = max_vectors;
+    P->nblk = 2 * device_sms();
     const int64_t n = std::max<int64_t>(ctx->n, 1);
     int st = NEK_OK;
     auto al = [&](double **p, int64_t cnt) {

@@ -302,7 +302,7 @@ static cudaError_t ax_v6_launch_f(int64_t nelem, const float *u, const float *G,
         attr = true;
     }
     const int64_t nbat = (nelem + C::EPB - 1) / C::EPB;
-    const int64_t grid = std::min<int64_t>(nbat, (int64_t)C::MINB * 148);
+    const int64_t grid = std::min<int64_t>(nbat, (int64_t)C::MINB * device_sms());
     if (grid <= 0) return cudaSuccess;
     ax_v6_kernel<NQ, HELM, false, float><<<(unsigned)grid, C::NT, C::SMEM, s>>>(
         nelem, 0, nullptr, u, G, wJ, mbits, h1, h2, w, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr,

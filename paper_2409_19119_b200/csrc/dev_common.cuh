@@ -1,0 +1,199 @@
+// dev_common.cuh -- device helpers shared by the kernel translation units (ax.cu, gs.cu, vec.cu):
+// Dirichlet/owner bit access, fixed-order block reductions, the last-CTA finish, and the NVLink
+// peer-memory primitives (release/acquire epochs, mailbox push/pull).
+//
+// All reductions are two-level and fixed-order (no floating-point atomics), so results are bitwise
+// repeatable run to run (reading 7/8).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "ax_tma.cuh"
+#include "nek_ctx.h"
+
+namespace nekb200 {
+
+__device__ __forceinline__ bool bit_of(const uint32_t *__restrict__ bits, int64_t l)
+{
+    return (__ldg(bits + (l >> 5)) >> (l & 31)) & 1u;
+}
+
+// Fixed-order block sum of v (blockDim.x a multiple of 32, <= 1024): a
+// butterfly within each warp, then warp 0 folds the per-warp sums in warp
+// order.  Deterministic; result valid in thread 0.  sred needs 32 entries.
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double block_sum(double v, double *sred)
+{
+    const int t = threadIdx.x, nw = (int)(blockDim.x >> 5);
+    v = warp_sum(v);
+    if ((t & 31) == 0) sred[t >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (t < 32) {
+        r = t < nw ? sred[t] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+// Fixed-order block sum for any blockDim.x <= 1024 (smem tree); sred needs blockDim.x entries.
+__device__ __forceinline__ double block_sum_any(double v, double *sred)
+{
+    const int t = threadIdx.x;
+    sred[t] = v;
+    __syncthreads();
+    for (int s = 512; s > 0; s >>= 1) {
+        if (s < (int)blockDim.x && t < s && t + s < (int)blockDim.x) sred[t] += sred[t + s];
+        __syncthreads();
+    }
+    double r = sred[0];
+    __syncthreads();
+    return r;
+}
+
+// ------------------------------------------------------------ peer memory
+// One process per GPU (or one context per virtual rank in the loopback group); every rank maps its
+// peers' mailbox / halo buffers and writes into them directly (NVLink, or the same device).  A value
+// block is followed by a system-scope release store of a monotonically increasing epoch; the reader
+// acquires the epoch and then reads.  All ranks run the same sequence of exchanges, so epochs agree.
+// A spin gives up after timeout_ns of %globaltimer and raises *err (a volatile store into mapped host
+// memory, visible to the host without a synchronisation): error, never a hang.
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p)
+{
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ bool wait_epoch(const uint64_t *flag, uint64_t e, int *err, uint64_t timeout_ns)
+{
+    if (ld_acquire_sys(flag) >= e) return true;
+    const uint64_t t0 = globaltimer_ns();
+    for (int it = 0;; ++it) {
+        if (ld_acquire_sys(flag) >= e) return true;
+        if (it > 64) __nanosleep(64);
+        if ((it & 255) == 0 && globaltimer_ns() - t0 > timeout_ns) break;
+    }
+    *(volatile int *)err = 1;
+    __threadfence_system();
+    return false;
+}
+
+// single thread: publish up to 3 values on `channel` to every rank (self included)
+__device__ __forceinline__ void mail_push(const P2PMail &M, int channel, double v0, double v1, double v2)
+{
+    const uint64_t e = ++M.epochs[channel];
+    const size_t base = ((size_t)channel * 2 + (e & 1)) * M.nranks;
+    for (int q = 0; q < M.nranks; ++q) {
+        double *dst = (q == M.me ? M.mbox : M.peer_mbox[q]) + (base + M.me) * 4;
+        dst[0] = v0; dst[1] = v1; dst[2] = v2;
+    }
+    __threadfence_system();
+    for (int q = 0; q < M.nranks; ++q) {
+        double *dst = (q == M.me ? M.mbox : M.peer_mbox[q]) + (base + M.me) * 4;
+        st_release_sys(reinterpret_cast<uint64_t *>(dst + 3), e);
+    }
+}
+
+// single thread: wait for the current epoch of `channel` from every rank and
+// return the rank-ordered sums of the value slots (NaN after a timeout)
+__device__ __forceinline__ void mail_pull(const P2PMail &M, int channel, double *sum3)
+{
+    const uint64_t e = *(volatile uint64_t *)&M.epochs[channel];
+    const size_t base = ((size_t)channel * 2 + (e & 1)) * M.nranks;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    bool ok = true;
+    for (int q = 0; q < M.nranks; ++q) {
+        const double *src = M.mbox + (base + q) * 4;
+        ok &= wait_epoch(reinterpret_cast<const uint64_t *>(src + 3), e, M.err, M.timeout_ns);
+        const double b0 = ((volatile const double *)src)[0], b1 = ((volatile const double *)src)[1],
+                     b2 = ((volatile const double *)src)[2];
+        if (q == 0) { a0 = b0; a1 = b1; a2 = b2; }
+        else { a0 += b0; a1 += b1; a2 += b2; }
+    }
+    if (!ok) a0 = a1 = a2 = __longlong_as_double(0x7ff8000000000000ll);
+    sum3[0] = a0; sum3[1] = a1; sum3[2] = a2;
+}
+
+// The same with the per-rank waits in parallel: called by all 32 lanes of one warp; lane q < nranks
+// acquires rank q's slot, lane 0 folds the values in rank order (the bits of mail_pull).  nranks <= 32.
+__device__ __forceinline__ void mail_pull_warp(const P2PMail &M, int channel, double *sum3)
+{
+    const int lane = threadIdx.x & 31;
+    if (M.nranks > 32) {
+        if (lane == 0) mail_pull(M, channel, sum3);
+        return;
+    }
+    const uint64_t e = *(volatile uint64_t *)&M.epochs[channel];
+    const size_t base = ((size_t)channel * 2 + (e & 1)) * M.nranks;
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    bool ok = true;
+    if (lane < M.nranks) {
+        const double *src = M.mbox + (base + lane) * 4;
+        ok = wait_epoch(reinterpret_cast<const uint64_t *>(src + 3), e, M.err, M.timeout_ns);
+        b0 = ((volatile const double *)src)[0];
+        b1 = ((volatile const double *)src)[1];
+        b2 = ((volatile const double *)src)[2];
+    }
+    const bool all_ok = __all_sync(0xffffffffu, ok);
+    double a0 = __shfl_sync(0xffffffffu, b0, 0), a1 = __shfl_sync(0xffffffffu, b1, 0),
+           a2 = __shfl_sync(0xffffffffu, b2, 0);
+    for (int q = 1; q < M.nranks; ++q) {
+        const double c0 = __shfl_sync(0xffffffffu, b0, q), c1 = __shfl_sync(0xffffffffu, b1, q),
+                     c2 = __shfl_sync(0xffffffffu, b2, q);
+        a0 += c0; a1 += c1; a2 += c2;
+    }
+    if (!all_ok) a0 = a1 = a2 = __longlong_as_double(0x7ff8000000000000ll);
+    if (lane == 0) { sum3[0] = a0; sum3[1] = a1; sum3[2] = a2; }
+}
+
+// Last CTA to finish sums part[0..count) (fixed order) into dst[0] and resets the counter.
+// ctas_total: CTAs (over one or several concurrent launches) that share `counter`.
+__device__ __forceinline__ void last_block_finish(double *part, int64_t count, double *dst, unsigned int *counter,
+                                                  double *sred, int *s_last, const P2PMail *mail = nullptr,
+                                                  unsigned int ctas_total = 0)
+{
+    if (threadIdx.x == 0) {
+        __threadfence();
+        *s_last = atomicAdd(counter, 1u) == (ctas_total ? ctas_total : gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (*s_last) {
+        __threadfence();
+        double a = 0.0;
+        for (int64_t c = threadIdx.x; c < count; c += blockDim.x) a += ((volatile double *)part)[c];
+        a = block_sum(a, sred);
+        if (threadIdx.x == 0) {
+            dst[0] = a;
+            *counter = 0u;
+            if (mail) mail_push(*mail, 0, a, 0.0, 0.0);   // sigma straight to every rank (channel 0)
+        }
+    }
+}
+
+// grid of a grid-stride kernel: enough CTAs for n items at `per` items per CTA, at most `waves` CTAs
+// per SM of the current device
+inline int stride_grid(int64_t n, int per, int waves)
+{
+    const int64_t want = (n + per - 1) / per;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)waves * device_sms()));
+}
+
+}  // namespace nekb200

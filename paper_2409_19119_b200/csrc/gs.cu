@@ -1,0 +1,341 @@
+// gs.cu -- the gather-scatter QQ^T of the hot path ("C0 continuity implies ... unit-depth
+// stencils"; reading 7): local runs, the interface partials and the halo pack/unpack of
+// the cross-GPU exchange (NCCL-staged and NVLink peer-memory forms).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
+#include "dev_common.cuh"
+
+namespace nekb200 {
+
+constexpr int GS_PPT_DEFAULT = 8;
+// One thread per run: left fold in canonical order, then broadcast.
+__global__ void gs_local_kernel(int64_t nruns, const int32_t *__restrict__ perm, const int32_t *__restrict__ offs,
+                                double *__restrict__ v, const int *done)
+{
+    if (done && *(volatile const int *)done) return;
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nruns) return;
+    const int o0 = offs[r], o1 = offs[r + 1];
+    double s = v[perm[o0]];
+    for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
+    for (int c = o0; c < o1; ++c) v[perm[c]] = s;
+}
+
+cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *offs, double *v, const int *done,
+                            cudaStream_t s)
+{
+    if (nruns <= 0) return cudaSuccess;
+    gs_local_kernel<<<(unsigned)((nruns + 255) / 256), 256, 0, s>>>(nruns, perm, offs, v, done);
+    return cudaGetLastError();
+}
+
+// Runs grouped by length (2: face, 4: edge, 8: vertex nodes of a box; anything
+// else generic), each class kept in canonical first-touch order, copies
+// ascending: the sum order of every run is unchanged (bit-exact with the
+// oracle) but fixed-length runs need no offsets and load their indices as one
+// vector (one dependent load level fewer).
+constexpr int GS_PPT = 8;   // pairs per thread (quads: GS_PPT / 2)
+
+// Each warp takes a contiguous block of runs of one class and lane l handles
+// runs l, l+32, ... of it, so every warp-wide load touches consecutive runs
+// (first-touch order keeps their copies close in memory).
+template <class T, int GS_PAIRS_PER_THREAD, int GS_QUADS_PER_THREAD>
+__device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n2, const int2 *__restrict__ p2,
+                                                int64_t n4, const int4 *__restrict__ p4, int64_t n8,
+                                                const int4 *__restrict__ p8, int64_t ng,
+                                                const int32_t *__restrict__ pg, const int32_t *__restrict__ og,
+                                                T *__restrict__ v, uint64_t pol)
+{
+    const int64_t w2 = (n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD);
+    const int64_t w4 = (n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD);
+    const int64_t w8 = (n8 + 31) / 32;
+    if (wid < w2) {
+        const int64_t r0 = wid * 32 * GS_PAIRS_PER_THREAD + lane;
+        int2 c[GS_PAIRS_PER_THREAD];
+        T a[GS_PAIRS_PER_THREAD], b[GS_PAIRS_PER_THREAD];
+#pragma unroll
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (r0 + 32 * q < n2) c[q] = tma::ldi2(p2 + r0 + 32 * q, pol);
+#pragma unroll
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
+            if (r0 + 32 * q < n2) { a[q] = tma::ld1(v + c[q].x, pol); b[q] = tma::ld1(v + c[q].y, pol); }
+#pragma unroll
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
+            if (r0 + 32 * q < n2) { const T s = a[q] + b[q]; tma::st1(v + c[q].x, s, pol); tma::st1(v + c[q].y, s, pol); }
+        return;
+    }
+    wid -= w2;
+    if (wid < w4) {
+        const int64_t r0 = wid * 32 * GS_QUADS_PER_THREAD + lane;
+        int4 c[GS_QUADS_PER_THREAD];
+        T a[GS_QUADS_PER_THREAD][4];
+#pragma unroll
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (r0 + 32 * q < n4) c[q] = tma::ldi4(p4 + r0 + 32 * q, pol);
+#pragma unroll
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
+            if (r0 + 32 * q < n4) {
+                a[q][0] = tma::ld1(v + c[q].x, pol); a[q][1] = tma::ld1(v + c[q].y, pol);
+                a[q][2] = tma::ld1(v + c[q].z, pol); a[q][3] = tma::ld1(v + c[q].w, pol);
+            }
+#pragma unroll
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
+            if (r0 + 32 * q < n4) {
+                const T s = ((a[q][0] + a[q][1]) + a[q][2]) + a[q][3];
+                tma::st1(v + c[q].x, s, pol); tma::st1(v + c[q].y, s, pol);
+                tma::st1(v + c[q].z, s, pol); tma::st1(v + c[q].w, s, pol);
+            }
+        return;
+    }
+    wid -= w4;
+    if (wid < w8) {
+        const int64_t r = wid * 32 + lane;
+        if (r >= n8) return;
+        const int4 a = p8[2 * r], b = p8[2 * r + 1];
+        const T s = ((((((v[a.x] + v[a.y]) + v[a.z]) + v[a.w]) + v[b.x]) + v[b.y]) + v[b.z]) + v[b.w];
+        v[a.x] = s; v[a.y] = s; v[a.z] = s; v[a.w] = s;
+        v[b.x] = s; v[b.y] = s; v[b.z] = s; v[b.w] = s;
+        return;
+    }
+    wid -= w8;
+    const int64_t r = wid * 32 + lane;
+    if (r < ng) {
+        const int o0 = og[r], o1 = og[r + 1];
+        T s = v[pg[o0]];
+        for (int c = o0 + 1; c < o1; ++c) s += v[pg[c]];
+        for (int c = o0; c < o1; ++c) v[pg[c]] = s;
+    }
+}
+
+template <class T, int PPT>
+__global__ void __launch_bounds__(256)
+    gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
+                      const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
+                      const int32_t *__restrict__ og, T *__restrict__ v, const int *done, int keep)
+{
+    if (done && *(volatile const int *)done) return;
+    gs_classes_body<T, PPT, PPT / 2>((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, n2, p2,
+                                     n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(keep));
+}
+
+static int64_t gs_class_warps(const GsClasses &C, int ppt)
+{
+    const int qpt = ppt > 1 ? ppt / 2 : 1;
+    return (C.n2 + 32 * ppt - 1) / (32 * ppt) + (C.n4 + 32 * qpt - 1) / (32 * qpt) + (C.n8 + 31) / 32 +
+           (C.ng + 31) / 32;
+}
+
+// local runs (warps [0, cw)) and, after them, the halo unpack (warps [cw, ...)):
+// one lane per interface run waits for this epoch's halo of every neighbour,
+// folds the contributions in rank order and writes the total to the local copies.
+template <class T, int PPT>
+__global__ void __launch_bounds__(256)
+    gs_classes_unpack_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4,
+                             int64_t n8, const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
+                             const int32_t *__restrict__ og, int64_t cw, HaloUnpack U, T *__restrict__ v,
+                             const int *done, int C_keep)
+{
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const bool skip = done && *(volatile const int *)done;
+    if (wid < cw) {
+        if (!skip) gs_classes_body<T, PPT, PPT / 2>(wid, lane, n2, p2, n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(C_keep));
+        return;
+    }
+    const uint64_t e = *(volatile const uint64_t *)(U.epochs + 2);
+    bool ok = true;
+    if (lane == 0)
+        for (int k = 0; k < U.nnbr; ++k) ok &= wait_epoch(U.hflags + U.nbr[k], e, U.err, U.timeout_ns);
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (skip) return;
+    const int64_t r = (wid - cw) * 32 + lane;
+    if (r >= U.nifc) return;
+    const T *recv = reinterpret_cast<const T *>(U.recv) + (int64_t)(e & 1) * U.half;
+    const T *partial = reinterpret_cast<const T *>(U.partial);
+    const int c0 = U.coffs[r], c1 = U.coffs[r + 1];
+    int src = U.contrib[c0];
+    T s = src < 0 ? partial[r] : ((volatile const T *)recv)[src];
+    for (int c = c0 + 1; c < c1; ++c) {
+        src = U.contrib[c];
+        s += src < 0 ? partial[r] : ((volatile const T *)recv)[src];
+    }
+    if (!ok) s = T(__longlong_as_double(0x7ff8000000000000ll));   // a neighbour timed out: NaN, not stale data
+    for (int c = U.offs[r]; c < U.offs[r + 1]; ++c) v[U.perm[c]] = s;
+}
+
+template <class T>
+cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, T *v, const int *done,
+                                     cudaStream_t s)
+{
+    const int64_t cw = gs_class_warps(C, GS_PPT), uw = (U.nifc + 31) / 32;
+    const int64_t warps = cw + std::max<int64_t>(uw, 1);   // at least one waiting warp keeps epochs in step
+    const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+    gs_classes_unpack_kernel<T, GS_PPT><<<grid, 256, 0, s>>>(C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8,
+                                                             (const int4 *)C.p8, C.ng, C.pg, C.og, cw, U, v, done, C.keep);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_gs_classes(const GsClasses &C, T *v, const int *done, cudaStream_t s)
+{
+    const int64_t warps = gs_class_warps(C, GS_PPT);
+    if (warps <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+    gs_classes_kernel<T, GS_PPT><<<grid, 256, 0, s>>>(C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8,
+                                                      (const int4 *)C.p8, C.ng, C.pg, C.og, v, done, C.keep);
+    return cudaGetLastError();
+}
+
+template <class T>
+__global__ void gs_ifc_partial_kernel(int64_t nifc, const int32_t *__restrict__ perm, const int32_t *__restrict__ offs,
+                                      const T *__restrict__ v, T *__restrict__ partial, const int *done)
+{
+    if (done && *(volatile const int *)done) return;
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nifc) return;
+    const int o0 = offs[r], o1 = offs[r + 1];
+    T s = v[perm[o0]];
+    for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
+    partial[r] = s;
+}
+
+template <class T>
+__global__ void gs_pack_kernel(int64_t nslots, const int32_t *__restrict__ send_run, const T *__restrict__ partial,
+                               T *__restrict__ sendbuf, const int *done)
+{
+    if (done && *(volatile const int *)done) return;
+    const int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sidx < nslots) sendbuf[sidx] = partial[send_run[sidx]];
+}
+
+template <class T>
+cudaError_t launch_gs_ifc_pack(int64_t nifc, const int32_t *perm, const int32_t *offs, const T *v,
+                               T *partial, int64_t nslots, const int32_t *send_run, T *sendbuf,
+                               const int *done, cudaStream_t s)
+{
+    if (nifc > 0) gs_ifc_partial_kernel<<<(unsigned)((nifc + 255) / 256), 256, 0, s>>>(nifc, perm, offs, v, partial, done);
+    if (nslots > 0) gs_pack_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, s>>>(nslots, send_run, partial, sendbuf, done);
+    return cudaGetLastError();
+}
+
+// total = fold of contributions in ascending rank order (own partial or a
+// received slot), then written to every local copy.
+template <class T>
+__global__ void gs_unpack_kernel(int64_t nifc, const int32_t *__restrict__ perm, const int32_t *__restrict__ offs,
+                                 const int32_t *__restrict__ coffs, const int32_t *__restrict__ contrib,
+                                 const T *__restrict__ partial, const T *__restrict__ recvbuf,
+                                 T *__restrict__ v, const int *done, const uint64_t *epoch, int64_t half)
+{
+    if (done && *(volatile const int *)done) return;
+    if (epoch) recvbuf += (int64_t)(*epoch & 1) * half;   // P2P: double-buffered by epoch parity
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nifc) return;
+    const int c0 = coffs[r], c1 = coffs[r + 1];
+    int src = contrib[c0];
+    T s = src < 0 ? partial[r] : recvbuf[src];
+    for (int c = c0 + 1; c < c1; ++c) {
+        src = contrib[c];
+        s += src < 0 ? partial[r] : recvbuf[src];
+    }
+    for (int c = offs[r]; c < offs[r + 1]; ++c) v[perm[c]] = s;
+}
+
+template <class T>
+cudaError_t launch_gs_ifc_unpack(int64_t nifc, const int32_t *perm, const int32_t *offs, const int32_t *coffs,
+                                 const int32_t *contrib, const T *partial, const T *recvbuf, T *v,
+                                 const int *done, cudaStream_t s, const uint64_t *epoch, int64_t half)
+{
+    if (nifc <= 0) return cudaSuccess;
+    gs_unpack_kernel<<<(unsigned)((nifc + 255) / 256), 256, 0, s>>>(nifc, perm, offs, coffs, contrib, partial,
+                                                                    recvbuf, v, done, epoch, half);
+    return cudaGetLastError();
+}
+
+// pack with the interface partials folded in (one thread per send slot; a run
+// shared with several neighbours is folded once per slot, same bits)
+template <class T>
+__global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restrict__ perm,
+                                         const int32_t *__restrict__ offs, const T *__restrict__ v,
+                                         T *__restrict__ partial, const int32_t *__restrict__ send_run,
+                                         const int32_t *__restrict__ slot_nbr, double *const *peer_recv,
+                                         const int64_t *__restrict__ remote_off, const int64_t *__restrict__ send_offs,
+                                         const int64_t *__restrict__ remote_half, int nnbr, int me,
+                                         uint64_t *const *peer_hflags, uint64_t *epochs, unsigned int *counter,
+                                         const int *done, const int4 *__restrict__ pack4)
+{
+    __shared__ int s_last;
+    const uint64_t e = epochs[2] + 1;
+    const int64_t par = (int64_t)(e & 1);   // receive half by epoch parity, in units of the NEIGHBOUR's half size
+    if (!(done && *(volatile const int *)done)) {
+        for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < nslots;
+             sidx += (int64_t)gridDim.x * blockDim.x) {
+            const int run = send_run[sidx];
+            T s;
+            const int4 c4 = pack4 ? pack4[sidx] : make_int4(-2, -1, -1, -1);
+            if (c4.x >= 0) {                     // <= 4 local copies, listed per slot (one dependent level)
+                s = v[c4.x];
+                if (c4.y >= 0) s += v[c4.y];
+                if (c4.z >= 0) s += v[c4.z];
+                if (c4.w >= 0) s += v[c4.w];
+            } else {
+                const int o0 = offs[run], o1 = offs[run + 1];
+                s = v[perm[o0]];
+                for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
+            }
+            partial[run] = s;
+            const int k = slot_nbr[sidx];
+            reinterpret_cast<T *>(peer_recv[k])[par * remote_half[k] + remote_off[k] + (sidx - send_offs[k])] = s;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        *counter = 0u;
+        epochs[2] = e;
+        __threadfence_system();
+        for (int k = 0; k < nnbr; ++k) st_release_sys(peer_hflags[k] + me, e);
+    }
+}
+
+template <class T>
+cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const T *v, T *partial,
+                                     int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
+                                     double *const *peer_recv, const int64_t *remote_off, const int64_t *send_offs,
+                                     const int64_t *remote_half, int nnbr, int me, uint64_t *const *peer_hflags,
+                                     uint64_t *epochs, unsigned int *counter, const int *done, cudaStream_t s,
+                                     const int4 *pack4)
+{
+    // latency-bound gathers (slot -> copies -> values with pack4, else slot -> run -> copies -> values)
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + 127) / 128, 16 * device_sms()));
+    gs_pack_p2p_fused_kernel<<<blocks, 128, 0, s>>>(nslots, perm, offs, v, partial, send_run, slot_nbr, peer_recv,
+                                                    remote_off, send_offs, remote_half, nnbr, me, peer_hflags, epochs,
+                                                    counter, done, pack4);
+    return cudaGetLastError();
+}
+
+// the gather-scatter family for the FP64 path and the FP32 pMG levels (NEXT #3)
+#define NEK_GS_INST(T)                                                                                          \
+    template cudaError_t launch_gs_classes<T>(const GsClasses &, T *, const int *, cudaStream_t);                \
+    template cudaError_t launch_gs_classes_unpack<T>(const GsClasses &, const HaloUnpack &, T *, const int *,   \
+                                                     cudaStream_t);                                             \
+    template cudaError_t launch_gs_ifc_pack<T>(int64_t, const int32_t *, const int32_t *, const T *, T *, int64_t, \
+                                               const int32_t *, T *, const int *, cudaStream_t);                \
+    template cudaError_t launch_gs_ifc_unpack<T>(int64_t, const int32_t *, const int32_t *, const int32_t *,    \
+                                                 const int32_t *, const T *, const T *, T *, const int *,       \
+                                                 cudaStream_t, const uint64_t *, int64_t);                      \
+    template cudaError_t launch_gs_pack_p2p_fused<T>(const int32_t *, const int32_t *, const T *, T *, int64_t,  \
+                                                     const int32_t *, const int32_t *, double *const *,         \
+                                                     const int64_t *, const int64_t *, const int64_t *, int, int, \
+                                                     uint64_t *const *, uint64_t *, unsigned int *, const int *, \
+                                                     cudaStream_t, const int4 *);
+NEK_GS_INST(double)
+NEK_GS_INST(float)
+#undef NEK_GS_INST
+
+}  // namespace nekb200

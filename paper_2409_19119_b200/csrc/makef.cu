@@ -617,7 +617,7 @@ static cudaError_t geom_launch(int64_t E, const double *xyz, double *G9, unsigne
     const size_t smem = sizeof(double) * (3 * C::SZ_U + 2 * C::SZ_A + 3 * C::SZ_AA);
     cudaError_t e = cudaFuncSetAttribute(makef_geom_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int grid = (int)std::min<int64_t>(E, 148 * 2);
+    const int grid = (int)std::min<int64_t>(E, 2 * (int64_t)device_sms());
     makef_geom_kernel<NQ><<<grid, C::NT, smem, s>>>(E, xyz, E * C::P3, G9, bad);
     return cudaGetLastError();
 }
@@ -635,7 +635,7 @@ static cudaError_t apply3_launch(int64_t E, const double *G9, const double *u0, 
         attr = true;
     }
     const int per_sm = std::max(1, std::min((int)((227 * 1024) / (smem + 1024)), 2048 / NT));
-    const int grid = (int)std::min<int64_t>(E, 148 * (int64_t)per_sm);
+    const int grid = (int)std::min<int64_t>(E, (int64_t)device_sms() * per_sm);
     makef3_kernel<NQ, NT><<<grid, NT, smem, s>>>(E, G9, u0, u1, u2, f0, f1, f2);
     return cudaGetLastError();
 }
@@ -671,7 +671,7 @@ static cudaError_t apply_launch(int64_t E, const double *G9, const double *u0, c
     }
     int per_sm = (int)((227 * 1024) / (smem + 1024));
     per_sm = std::max(1, std::min(per_sm, 2048 / C::NT));
-    const int grid = (int)std::min<int64_t>(E, 148 * (int64_t)per_sm);
+    const int grid = (int)std::min<int64_t>(E, (int64_t)device_sms() * per_sm);
     makef_kernel<NQ><<<grid, C::NT, smem, s>>>(E, G9, u0, u1, u2, f0, f1, f2);
     return cudaGetLastError();
 }
@@ -734,7 +734,7 @@ extern "C" int nek_probe_dfma_tflops(int device, double *tflops)
     if (cudaMalloc((void **)&out, sizeof(double)) != cudaSuccess) return NEK_ENOMEM;
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
-    const int grid = 148 * 8, iters = 4096;
+    const int grid = 8 * device_sms(), iters = 4096;
     dfma_probe_kernel<<<grid, 256>>>(64, 1.0, out);          // warm-up
     cudaEventRecord(a);
     dfma_probe_kernel<<<grid, 256>>>(iters, 1.0, out);

@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "loopback.h"
 #include "nek.h"
 #include "nek_plan_impl.h"
 
@@ -25,9 +26,6 @@ struct PcgScalars {
     double sigma;      // global <p, A p> of the current iteration (P2P path)
     double alpha;      // alpha of the last update whose x += alpha p is still pending (fused path)
     double beta;       // beta for the next direction update (fused path)
-    double rho_next;   // folded P2P path: rho of the current iteration (set by the Ax bookkeeping CTA)
-    int fold_ready;    // folded P2P path: 1 once an update has pushed (rho', rr) for the next Ax to pull
-    int pad_;
 };
 
 // NVLink peer mailbox of a rank: [channel][epoch parity][rank][4] doubles, slot 3 = epoch.
@@ -35,16 +33,9 @@ struct P2PMail {
     double *mbox = nullptr;               // local mailbox
     double *const *peer_mbox = nullptr;   // [nranks] (own entry = local)
     uint64_t *epochs = nullptr;
-    int *err = nullptr;
+    int *err = nullptr;                   // mapped host memory: raised on a timed-out wait
     int me = 0, nranks = 1;
-};
-
-// Gather-scatter folded into the residual update: per local point an index
-// (-1: take w as is; >= 0: partner copy of a pair run; <= -2: generic run -(id+2)
-// in perm/offs, the non-pair local runs in canonical order).
-struct GsInline {
-    const int32_t *idx = nullptr;
-    const int32_t *perm = nullptr, *offs = nullptr;
+    uint64_t timeout_ns = 0;
 };
 
 // Reduction slots (device): red_loc = this rank's partial sums, red_all = the
@@ -94,16 +85,14 @@ struct AxLaunch {
     const double *r = nullptr, *dinv = nullptr;
     const PcgScalars *sc = nullptr;
     int keep = 0;                        // L2-resident mode: bit 0 p, r, Dinv, w; bit 1 also x
-    // folded P2P bookkeeping (fused Ax v5 only): bit 0 = pull (rho', rr) of the last update from the
-    // mailbox at entry and take beta from it; bit 1 = this launch's CTA 0 also does the bookkeeping
-    int fold = 0;
-    double *hist = nullptr;
     int64_t grid = 0;                    // > 0: CTAs of this launch (v5), else ax_grid
+    int variant = -1;                    // >= 0: the Ax variant of this launch (overrides the context's)
 };
 cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
                       const uint32_t *mbits, double h1, double h2, double *w, cudaStream_t s, int *nlaunch);
 int64_t ax_grid(int variant, int N, int64_t nelem);      // partial slots one launch writes
-bool ax_has_fold(int variant, int N);
+bool ax_variant_valid(int variant);
+int ax_concrete_variant(int variant, int N, int64_t nelem);   // the configuration variant 0 picks for nelem
 int ax_effective_variant(int variant, int N, bool fused, int keep);
 int ax_partials_needed(int variant, int N, int64_t E);
 // FP32 operator (v6, N <= 9): Gf is [E][ax_gstride_f(N)] (6 planes, padded to 16 bytes per element)
@@ -142,10 +131,7 @@ cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *ob
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail = nullptr, const GsInline *gi = nullptr, int keep = 0,
-                                    int fold = 0);
-// folded P2P path: the bookkeeping of the last pushed (rho', rr) when no Ax followed it
-cudaError_t launch_pcg_fold_finish(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
+                                    const P2PMail *mail = nullptr, int keep = 0);
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
 // device ranges whose L2 lines are demoted from evict_last after an L2-resident solve
 struct L2Ranges {
@@ -168,6 +154,7 @@ struct HaloUnpack {
     const uint64_t *hflags = nullptr, *epochs = nullptr;
     int nnbr = 0;
     int *err = nullptr;
+    uint64_t timeout_ns = 0;
 };
 template <class T>
 cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, T *v, const int *done,
@@ -183,8 +170,9 @@ cudaError_t launch_multiaxpy(int64_t n, int l, double a, double *y, const double
 cudaError_t launch_axpby(int64_t n, double alpha, const double *x, double beta, const double *y, double *z,
                          cudaStream_t s);
 // NVLink peer-memory exchange (CUDA IPC mappings; see kernels.cu)
-cudaError_t launch_red_exchange(int channel, int me, int nranks, const double *red_loc, double *red_all, double *mbox,
-                                double *const *peer_mbox, uint64_t *epochs, int *err, cudaStream_t s);
+// phase: 1 = push, 2 = pull, 3 = both (see vec.cu)
+cudaError_t launch_red_exchange(int channel, const P2PMail &M, const double *red_loc, double *red_all, int phase,
+                                cudaStream_t s);
 template <class T>
 cudaError_t launch_gs_pack_p2p_fused(const int32_t *perm, const int32_t *offs, const T *v, T *partial,
                                      int64_t nslots, const int32_t *send_run, const int32_t *slot_nbr,
@@ -203,6 +191,7 @@ cudaError_t launch_pcg_pupdate(int64_t n, const double *dinv, const double *r, d
                                cudaStream_t s);
 int vec_blocks();
 int upd_blocks();
+int device_sms();   // multiprocessors of the current device (cached per device)
 
 // makef.cu: dealiased advection (NEXT #4)
 int makef_lattice(int N);
@@ -252,14 +241,11 @@ struct nek_ctx {
     int32_t *perm = nullptr, *offs = nullptr;
     int64_t nruns = 0, nperm = 0;
     int32_t *gs_p2 = nullptr, *gs_p4 = nullptr, *gs_p8 = nullptr, *gs_pg = nullptr, *gs_og = nullptr;
-    int32_t *gsi_idx = nullptr, *gsi_perm = nullptr, *gsi_offs = nullptr;   // GsInline tables
-    bool gs_inline = false;
     int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
-    bool fold = false;                              // P2P: bookkeeping folded into the next Ax (no fin kernel)
     bool bnd_split = true;                          // concurrent boundary/interior Ax share one wave of CTAs
     int64_t l2_setaside = 0, l2_setaside_max = 0;   // persisting L2 bytes granted / allowed
     bool concurrent_bnd = false;
-    bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts         // NEK_CONCURRENT_BND=1: boundary Ax + send on s_hi beside the interior
+    bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts
     nekb200::GsClasses gsc;
     int32_t *ifc_perm = nullptr, *ifc_offs = nullptr, *send_run = nullptr, *coffs = nullptr, *contrib = nullptr;
     int32_t *pack4 = nullptr;   // [nslots][4] local copies of each send slot's run (-1 pad; x = -2: > 4 copies)
@@ -295,7 +281,14 @@ struct nek_ctx {
     double *mbox = nullptr;                 // [2 channels][2 parities][nranks][4]
     double **d_peer_mbox = nullptr;         // [nranks]
     uint64_t *epochs = nullptr;             // [4]: channel 0, channel 1, halo pack, halo wait
-    int *p2p_err = nullptr;
+    int *p2p_err = nullptr;                 // device view of p2p_err_host (mapped pinned host memory)
+    int *p2p_err_host = nullptr;            // raised by a timed-out peer wait; sticky (epochs are then out of step)
+    uint64_t p2p_timeout_ns = 10000000000ull;
+    // loopback group (P virtual ranks on one GPU, loopback.h)
+    nekb200::LoopGroup *lb = nullptr;
+    cudaEvent_t ev_lb[2] = {nullptr, nullptr};
+    unsigned lb_seq = 0;
+    std::vector<const double *> lb_halo_src;   // staged transport: each neighbour's send slots for this rank
     double *recv2 = nullptr;                // 2 x nslots halo receive buffer (P2P)
     double **d_peer_recv = nullptr;         // [nnbr]
     int64_t *d_remote_off = nullptr, *d_send_offs = nullptr, *d_remote_half = nullptr;

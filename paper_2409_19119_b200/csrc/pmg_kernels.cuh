@@ -93,7 +93,7 @@ cudaError_t launch_prolong_add(int64_t E, int Nc, int Nf, const T *J, const T *e
     const int a = Nc + 1, b = Nf + 1;
     const size_t smem = sizeof(T) * (256 + a * a * a + a * a * b + a * b * b);
     xfer_attr<T>();
-    const int grid = (int)std::min<int64_t>(E, 148 * 16);
+    const int grid = (int)std::min<int64_t>(E, 16 * device_sms());
     xfer_kernel<false, true, T><<<grid, XF_THREADS, smem, s>>>(E, a, b, J, ec, nullptr, uf, done);
     return cudaGetLastError();
 }
@@ -106,7 +106,7 @@ cudaError_t launch_restrict(int64_t E, int Nf, int Nc, const T *J, const T *rf, 
     const int a = Nf + 1, b = Nc + 1;
     const size_t smem = sizeof(T) * (256 + a * a * a + a * a * b + a * b * b);
     xfer_attr<T>();
-    const int grid = (int)std::min<int64_t>(E, 148 * 16);
+    const int grid = (int)std::min<int64_t>(E, 16 * device_sms());
     xfer_kernel<true, false, T><<<grid, XF_THREADS, smem, s>>>(E, a, b, J, rf, obits, fc, done);
     return cudaGetLastError();
 }
@@ -143,7 +143,7 @@ cudaError_t launch_cheb(int mode, int64_t n, const T *dinv, const T *f, const T 
                         double c2, T *d, T *x, T *r, const int *done, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 8 * device_sms()));
     cheb_kernel<T><<<grid, 256, 0, s>>>(mode, n, dinv, f, w, (T)theta, (T)c1, (T)c2, d, x, r, done);
     return cudaGetLastError();
 }
@@ -161,7 +161,7 @@ template <class Ti, class To>
 cudaError_t launch_convert(int64_t n, const Ti *in, To *out, const int *done, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 8 * device_sms()));
     convert_kernel<Ti, To><<<grid, 256, 0, s>>>(n, in, out, done);
     return cudaGetLastError();
 }
@@ -182,7 +182,7 @@ cudaError_t launch_geom_to_f32(int64_t E, int N, const double *G, float *Gf, cud
     const int P3 = (N + 1) * (N + 1) * (N + 1), gs = ax_gstride_f(N);
     const int64_t tot = E * (int64_t)gs;
     if (tot <= 0) return cudaSuccess;
-    geom_to_f32_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(E, P3, gs, G, Gf);
+    geom_to_f32_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 8 * device_sms()), 256, 0, s>>>(E, P3, gs, G, Gf);
     return cudaGetLastError();
 }
 
@@ -284,7 +284,7 @@ cudaError_t launch_lanczos_rz(int64_t n, double alpha, const double *w, const do
                               cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 8 * device_sms()));
     lanczos_rz_kernel<<<grid, 256, 0, s>>>(n, alpha, w, dinv, r, z);
     return cudaGetLastError();
 }

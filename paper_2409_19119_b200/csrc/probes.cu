@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(1024) probe_smem_kernel(int iters, double *out
 
 static int sm_count(int device)
 {
-    int sms = 148;
+    int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return sms;
 }

@@ -82,6 +82,10 @@ class nek_pmg_info_t(ctypes.Structure):
 _P, _I, _I64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 _sig = {
     "nek_version": ([], _I),
+    "nek_loopback_create": ([_I, _I, ctypes.POINTER(_P)], _I),
+    "nek_loopback_comm": ([_P, _I, ctypes.POINTER(nek_comm)], _I),
+    "nek_loopback_abort": ([_P], _I),
+    "nek_loopback_free": ([_P], _I),
     "nek_last_error": ([], ctypes.c_char_p),
     "nek_comm_unique_id": ([_P], _I),
     "nek_setup": ([ctypes.POINTER(_P), _I64, _I, _P, _P, _P, ctypes.POINTER(nek_comm), _I, _P], _I),
@@ -134,8 +138,8 @@ def _np_ptr(a):
     return ctypes.c_void_p(a.ctypes.data) if a is not None else None
 
 
-def _field_ptr(a, n, name, writable=False):
-    """(pointer, is_device, stream) of a float64 field of length n."""
+def _field_ptr(a, n, name, writable=False, device=None):
+    """(pointer, stream) of a float64 field of length n; a CUDA tensor must live on `device`."""
     if isinstance(a, np.ndarray):
         if a.dtype != np.float64 or a.size != n or not a.flags.c_contiguous or (writable and not a.flags.writeable):
             raise ValueError(f"{name}: need a C-contiguous float64 array of {n} entries")
@@ -146,6 +150,8 @@ def _field_ptr(a, n, name, writable=False):
     if a.dtype != torch.float64 or a.numel() != n or not a.is_contiguous():
         raise ValueError(f"{name}: need a contiguous float64 tensor of {n} entries")
     if a.is_cuda:
+        if device is not None and a.device.index != device:
+            raise ValueError(f"{name}: tensor on cuda:{a.device.index}, context on cuda:{device}")
         return ctypes.c_void_p(a.data_ptr()), torch.cuda.current_stream(a.device).cuda_stream
     return ctypes.c_void_p(a.data_ptr()), None   # host (possibly pinned) tensor
 
@@ -191,12 +197,39 @@ def comm_from_torch(device=None):
     return (rank, world, bytes(t.cpu().numpy().tobytes()))
 
 
+class Loopback:
+    """nek_loopback_*: P virtual ranks in one process on one GPU (include/nek.h).  Drive each rank
+    from its own thread with comm=lb.comm(rank); transport 0 = peer-memory (NVLink-path) kernels,
+    1 = NCCL-path kernels around staged copies."""
+
+    def __init__(self, nranks, transport=0):
+        h = ctypes.c_void_p()
+        _check(_lib.nek_loopback_create(int(nranks), int(transport), ctypes.byref(h)))
+        self._h = h
+        self.nranks = int(nranks)
+
+    def comm(self, rank) -> "nek_comm":
+        c = nek_comm()
+        _check(_lib.nek_loopback_comm(self._h, int(rank), ctypes.byref(c)))
+        return c
+
+    def abort(self):
+        if self._h:
+            _lib.nek_loopback_abort(self._h)
+
+    def free(self):
+        if self._h:
+            _lib.nek_loopback_free(self._h)
+            self._h = None
+
+
 class Context:
     """A nek_ctx: one rank's elements, on one GPU."""
 
-    def __init__(self, handle, E, N):
+    def __init__(self, handle, E, N, device=0):
         self._h = handle
         self.E, self.N = E, N
+        self.device = device
         self.n = E * (N + 1) ** 3
 
     @property
@@ -227,7 +260,9 @@ def setup(E, N, xyz, gid, mask=None, comm=None, device=0, stream=None) -> Contex
         raise ValueError("xyz must hold 3*E*(N+1)^3 and gid E*(N+1)^3 entries")
     m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
     c = None
-    if comm is not None and comm[1] > 1:
+    if isinstance(comm, nek_comm):
+        c = comm if comm.nranks > 1 else None
+    elif comm is not None and comm[1] > 1:
         c = nek_comm()
         c.rank, c.nranks = int(comm[0]), int(comm[1])
         ctypes.memmove(c.nccl_id, bytes(comm[2]), 128)
@@ -236,28 +271,28 @@ def setup(E, N, xyz, gid, mask=None, comm=None, device=0, stream=None) -> Contex
                         ctypes.byref(c) if c is not None else None, int(device),
                         ctypes.c_void_p(stream) if stream else None)
     _check(st)
-    return Context(h, int(E), int(N))
+    return Context(h, int(E), int(N), int(device))
 
 
 def ax(ctx: Context, h1, h2, u, w):
     """nek_ax: w = M QQ^T (h1 K_L + h2 B_L) M u."""
-    pu, su = _field_ptr(u, ctx.n, "u")
-    pw, sw = _field_ptr(w, ctx.n, "w", writable=True)
+    pu, su = _field_ptr(u, ctx.n, "u", device=ctx.device)
+    pw, sw = _field_ptr(w, ctx.n, "w", writable=True, device=ctx.device)
     _check(_lib.nek_ax(ctx.handle, float(h1), float(h2), pu, pw, _stream_of(su, sw)), ctx.handle)
     return w
 
 
 def gs(ctx: Context, v):
     """nek_gs: v <- QQ^T v in place."""
-    pv, sv = _field_ptr(v, ctx.n, "v", writable=True)
+    pv, sv = _field_ptr(v, ctx.n, "v", writable=True, device=ctx.device)
     _check(_lib.nek_gs(ctx.handle, pv, _stream_of(sv)), ctx.handle)
     return v
 
 
 def pcg_solve(ctx: Context, h1, h2, b, x, tol, maxit, want_hist=False):
     """nek_pcg_solve -> (status, iters, relres, hist or None)."""
-    pb, sb = _field_ptr(b, ctx.n, "b")
-    px, sx = _field_ptr(x, ctx.n, "x", writable=True)
+    pb, sb = _field_ptr(b, ctx.n, "b", device=ctx.device)
+    px, sx = _field_ptr(x, ctx.n, "x", writable=True, device=ctx.device)
     it = ctypes.c_int(0)
     rr = ctypes.c_double(0.0)
     hist = np.zeros(int(maxit) + 1) if want_hist else None
@@ -298,7 +333,7 @@ def get_geom(ctx: Context):
 def get_dinv(ctx: Context, h1, h2, out=None):
     if out is None:
         out = np.zeros(ctx.n)
-    p, s = _field_ptr(out, ctx.n, "dinv", writable=True)
+    p, s = _field_ptr(out, ctx.n, "dinv", writable=True, device=ctx.device)
     _check(_lib.nek_get_dinv(ctx.handle, float(h1), float(h2), p, _stream_of(s)), ctx.handle)
     return out
 
@@ -329,8 +364,8 @@ class Projection:
 
     def solve(self, h1, h2, b, x, tol, maxit):
         """-> (status, iters, relres)"""
-        pb, sb = _field_ptr(b, self.ctx.n, "b")
-        px, sx = _field_ptr(x, self.ctx.n, "x", writable=True)
+        pb, sb = _field_ptr(b, self.ctx.n, "b", device=self.ctx.device)
+        px, sx = _field_ptr(x, self.ctx.n, "x", writable=True, device=self.ctx.device)
         it = ctypes.c_int(0)
         rr = ctypes.c_double(0.0)
         st = _lib.nek_proj_solve(self._h, float(h1), float(h2), pb, px, float(tol), int(maxit), ctypes.byref(it),
@@ -383,15 +418,15 @@ class PMG:
 
     def apply(self, r, z):
         """z = V(r)."""
-        pr, sr = _field_ptr(r, self.ctx.n, "r")
-        pz, sz = _field_ptr(z, self.ctx.n, "z", writable=True)
+        pr, sr = _field_ptr(r, self.ctx.n, "r", device=self.ctx.device)
+        pz, sz = _field_ptr(z, self.ctx.n, "z", writable=True, device=self.ctx.device)
         _check(_lib.nek_pmg_apply(self._h, pr, pz, _stream_of(sr, sz)), self.ctx.handle)
         return z
 
     def solve(self, b, x, tol, maxit, want_hist=False):
         """-> (status, iters, relres, hist or None)"""
-        pb, sb = _field_ptr(b, self.ctx.n, "b")
-        px, sx = _field_ptr(x, self.ctx.n, "x", writable=True)
+        pb, sb = _field_ptr(b, self.ctx.n, "b", device=self.ctx.device)
+        px, sx = _field_ptr(x, self.ctx.n, "x", writable=True, device=self.ctx.device)
         it = ctypes.c_int(0)
         rr = ctypes.c_double(0.0)
         hist = np.zeros(int(maxit) + 1) if want_hist else None
@@ -462,7 +497,7 @@ class Makef:
         ps, ss = [], []
         for a, name, wr in ((u, "u", False), (v, "v", False), (w, "w", False), (fu, "fu", True), (fv, "fv", True),
                             (fw, "fw", True)):
-            p_, s_ = _field_ptr(a, self.ctx.n, name, writable=wr)
+            p_, s_ = _field_ptr(a, self.ctx.n, name, writable=wr, device=self.ctx.device)
             ps.append(p_); ss.append(s_)
         _check(_lib.nek_makef_apply(self._h, *ps, _stream_of(*ss)), self.ctx.handle)
         return fu, fv, fw

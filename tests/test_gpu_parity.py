@@ -4,9 +4,10 @@ Tolerances (DESIGN.md "Parity bar"):
   * gather-scatter maps: byte-equal; gs values at one rank: bit-equal;
   * geometry, Ax, Jacobi diagonal: relative 1e-12 normwise (max-abs / max-abs,
     BASELINE north_star "agree to relative 1e-12", reading 16);
-  * PCG: identical iteration count (+-1) on converged solves, final x 1e-12,
-    residual history |d(||r_k||/||b||)| <= max(1e-12 max(1, h_k), 10 x the
-    oracle's own summation-order noise) on fixed windows (reading 17).
+  * PCG (reading 17): on fixed windows of <= 100 iterations |d(||r_k||/||b||)| <= 1e-12 at every k
+    (oracle.WINDOW_TOL; the measured maximum is printed) and x within 1e-12 normwise; on converged
+    solves the iteration count equal to the oracle's (+-1), final x within 1e-12, and the history
+    within max(1e-12, 10 x the oracle's own summation-order noise).
 """
 import os
 
@@ -27,6 +28,18 @@ def nek():
         pytest.skip("no CUDA device")
     from paper_2409_19119_b200 import nek as _nek
     return _nek
+
+
+WINDOW_TOL = oracle.WINDOW_TOL
+
+
+def window_check(tag, hg, ho, xg=None, xo=None):
+    """Reading 17 on a fixed window: flat 1e-12 on the ||b||-normalised history, x within 1e-12."""
+    d = float(np.abs(np.asarray(hg) - np.asarray(ho)).max())
+    xe = rel(xg, xo) if xg is not None else 0.0
+    print(f"[window] {tag}: {len(hg) - 1} it, max |d hist| = {d:.2e}, x err {xe:.2e}")
+    assert len(hg) == len(ho) and d <= WINDOW_TOL, (tag, d)
+    assert xe <= 1e-12, (tag, xe)
 
 
 def rel(a, b):
@@ -144,9 +157,7 @@ def test_pcg_fixed_window(case, nek):
     xd = torch.zeros_like(bd)
     st, it, rr, hg = nek.pcg_solve(ctx, h[0], h[1], bd, xd, 0.0, win, want_hist=True)
     assert it == ito == win and st == nek.MAXIT
-    tol = O.hist_tolerance(h[0], h[1], b, win)
-    assert np.all(np.abs(hg - ho) <= tol)
-    assert rel(xd.cpu().numpy(), xo) <= 1e-10
+    window_check(f"N={m.N} E={m.E}", hg, ho, xd.cpu().numpy(), xo)
 
 
 def test_pcg_converged_manufactured(nek):
@@ -225,12 +236,15 @@ def test_empty_mesh(nek):
 
 
 def test_config2_full_size(nek):
-    """BASELINE config 2 (16^3, N=7) at full size: Ax+gs element-by-element against
-    the oracle, bit-exact gs, and the first 10 PCG iterations' residuals."""
+    """BASELINE config 2 (16^3, N=7) at full size in the launch configuration bench.py times (default
+    variant -> the fused v5 PCG launch, L2-resident vectors, CUDA graph of 10 iterations, 100 fixed
+    iterations): Ax+gs element by element against the oracle, bit-exact gs, and the 100-iteration
+    residual history and x at the flat window bar."""
     m = mg.config_mesh(2)
     O = oracle.Oracle.from_mesh(m)
     ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
     try:
+        assert nek.get_info(ctx)["l2_keep"] > 0          # the bench's L2-resident mode
         u = mg.random_evector(m, seed=8)
         ud = torch.from_numpy(u).cuda(); wd = torch.empty_like(ud)
         nek.ax(ctx, 1.0, 0.0, ud, wd)
@@ -240,16 +254,44 @@ def test_config2_full_size(nek):
         nek.gs(ctx, v)
         torch.cuda.synchronize()
         assert np.array_equal(v.cpu().numpy(), O.gs_apply(u))
-        b = mg.smooth_field(m, seed=1)
-        _, ito, _, ho = O.pcg(1.0, 0.0, b, 0.0, 10)
+        uu, f = mg.manufactured(m)
+        b = oracle.mask(m.mask, O.gs_apply(O.wJ * f))     # the bench's manufactured right-hand side
+        xo, ito, _, ho = O.pcg(1.0, 0.0, b, 0.0, 100)
         x = torch.zeros_like(ud)
-        st, it, _, hg = nek.pcg_solve(ctx, 1.0, 0.0, torch.from_numpy(b).cuda(), x, 0.0, 10, want_hist=True)
-        assert it == 10 and np.all(np.abs(hg - ho) <= O.hist_tolerance(1.0, 0.0, b, 10))
+        st, it, _, hg = nek.pcg_solve(ctx, 1.0, 0.0, torch.from_numpy(b).cuda(), x, 0.0, 100, want_hist=True)
+        assert it == 100 and st == nek.MAXIT
+        window_check("config 2, 100 it", hg, ho, x.cpu().numpy(), xo)
     finally:
         nek.free(ctx)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
+def test_config2_converged(nek):
+    """Config 2 manufactured solve to 1e-10 (the oracle takes 665 iterations): the same
+    iteration count (+-1), x within 1e-12 normwise, history within the converged-solve bar."""
+    m = mg.config_mesh(2)
+    O = oracle.Oracle.from_mesh(m)
+    uu, f = mg.manufactured(m)
+    b = oracle.mask(m.mask, O.gs_apply(O.wJ * f))
+    xo, ito, sto, ho = O.pcg(1.0, 0.0, b, 1e-10, 2000)
+    assert sto == 0 and ito == 665
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+        st, it, _, hg = nek.pcg_solve(ctx, 1.0, 0.0, torch.from_numpy(b).cuda(), x, 1e-10, 2000, want_hist=True)
+        assert st == nek.OK and abs(it - ito) <= 1, (it, ito)
+        xe = rel(x.cpu().numpy(), xo)
+        k = min(len(hg), len(ho))
+        tol = O.hist_tolerance(1.0, 0.0, b, k - 1)
+        k = min(k, tol.size)
+        d = np.abs(hg[:k] - ho[:k])
+        print(f"[converged] config 2: {it} it (oracle {ito}), x err {xe:.2e}, max |d hist| {d.max():.2e}")
+        assert xe <= 1e-12
+        assert np.all(d <= tol[:k])
+    finally:
+        nek.free(ctx)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 8, 10, 11, 12])
 def test_ax_all_variants_N7(nek, variant):
     """Every Ax kernel variant (nek_set_variant) against the oracle, Poisson and Helmholtz."""
     m = mg.box_mesh(3, 4, 5, 7, deform="bubble")
@@ -266,7 +308,20 @@ def test_ax_all_variants_N7(nek, variant):
         _, ito, _, ho = O.pcg(1.0, 0.0, b, 0.0, 30)
         x = np.zeros(m.n_local)
         st, it, _, hg = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, 30, want_hist=True)
-        assert it == 30 and np.all(np.abs(hg - ho) <= O.hist_tolerance(1.0, 0.0, b, 30))
+        assert it == 30
+        window_check(f"variant {variant}", hg, ho)
+    finally:
+        nek.free(ctx)
+
+
+def test_unknown_variant_rejected(nek):
+    m = mg.config_mesh(1)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        for v in (2, 3, 4, 5, 6, 7, 9, 13, -1):
+            with pytest.raises(nek.NekError) as ei:
+                nek.set_variant(ctx, v)
+            assert ei.value.code == nek.EINVAL
     finally:
         nek.free(ctx)
 
@@ -294,36 +349,29 @@ def test_ax_generic_orders(nek, N, variant):
             _, ito, _, ho = O.pcg(h[0], h[1], b, 0.0, 20)
             x = np.zeros(m.n_local)
             st, it, _, hg = nek.pcg_solve(ctx, h[0], h[1], b, x, 0.0, 20, want_hist=True)
-            assert it == 20 and np.all(np.abs(hg - ho) <= O.hist_tolerance(h[0], h[1], b, 20)), h
+            assert it == 20
+            window_check(f"N={N} variant {variant} h={h}", hg, ho)
     finally:
         nek.free(ctx)
 
 
-def test_pcg_bitwise_repeatable_and_gs_inline_equivalent(nek):
-    """Two solves give identical bits; folding the gather-scatter into the residual
-    update (default) gives the same bits as the separate gs kernel (NEK_GS_INLINE=0),
-    and host-pointer and device-pointer calls agree bitwise."""
-    import os
+def test_pcg_bitwise_repeatable(nek):
+    """Two solves give identical bits, and host-pointer and device-pointer calls agree bitwise."""
     m = mg.box_mesh(6, 5, 4, 7, deform="bubble")
     b = mg.smooth_field(m, seed=7)
     outs = []
-    for inline in ("0", "1"):
-        os.environ["NEK_GS_INLINE"] = inline
-        try:
-            ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
-        finally:
-            os.environ.pop("NEK_GS_INLINE", None)
-        try:
-            bd = torch.from_numpy(b).cuda()
-            for _ in range(2):
-                xd = torch.zeros_like(bd)
-                st, it, rr, hg = nek.pcg_solve(ctx, 1.0, 0.0, bd, xd, 1e-9, 400, want_hist=True)
-                outs.append((xd.cpu().numpy(), it, hg))
-            xh = np.zeros(m.n_local)
-            st, it, rr, hh = nek.pcg_solve(ctx, 1.0, 0.0, b, xh, 1e-9, 400, want_hist=True)
-            outs.append((xh, it, hh))
-        finally:
-            nek.free(ctx)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        bd = torch.from_numpy(b).cuda()
+        for _ in range(2):
+            xd = torch.zeros_like(bd)
+            st, it, rr, hg = nek.pcg_solve(ctx, 1.0, 0.0, bd, xd, 1e-9, 400, want_hist=True)
+            outs.append((xd.cpu().numpy(), it, hg))
+        xh = np.zeros(m.n_local)
+        st, it, rr, hh = nek.pcg_solve(ctx, 1.0, 0.0, b, xh, 1e-9, 400, want_hist=True)
+        outs.append((xh, it, hh))
+    finally:
+        nek.free(ctx)
     x0, it0, h0 = outs[0]
     for x, it, h in outs[1:]:
         assert it == it0 and np.array_equal(x, x0) and np.array_equal(h, h0)
@@ -355,8 +403,8 @@ def test_rod_bundle_parity(nek, N, dirichlet):
         xo, ito, _, ho = O.pcg(h[0], h[1], b, 0.0, win)
         x = np.zeros(m.n_local)
         st, it, _, hg = nek.pcg_solve(ctx, h[0], h[1], b, x, 0.0, win, want_hist=True)
-        assert it == ito and np.all(np.abs(hg - ho) <= O.hist_tolerance(h[0], h[1], b, win))
-        assert rel(x, xo) <= 1e-9
+        assert it == ito
+        window_check(f"rod bundle N={N} {dirichlet}", hg, ho, x, xo)
     finally:
         nek.free(ctx)
 
@@ -392,7 +440,7 @@ def test_config3_full_size_sampled(nek):
     """BASELINE config 3 at full size (E = 131072, N = 7, ~45M DOF, 67M local points) on one GPU, in
     the launch configuration bench.py --mesh cfg3 times: nek_ax (Ax + gs) on a continuous field
     against the oracle run on sampled elements (the operator restricted to an element's interior nodes
-    only needs that element: rows of interior nodes are compared, normwise against ||w||), and a
+    only needs that element: its interior rows are compared, normwise per element), and a
     20-iteration PCG window against properties that hold at any size (finite, monotone A-norm-like
     decrease is not guaranteed, so: same iteration count, relres equal to the device history)."""
     m = mg.box_mesh(32, 64, 64, 7, deform="bubble", eps=0.05, dirichlet="all")
@@ -403,7 +451,6 @@ def test_config3_full_size_sampled(nek):
         nek.ax(ctx, 1.0, 0.0, u, w)
         wh = w.cpu().numpy()
         uh = u.cpu().numpy()
-        wmax = np.abs(wh).max()
         P3 = 512
         rng = np.random.default_rng(0)
         els = rng.choice(m.E, 24, replace=False)
@@ -416,7 +463,7 @@ def test_config3_full_size_sampled(nek):
             loc = e * P3 + q
             want = Os.apply(1.0, 0.0, uh[loc])          # element-interior rows need no neighbours
             got = wh[loc]
-            assert np.abs(got[inner] - want[inner]).max() <= 1e-12 * wmax     # normwise (reading 16)
+            assert rel(got[inner], want[inner]) <= 1e-12     # per element, normwise (reading 16)
         x = torch.zeros_like(u)
         u = torch.from_numpy(mg.smooth_field(m, seed=3)).cuda()
         st, it, rr, hist = nek.pcg_solve(ctx, 1.0, 0.0, u, x, 0.0, 20, want_hist=True)
@@ -455,50 +502,3 @@ def test_pcg_l2_resident_bitwise(nek, keep):
     x0, it0, h0 = res["0"]
     x1, it1, h1 = res[keep]
     assert it1 == it0 and np.array_equal(x1, x0) and np.array_equal(h1, h0)
-
-
-@pytest.mark.parametrize("env", [{"NEK_PDL": "1"}, {"NEK_GS_PPT": "1"}, {"NEK_GS_PPT": "2"}, {"NEK_UPD_TMA": "1"},
-                                 {"NEK_UPD_CFG": "8"}])
-def test_pcg_measured_alternatives(env):
-    """The kept-but-not-default launch configurations ('measured and rejected'):
-    programmatic dependent launch and gs pairs-per-thread change no arithmetic (bit-identical to the
-    default); the TMA-staged and the 8-CTA/SM residual updates sum the dot products in a different
-    (still fixed) order, so they agree with the oracle-checked default to rounding.  The switches are
-    read once per process, hence a subprocess per setting.  N = 6 with an odd element count makes
-    n_local odd (the scalar tail of the vector kernels)."""
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    import json
-    import subprocess
-    import sys
-    code = r'''
-import json, sys, numpy as np, torch
-sys.path.insert(0, %r)
-from paper_2409_19119_b200 import nek
-from workloads import meshgen as mg
-out = {}
-for (ex, ey, ez, N) in ((6, 5, 4, 7), (3, 3, 3, 6)):
-    m = mg.box_mesh(ex, ey, ez, N, deform="bubble")
-    b = torch.from_numpy(mg.smooth_field(m, seed=5)).cuda()
-    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
-    x = torch.zeros_like(b)
-    st, it, rr, h = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 1e-9, 600, want_hist=True)
-    out[str(N)] = {"it": it, "x": x.cpu().numpy().tolist(), "h": list(map(float, h))}
-    nek.free(ctx)
-print(json.dumps(out))
-''' % ROOT
-    def run(extra):
-        e = dict(os.environ)
-        e.update(extra)
-        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, timeout=600)
-        assert r.returncode == 0, r.stderr[-2000:]
-        return json.loads(r.stdout.strip().splitlines()[-1])
-    base, alt = run({}), run(env)
-    exact = "NEK_UPD_TMA" not in env and "NEK_UPD_CFG" not in env
-    for N in base:
-        xb, xa = np.array(base[N]["x"]), np.array(alt[N]["x"])
-        if exact:
-            assert alt[N]["it"] == base[N]["it"] and np.array_equal(xa, xb) and alt[N]["h"] == base[N]["h"]
-        else:
-            assert abs(alt[N]["it"] - base[N]["it"]) <= 1
-            assert np.abs(xa - xb).max() <= 1e-12 * np.abs(xb).max()

@@ -82,11 +82,33 @@ def test_manufactured_config1():
     x, it, st, hist = O.pcg(1.0, 0.0, b, 1e-10, 500)
     assert st == 0
     err = np.abs(x - u).max()
-    # survey prototype: 24 iterations, 1.54e-3 ([scratch]); we pin the
-    # discretisation error band and an iteration count close to the prototype's.
-    assert 1e-3 < err < 2.5e-3
-    assert 15 <= it <= 40
+    # SURVEY 8(c) "Whole path" pin: 24 iterations, max error 1.54e-3 (the oracle is deterministic)
+    assert it == 24
+    assert abs(err - 1.54e-3) <= 0.01 * 1.54e-3
     assert hist[0] == 1.0 and hist[-1] <= 1e-10
+
+
+def test_manufactured_8cubed_N7():
+    """8^3 elements, N = 7, bubble map, tol 1e-10 -> 336 iterations, max error 6.0e-12."""
+    m = mg.box_mesh(8, 8, 8, 7, deform="bubble", eps=0.05, dirichlet="all")
+    O = oracle.Oracle.from_mesh(m)
+    b, u = _rhs(O, m)
+    x, it, st, hist = O.pcg(1.0, 0.0, b, 1e-10, 2000)
+    assert st == 0 and it == 336
+    assert abs(np.abs(x - u).max() - 6.0e-12) <= 0.05 * 6.0e-12
+
+
+@pytest.mark.slow
+def test_manufactured_config2():
+    """config 2 (16^3, N = 7), tol 1e-10 -> 665 iterations, max error 6.4e-12,
+    ||r_100|| / ||b|| = 0.12."""
+    m = mg.config_mesh(2)
+    O = oracle.Oracle.from_mesh(m)
+    b, u = _rhs(O, m)
+    x, it, st, hist = O.pcg(1.0, 0.0, b, 1e-10, 2000)
+    assert st == 0 and it == 665
+    assert abs(np.abs(x - u).max() - 6.4e-12) <= 0.05 * 6.4e-12
+    assert abs(hist[100] - 0.12) <= 0.005
 
 
 @pytest.mark.slow
