@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pmg", action="store_true", help="skip the Jacobi vs pMG time-to-solution section")
     ap.add_argument("--no-peaks", action="store_true", help="skip the on-box peak probes")
+    ap.add_argument("--no-beyond", action="store_true", help="skip the beyond-L2 roofline point (16x16x128)")
     ap.add_argument("--variant", type=int, default=0, help="Ax kernel variant (nek_set_variant; 0 = default)")
     ap.add_argument("--mesh", default="box", choices=["box", "rod", "cfg3"],
                     help="box: 16x16xez elements per GPU (config 2 at ez=16); rod: 17x17-pin rod bundle, "
@@ -149,26 +150,50 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(mesh, iters, h2=0.0):
-    """The oracle as it stands, single-threaded C, on a bounded sample."""
+def pcg_bytes_per_local_point(info, N):
+    """Algorithmic HBM bytes per local point of one UNFUSED Jacobi-PCG iteration:
+    Ax (u, 6 metric factors, w) + gs (20 B per shared copy + 4 B per run) + the CG vector updates
+    (64 B: x, p, r, w in, x, r out...) + the direction update (32 B) -- what a plain code such as the
+    oracle moves; the fused GPU path moves 148 B."""
+    nl = info["n_local"]
+    gs = (20.0 * (info["n_perm"] + info["n_ifc_perm"]) + 4.0 * (info["n_runs"] + info["n_ifc_runs"])) / nl
+    return 64.0 + gs + 64.0 + 32.0
+
+
+def cpu_baseline(mesh, h2, info, budget_s=8.0):
+    """The oracle as it stands (plain C, Dot2 inner products) on the host cores: serial and the
+    OpenMP build over all cores of os.sched_getaffinity (same arithmetic, bitwise), median of 3
+    timings each of a bounded number of PCG iterations on the N=1 workload mesh; with the host's
+    STREAM triad (1 thread / all threads) so the oracle's own CPU roofline fraction is stated."""
     import oracle
     from workloads import meshgen as mg
-    iters = max(2, int(iters * 2097152 / mesh.n_local))     # ~10-30 s of CPU work
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     O = oracle.Oracle.from_mesh(mesh)
     b = mg.smooth_field(mesh, seed=1)
     d = O.dinv(1.0, h2)
-    t0 = time.perf_counter()
-    O.pcg(1.0, h2, b, 0.0, iters, dinv=d)
-    dt = time.perf_counter() - t0
-    return {"value": mesh.n_dof * iters / dt / 1e9, "unit": "GDOF/s", "cores": 1, "kind": "oracle",
-            "sample": f"{iters} Jacobi-PCG iterations (incl. init) on the N=1 workload mesh, plain C oracle, 1 thread",
-            "host": host_info()}
-
-
-def host_info():
-    """CPU model, cores available and a one-thread STREAM-triad figure of the host (SURVEY 8(d):
-    the CPU's own roofline for the oracle baseline)."""
-    import numpy as np
+    bpp = pcg_bytes_per_local_point(info, mesh.N)
+    res = {}
+    for omp in (False, True):
+        oracle.use_openmp(omp)
+        L = oracle.lib()
+        t0 = time.perf_counter()
+        O.pcg(1.0, h2, b, 0.0, 2, dinv=d)                     # probe: seconds per iteration
+        per_it = max((time.perf_counter() - t0) / 3.0, 1e-4)
+        iters = int(max(2, min(200, budget_s / 3.0 / per_it)))
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            O.pcg(1.0, h2, b, 0.0, iters, dinv=d)
+            ts.append(time.perf_counter() - t0)
+        dt = statistics.median(ts)
+        threads = L.or_threads()
+        triad = L.or_triad_gbps(1 << 26, 3)
+        gbps = bpp * mesh.n_local * iters / dt / 1e9
+        res["omp" if omp else "serial"] = {
+            "value": mesh.n_dof * iters / dt / 1e9, "threads": threads, "iters": iters, "median_s": dt,
+            "algorithmic_GBps": gbps, "triad_GBps": triad, "frac_of_triad": gbps / triad if triad else None}
+    oracle.use_openmp(False)
     model = None
     try:
         for line in open("/proc/cpuinfo"):
@@ -177,46 +202,120 @@ def host_info():
                 break
     except OSError:
         pass
-    n = 1 << 25                                   # 3 x 256 MiB
-    a, b, c = np.zeros(n), np.ones(n), np.full(n, 2.0)
-    best = 1e9
-    for _ in range(3):
-        t0 = time.perf_counter()
-        np.multiply(c, 3.0, out=a)
-        np.add(a, b, out=a)                       # a = b + 3 c (two passes: 5 streams of 8 B)
-        best = min(best, time.perf_counter() - t0)
-    return {"cpu_model": model, "cores_available": len(os.sched_getaffinity(0)),
-            "triad_1thread_GBps": 5 * 8 * n / best / 1e9,
-            "triad_note": "numpy a = c*3; a += b (5 x 8 B per element moved), best of 3, one thread"}
+    o = res["omp"]
+    return {"value": o["value"], "unit": "GDOF/s", "cores": o["threads"], "kind": "oracle",
+            "sample": f"{o['iters']} Jacobi-PCG iterations on the N=1 workload mesh, median of 3, plain C oracle "
+                      f"(OpenMP over elements / runs / points, {o['threads']} threads; Dot2 inner products sequential)",
+            "serial": res["serial"], "all_cores": res["omp"], "cpu_model": model, "cores_available": cores,
+            "bytes_per_local_point_per_iter": bpp,
+            "note": "algorithmic_GBps = unfused PCG bytes per local point (SURVEY 8(d)) x points x iterations / time; "
+                    "triad = a = b + 3c over 3 x 512 MiB, best of 3, the same build's threads"}
 
 
 def run_reference(args):
+    """The reference arm of this tier: the oracle as it stands, timed on the host cores (OpenMP build,
+    all cores of os.sched_getaffinity), on the same workload, metric and unit; each step a bounded
+    number of PCG iterations."""
     rank, world, _ = rank_env()
     if rank != 0:
         return 0
     mesh = make_mesh(0, 1, args.ez, args.order, args)
     import oracle
     from workloads import meshgen as mg
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    oracle.use_openmp(True)
     O = oracle.Oracle.from_mesh(mesh)
     b = mg.smooth_field(mesh, seed=1)
     d = O.dinv(1.0, args.h2)
-    it_per_step = max(1, int(10 * 2097152 / mesh.n_local))
+    t0 = time.perf_counter()
+    O.pcg(1.0, args.h2, b, 0.0, 2, dinv=d)
+    per_it = max((time.perf_counter() - t0) / 3.0, 1e-4)
+    it_per_step = int(max(1, min(args.iters, 20.0 / max(args.steps + args.warmup, 1) / per_it)))
     for _ in range(args.warmup):
         O.pcg(1.0, args.h2, b, 0.0, it_per_step, dinv=d)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         O.pcg(1.0, args.h2, b, 0.0, it_per_step, dinv=d)
     dt = time.perf_counter() - t0
+    threads = oracle.lib().or_threads()
     val = mesh.n_dof * it_per_step * args.steps / dt / 1e9
-    sample = f"{it_per_step} Jacobi-PCG iterations per step on the N=1 workload mesh, plain C oracle, 1 thread"
+    a2 = argparse.Namespace(**vars(args))
+    a2.iters = it_per_step
+    sample = (f"{it_per_step} Jacobi-PCG iterations per step (the GPU arm runs {args.iters}) on the N=1 workload "
+              f"mesh, plain C oracle, OpenMP {threads} threads")
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": val, "unit": "GDOF/s", "n_gpus": 1,
                       "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
                       "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                      "data": "synthetic", "config": {"workload": workload_name(args, 1), "E": mesh.E,
-                                                      "N": mesh.N, "n_dof": mesh.n_dof},
-                      "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": 1, "kind": "oracle", "sample": sample},
+                      "data": "synthetic", "config": {"workload": workload_name(a2, 1), "E": mesh.E,
+                                                      "N": mesh.N, "n_dof": mesh.n_dof,
+                                                      "pcg_iters_per_step": it_per_step},
+                      "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": threads, "kind": "oracle",
+                                       "sample": sample},
                       "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
     return 0
+
+
+def roofline_of(nek, ctx, info, h2, dev, flush, reps=10, pcg_iters=20):
+    """nek_ax (Ax + gs) and the per-kernel classes of a timed PCG pass on one context, against the
+    measured copy peak: algorithmic bytes per SURVEY 8(d) (Ax u + 6 factors + w [+ wJ]; gs 20 B per shared
+    copy + 4 B per run; the fused PCG Ax adds p, r, Dinv, x in and p, x out)."""
+    import torch
+    from workloads import meshgen as mg
+    stream = torch.cuda.current_stream(dev)
+    nl = info["n_local"]
+    gs_bytes = 20.0 * info["n_perm"] + 4.0 * info["n_runs"]
+    ax_bytes = 8.0 * (8 + (1 if h2 != 0.0 else 0)) * nl
+    u = torch.from_numpy(np.random.default_rng(2).standard_normal(nl)).to(dev)
+    w = torch.empty_like(u)
+    for _ in range(3):
+        nek.ax(ctx, 1.0, h2, u, w)
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nek.ax(ctx, 1.0, h2, u, w)
+        e1.record(stream)
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+    ms /= reps
+    out = {"ax_gs": {"ms_per_apply": ms, "gdof_per_s": info["n_dof"] / (ms * 1e-3) / 1e9,
+                     "algorithmic_bytes": ax_bytes + gs_bytes, "bytes_per_local_point": (ax_bytes + gs_bytes) / nl,
+                     "achieved_GBps": (ax_bytes + gs_bytes) / (ms * 1e-3) / 1e9}}
+    nek.get_stats(ctx, reset=True)
+    nek.set_timing(ctx, True)
+    b = torch.from_numpy(np.random.default_rng(3).standard_normal(nl)).to(dev)
+    x = torch.zeros_like(b)
+    nek.pcg_solve(ctx, 1.0, h2, b, x, 0.0, pcg_iters)      # capture the timing graph
+    nek.get_stats(ctx, reset=True)
+    torch.cuda.synchronize()
+    nek.pcg_solve(ctx, 1.0, h2, b, x, 0.0, pcg_iters)
+    st = nek.get_stats(ctx, reset=True)
+    nek.set_timing(ctx, False)
+    if st["ax_launches"] and st["ax_ms"] > 0:
+        per = st["ax_ms"] / st["ax_launches"]
+        byt = st["ax_bytes"] / st["ax_launches"]
+        out["pcg_ax"] = {"avg_launch_ms": per, "algorithmic_bytes_per_launch": byt,
+                         "achieved_GBps": byt / (per * 1e-3) / 1e9}
+    if st["gs_launches"] and st["gs_ms"] > 0:
+        per = st["gs_ms"] / st["gs_launches"]
+        out["gs"] = {"avg_launch_ms": per, "algorithmic_bytes_per_launch": gs_bytes,
+                     "achieved_GBps": gs_bytes / (per * 1e-3) / 1e9}
+    if st["vec_launches"] and st["vec_ms"] > 0:
+        it = max(1, pcg_iters)
+        out["vec_per_iter"] = {"ms": st["vec_ms"] / it, "algorithmic_bytes": 32.0 * nl,
+                               "achieved_GBps": 32.0 * nl / (st["vec_ms"] / it * 1e-3) / 1e9,
+                               "note": "residual update (w, r, Dinv in; r out) plus the bookkeeping kernels"}
+    return out
+
+
+def with_frac(d, peak):
+    for v in d.values():
+        if isinstance(v, dict) and "achieved_GBps" in v:
+            v["frac"] = v["achieved_GBps"] / peak
+    return d
 
 
 def main():
@@ -485,6 +584,25 @@ def main():
             peaks_box["nccl_allreduce_latency"] = lat
             peaks_box["nccl_sendrecv_GBps_rank0_to_1"] = bw
     log("peaks done")
+    # ---- beyond-L2 point (N = 1, box workload): 16 x 16 x 128 elements (11.2M DOF, vectors of 134 MB),
+    # where neither the vectors nor the metric factors fit in the L2 -- the HBM roofline proper
+    beyond = None
+    if world == 1 and args.mesh == "box" and not args.no_beyond:
+        mb = make_mesh(0, 1, 128, args.order)
+        cb = nek.setup(mb.E, mb.N, mb.xyz, mb.gid, mb.mask, device=local)
+        ib = nek.get_info(cb)
+        peak_b = 6457.1
+        try:
+            peak_b = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except Exception:
+            pass
+        beyond = with_frac(roofline_of(nek, cb, ib, args.h2, dev, flush), peak_b)
+        beyond["config"] = {"workload": f"{EX}x{EY}x128 elements, N={args.order}, bubble box", "E": mb.E,
+                            "n_dof": mb.n_dof, "n_local": mb.n_local, "l2_keep": ib["l2_keep"],
+                            "peak_GBps": peak_b}
+        nek.free(cb)
+        del mb
+    log("beyond-L2 done")
 
     # ---- max over ranks
     vals = torch.tensor([t_ms, ax_ms, e2e_s] + pm + pj + mkv, dtype=torch.float64, device=dev)
@@ -516,8 +634,6 @@ def main():
     ax_gdofs = n_dof_total * reps / (ax_ms * 1e-3) / 1e9
 
     if rank == 0:
-        P3 = (args.order + 1) ** 3
-        ax_bytes_per_elem = P3 * (8 + 48 + 8)     # u, 6 metric factors, w (Poisson: h2 = 0)
         roofline = None
         peaks = {}
         try:
@@ -526,9 +642,13 @@ def main():
             pass
         peak = peaks.get("hbm_gbs", 6650.0)
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        union = world > 1 and stats.get("axu_spans", 0) > 0 and stats.get("axu_ms", 0) > 0
         if timing and stats["ax_launches"] > 0 and stats["ax_ms"] > 0:
             per_launch_ms = stats["ax_ms"] / stats["ax_launches"]
             per_launch_bytes = stats["ax_bytes"] / stats["ax_launches"]
+            if union:   # N > 1: the boundary and interior launches overlap; bytes of both / their union time
+                per_launch_ms = stats["axu_ms"] / stats["axu_spans"]
+                per_launch_bytes = stats["ax_bytes"] / stats["axu_spans"]
             achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
             traffic = None
             try:
@@ -544,7 +664,25 @@ def main():
                         "avg_launch_ms": per_launch_ms,
                         "share_of_step": stats["ax_ms"] / kt_ms if kt_ms else None,
                         "timing": "CUDA event-record nodes around each kernel in a second pass of the same "
-                                  f"workload ({kt_steps} solves) right after the timed region"}
+                                  f"workload ({kt_steps} solves) right after the timed region"
+                                  + ("; N > 1: per operator, the union time of the concurrent boundary and "
+                                     "interior Ax launches (first start to last end) and the bytes of both"
+                                     if union else "")}
+        nl = mesh.n_local
+        gsb = 20.0 * (info["n_perm"] + info["n_ifc_perm"]) + 4.0 * (info["n_runs"] + info["n_ifc_runs"])
+        axb = 8.0 * (8 + (1 if args.h2 != 0.0 else 0)) * nl
+        ax_gs = {"gdof_per_s": ax_gdofs, "ms_per_apply": ax_ms / reps,
+                 "algorithmic_bytes_per_gpu": axb + gsb, "bytes_per_local_point": (axb + gsb) / nl,
+                 "achieved_GBps": (axb + gsb) / (ax_ms / reps * 1e-3) / 1e9,
+                 "note": "nek_ax = Ax (u, 6 metric factors, w) + local gs (20 B per shared copy + 4 B per run, "
+                         "SURVEY 8(d)) [+ halo]; L2 flushed before every apply"}
+        ax_gs["frac"] = ax_gs["achieved_GBps"] / peak
+        if timing and stats["gs_launches"] > 0 and stats["gs_ms"] > 0:
+            per = stats["gs_ms"] / stats["gs_launches"]
+            lgs = 20.0 * info["n_perm"] + 4.0 * info["n_runs"]
+            ax_gs["gs_kernel"] = {"avg_launch_ms": per, "algorithmic_bytes_per_launch": lgs,
+                                  "achieved_GBps": lgs / (per * 1e-3) / 1e9,
+                                  "frac": lgs / (per * 1e-3) / 1e9 / peak}
         out = {
             "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong" if args.mesh == "cfg3" else "weak",
@@ -558,8 +696,8 @@ def main():
                        "l2_resident": {"keep": info["l2_keep"], "setaside_bytes": info["l2_setaside"],
                                        "setaside_max": info["l2_setaside_max"]}},
             "pcg_iter_per_s": args.iters * args.steps / (t_ms * 1e-3),
-            "ax_gs": {"gdof_per_s": ax_gdofs, "ms_per_apply": ax_ms / reps,
-                      "algorithmic_GBps": (ax_bytes_per_elem * mesh.E * world / P3 * P3 + 0) * reps / (ax_ms * 1e-3) / 1e9},
+            "ax_gs": ax_gs,
+            "beyond_l2": beyond,
             "kernel_ms_per_step": ({k: stats[k] / kt_steps for k in ("ax_ms", "gs_ms", "halo_ms", "vec_ms")}
                                    if kt_ms else None),
             "gpu_launches": int(launch_stats["launches"]),
@@ -576,7 +714,7 @@ def main():
             "peaks_box": peaks_box,
         }
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(mesh, 50, args.h2)
+            out["cpu_baseline"] = cpu_baseline(mesh, args.h2, info)
         print(json.dumps(out), flush=True)
     nek.free(ctx)
     if dist:

@@ -351,6 +351,11 @@ typedef struct {
     int64_t launches;                          /* all kernels launched by the library */
     int64_t ax_elements;                       /* elements processed by Ax launches  */
     double  ax_bytes;                          /* algorithmic HBM bytes of those launches */
+    double  axu_ms;                            /* nranks > 1: device time of each operator's whole Ax phase
+                                                  (boundary launch, halo send and interior launch, which
+                                                  overlap on two streams), from its first start to its
+                                                  last end -- the union time of those launches   */
+    int64_t axu_spans;                         /* Ax phases timed in axu_ms                            */
 } nek_stats_t;
 
 int nek_set_timing(nek_ctx *ctx, int on);

@@ -20,6 +20,9 @@
  * (oracle/assemble.py) or a dense solve -- see DESIGN.md "Oracle pins".
  */
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -192,8 +195,13 @@ void or_ax_local(int64_t E, int N, const double *D, const double *G, const doubl
                  double h1, double h2, const double *u, double *w)
 {
     int Nq = N + 1, P3 = Nq * Nq * Nq;
+    /* elements are independent: the OpenMP build (bench timing only) splits the element loop over
+     * threads; every element's arithmetic is unchanged, so results are bitwise the same */
+#pragma omp parallel
+    {
     double *ur = malloc(sizeof(double) * P3), *us = malloc(sizeof(double) * P3), *ut = malloc(sizeof(double) * P3);
     double *gr = malloc(sizeof(double) * P3), *gs = malloc(sizeof(double) * P3), *gt = malloc(sizeof(double) * P3);
+#pragma omp for schedule(static)
     for (int64_t e = 0; e < E; ++e) {
         const double *ue = u + e * P3;
         const double *Ge = G + e * 6 * (int64_t)P3;
@@ -232,6 +240,7 @@ void or_ax_local(int64_t E, int N, const double *D, const double *G, const doubl
         }
     }
     free(ur); free(us); free(ut); free(gr); free(gs); free(gt);
+    }
 }
 
 /* ------------------------------------------------------- gather-scatter --- */
@@ -291,6 +300,7 @@ int64_t or_gs_map(int64_t n, const int64_t *gid, int64_t min_len,
  */
 void or_gs_apply(int64_t nruns, const int32_t *perm, const int64_t *offs, double *v)
 {
+#pragma omp parallel for schedule(static)   /* runs are disjoint */
     for (int64_t r = 0; r < nruns; ++r) {
         double s = v[perm[offs[r]]];
         for (int64_t c = offs[r] + 1; c < offs[r + 1]; ++c) s += v[perm[c]];
@@ -313,6 +323,7 @@ void or_gs_partial(int64_t nruns, const int32_t *perm, const int64_t *offs, cons
 /* or_mask: v[l] = 0 where mask[l] (reading 6). */
 void or_mask(int64_t n, const uint8_t *mask, double *v)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t l = 0; l < n; ++l) if (mask[l]) v[l] = 0.0;
 }
 
@@ -370,19 +381,42 @@ static void op_apply(const or_op *A, const double *u, double *tmp, double *w)
     or_mask(n, A->mask, w);
 }
 
-/* owner-copy inner product sum_g x_g y_g (reading 8).  Summed in ascending
- * local index; g_dot_reverse = 1 sums in descending order instead -- the same
- * mathematics with a different rounding, used only to measure the oracle's own
- * summation-order noise (reading 17). */
-static int g_dot_reverse = 0;
+/* owner-copy inner product sum_g x_g y_g (reading 8), evaluated as the Dot2 algorithm of Ogita,
+ * Rump and Oishi ("Accurate sum and dot product", SIAM J. Sci. Comput. 26, 2005, Alg. 5.3): every
+ * product is split exactly (TwoProduct via fma) and the running sum carried with its exact rounding
+ * error (TwoSum), so the result is as accurate as a twice-working-precision evaluation rounded once
+ * -- within an ulp of the exactly rounded definition for the well-conditioned sums of CG, and
+ * independent of the summation order.  g_dot_mode (test yardsticks of reading 17, never the
+ * default): 1 = the same in descending local index (order independence), 2 = plain recursive
+ * summation s += x y in ascending index -- the textbook rounding of the same inner product, whose
+ * distance from mode 0 is the drift two correct FP64 CG codes show on a converged solve. */
+static int g_dot_mode = 0;
+static void two_sum(double a, double b, double *s, double *e)
+{
+    const double x = a + b, z = x - a;
+    *e = (a - (x - z)) + (b - z);
+    *s = x;
+}
 static double dot_owner(int64_t n, const uint8_t *owner, const double *x, const double *y)
 {
-    double s = 0.0;
-    if (g_dot_reverse) { for (int64_t l = n - 1; l >= 0; --l) if (owner[l]) s += x[l] * y[l]; }
-    else { for (int64_t l = 0; l < n; ++l) if (owner[l]) s += x[l] * y[l]; }
-    return s;
+    double p = 0.0, s = 0.0;
+    if (g_dot_mode == 2) {
+        for (int64_t l = 0; l < n; ++l) if (owner[l]) p += x[l] * y[l];
+        return p;
+    }
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t l = g_dot_mode == 1 ? n - 1 - k : k;
+        if (!owner[l]) continue;
+        const double h = x[l] * y[l], r = fma(x[l], y[l], -h);   /* TwoProduct: h + r = x y exactly */
+        double q;
+        two_sum(p, h, &p, &q);
+        s += q + r;
+    }
+    return p + s;
 }
-void or_set_dot_reverse(int on) { g_dot_reverse = on; }
+void or_set_dot_mode(int mode) { g_dot_mode = mode; }
+static int g_upd_fma = 0;
+void or_set_upd_fma(int on) { g_upd_fma = on; }
 
 /*
  * or_pcg: Jacobi-preconditioned CG, Hestenes-Stiefel form, step by step as
@@ -422,12 +456,25 @@ int or_pcg(int64_t E, int N, const double *D, const double *G, const double *wJ,
         double sigma = dot_owner(n, owner, p, w);
         if (!(sigma > 0.0)) { status = -5; break; }
         double alpha = rho / sigma;
-        for (int64_t l = 0; l < n; ++l) { x[l] += alpha * p[l]; r[l] -= alpha * w[l]; }
+        if (g_upd_fma) {
+#pragma omp parallel for schedule(static)
+            for (int64_t l = 0; l < n; ++l) { x[l] = fma(alpha, p[l], x[l]); r[l] = fma(-alpha, w[l], r[l]); }
+        } else {
+#pragma omp parallel for schedule(static)
+            for (int64_t l = 0; l < n; ++l) { x[l] += alpha * p[l]; r[l] -= alpha * w[l]; }
+        }
+#pragma omp parallel for schedule(static)
         for (int64_t l = 0; l < n; ++l) z[l] = Dinv[l] * r[l];
         double rho1 = dot_owner(n, owner, r, z);
         double beta = rho1 / rho;
         rho = rho1;
-        for (int64_t l = 0; l < n; ++l) p[l] = z[l] + beta * p[l];
+        if (g_upd_fma) {
+#pragma omp parallel for schedule(static)
+            for (int64_t l = 0; l < n; ++l) p[l] = fma(beta, p[l], z[l]);
+        } else {
+#pragma omp parallel for schedule(static)
+            for (int64_t l = 0; l < n; ++l) p[l] = z[l] + beta * p[l];
+        }
     }
     *iters = k;
     free(r); free(z); free(p); free(w); free(tmp);
@@ -444,4 +491,42 @@ void or_op_apply(int64_t E, int N, const double *D, const double *G, const doubl
     double *tmp = malloc(sizeof(double) * n);
     op_apply(&A, u, tmp, w);
     free(tmp);
+}
+
+/* ---------------------------------------------------------- host probe --- */
+/* STREAM triad a = b + 3 c over n doubles, best of `reps`, in GB/s (3 x 8 B per element; the
+ * denominator of the oracle's own CPU roofline fraction).  Threads as OpenMP gives. */
+#include <time.h>
+double or_triad_gbps(int64_t n, int reps)
+{
+    double *a = malloc(sizeof(double) * n), *b = malloc(sizeof(double) * n), *c = malloc(sizeof(double) * n);
+    if (!a || !b || !c) { free(a); free(b); free(c); return 0.0; }
+#pragma omp parallel for schedule(static)
+    for (int64_t l = 0; l < n; ++l) { a[l] = 0.0; b[l] = 1.0; c[l] = 2.0; }
+    double best = 1e30;
+    for (int k = 0; k < reps; ++k) {
+        struct timespec t0, t1;
+        clock_gettime(CLOCK_MONOTONIC, &t0);
+#pragma omp parallel for schedule(static)
+        for (int64_t l = 0; l < n; ++l) a[l] = b[l] + 3.0 * c[l];
+        clock_gettime(CLOCK_MONOTONIC, &t1);
+        double dt = (t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec);
+        if (dt < best) best = dt;
+    }
+    double chk = a[n / 2];
+    free(a); free(b); free(c);
+    return chk == 7.0 ? 24.0 * (double)n / best / 1e9 : 0.0;
+}
+
+int or_threads(void)
+{
+#ifdef _OPENMP
+    int t = 1;
+#pragma omp parallel
+#pragma omp single
+    t = omp_get_num_threads();
+    return t;
+#else
+    return 1;
+#endif
 }

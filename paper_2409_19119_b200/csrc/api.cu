@@ -99,7 +99,7 @@ static cudaEvent_t take_event(nek_ctx *ctx)
     if (!P.free_ev.empty()) { cudaEvent_t e = P.free_ev.back(); P.free_ev.pop_back(); return e; }
     cudaEvent_t e; cudaEventCreate(&e); return e;
 }
-enum { CLS_AX = 0, CLS_GS = 1, CLS_HALO = 2, CLS_VEC = 3 };
+enum { CLS_AX = 0, CLS_GS = 1, CLS_HALO = 2, CLS_VEC = 3, CLS_AXU = 4 };
 struct Scope {
     nek_ctx *ctx; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
     // inside a stream capture the records must be EXTERNAL event nodes (a plain record only
@@ -127,7 +127,7 @@ struct Scope {
 static double *cls_slot(nek_ctx *ctx, int cls)
 {
     return cls == CLS_AX ? &ctx->stats.ax_ms : cls == CLS_GS ? &ctx->stats.gs_ms
-         : cls == CLS_HALO ? &ctx->stats.halo_ms : &ctx->stats.vec_ms;
+         : cls == CLS_HALO ? &ctx->stats.halo_ms : cls == CLS_AXU ? &ctx->stats.axu_ms : &ctx->stats.vec_ms;
 }
 
 // after a replay of a graph captured in timing mode (the caller synchronised the stream)
@@ -405,6 +405,9 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     }
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
     L.elist = ctx->elist;
+    {
+    Scope span(ctx, CLS_AXU);   // the whole Ax phase (both launches and the send), for the union time
+    ctx->stats.axu_spans += 1;
     if (ax_has_fused(ctx->variant, ctx->N) && ctx->p2p && !ctx->concurrent_bnd) {
         // Boundary elements, then the halo send, then the interior elements, in stream order: the
         // NVLink transfer overlaps the interior work and the send never waits for SM
@@ -445,6 +448,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
             if (push) L.mail = mail_of(ctx);
             if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         }
+    }
     }
     if (ctx->p2p) return gs_local_and_unpack_p2p(ctx, w, done);
     if ((st = do_gs_local(ctx, w, done)) != NEK_OK) return st;
@@ -849,7 +853,8 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     }
     // work vectors, reductions, scalars
     for (double **v : {&ctx->vr, &ctx->vp, &ctx->vw, &ctx->vx, &ctx->vdinv, &ctx->vtmp}) CK(dalloc(ctx, v, n));
-    ctx->npart = std::max<int64_t>(ax_partials_needed(1, N, E), std::max(2 * vec_blocks(), 2 * upd_blocks()));
+    // partial slots of (hi, lo) pairs: Ax one per CTA, the vector kernels two dots per CTA
+    ctx->npart = std::max<int64_t>(2 * (int64_t)ax_partials_needed(1, N, E), std::max(4 * vec_blocks(), 4 * upd_blocks()));
     {
         // L2-resident PCG vectors: when p, r, Dinv, w (and x) plus the gather-scatter lists fit in the
         // L2 next to the streamed metric factors (evict_first), keep them there (evict_last) across
@@ -1155,6 +1160,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
         ctx->graph_stats.halo_launches -= saved.halo_launches;
         ctx->graph_stats.vec_launches -= saved.vec_launches;
         ctx->graph_stats.ax_bytes -= saved.ax_bytes;
+        ctx->graph_stats.axu_spans -= saved.axu_spans;
         ctx->stats = saved;
         CK(cudaGraphInstantiate(&ctx->graph, g, 0));
         cudaGraphDestroy(g);
@@ -1169,6 +1175,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
             ctx->stats.launches += g.launches; ctx->stats.ax_launches += g.ax_launches;
             ctx->stats.ax_elements += g.ax_elements; ctx->stats.gs_launches += g.gs_launches;
             ctx->stats.halo_launches += g.halo_launches; ctx->stats.vec_launches += g.vec_launches;
+            ctx->stats.axu_spans += g.axu_spans;
             launched += C;
             if (ctx->timing) {   // per-kernel device time of this replay (event-record nodes)
                 CK(cudaStreamSynchronize(ctx->s_main));

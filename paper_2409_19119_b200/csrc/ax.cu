@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(NQ *NQ *v0_epb(NQ))
     if (done && *(volatile const int *)done) return;
     __shared__ double sD[NQ * NQ];
     __shared__ double sa[EPB][P2], sb[EPB][P2];
-    __shared__ double sred[P2 * EPB];
+    __shared__ double sred[2][P2 * EPB];
     const int t = threadIdx.x, g = threadIdx.y, i = t % NQ, j = t / NQ;
     const int64_t rel = (int64_t)blockIdx.x * EPB + g;
     const bool valid = rel < nelem;
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(NQ *NQ *v0_epb(NQ))
         for (int m = 0; m < NQ; ++m) rw[m] = fma(sD[k * NQ + m], gt, rw[m]);
         __syncthreads();
     }
-    double dot = 0.0;
+    double dhi = 0.0, dlo = 0.0;
     if (valid) {
 #pragma unroll
         for (int k = 0; k < NQ; ++k) {
@@ -161,34 +161,38 @@ __global__ void __launch_bounds__(NQ *NQ *v0_epb(NQ))
             if (h2 != 0.0) v = fma(h2 * wJ[l], ru[k], v);
             if (mbits && bit_of(mbits, l)) v = 0.0;
             w[l] = v;
-            dot = fma(ru[k], v, dot);
+            dd_add_prod(dhi, dlo, ru[k], v);
         }
     }
     if (part) {
-        // fixed-order CTA sum over the linear thread index
+        // fixed-order CTA sum (double-double) over the linear thread index
         const int lt = t + P2 * g, nt = P2 * EPB;
-        sred[lt] = dot;
+        sred[0][lt] = dhi;
+        sred[1][lt] = dlo;
         __syncthreads();
         for (int s2 = 512; s2 > 0; s2 >>= 1) {
-            if (s2 < nt && lt < s2 && lt + s2 < nt) sred[lt] += sred[lt + s2];
+            if (s2 < nt && lt < s2 && lt + s2 < nt) {
+                double h = sred[0][lt], lo = sred[1][lt];
+                dd_add(h, lo, sred[0][lt + s2], sred[1][lt + s2]);
+                sred[0][lt] = h;
+                sred[1][lt] = lo;
+            }
             __syncthreads();
         }
-        if (lt == 0) part[blockIdx.x] = sred[0];
+        if (lt == 0) { part[2 * blockIdx.x] = sred[0][0]; part[2 * blockIdx.x + 1] = sred[1][0]; }
     }
 }
 
-// Fixed-order reduction of count x nd partials (row-major [count][nd]) into dst[nd].
+// Fixed-order reduction of count (hi, lo) partials (part[2c], part[2c+1]) into dst[0] = hi + lo.
 __global__ void reduce_kernel(const double *__restrict__ part, int64_t count, int nd, double *__restrict__ dst,
                               const int *done)
 {
-    __shared__ double sred[1024];
+    __shared__ double sred[64];
     if (done && *(volatile const int *)done) return;
-    for (int d = 0; d < nd; ++d) {
-        double s = 0.0;
-        for (int64_t c = threadIdx.x; c < count; c += blockDim.x) s += part[c * nd + d];
-        s = block_sum(s, sred);
-        if (threadIdx.x == 0) dst[d] = s;
-    }
+    double hi = 0.0, lo = 0.0;
+    for (int64_t c = threadIdx.x; c < count; c += blockDim.x) dd_add(hi, lo, part[2 * c], part[2 * c + 1]);
+    block_sum_dd(hi, lo, sred);
+    if (threadIdx.x == 0) dst[0] = __dadd_rn(hi, lo);
 }
 
 cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst, const int *done, cudaStream_t s)
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(128, MINB)
         return;
     }
     const int kb = 2 * wq;                       // this warp's first k-slab
-    double dot = 0.0;
+    double dhi = 0.0, dlo = 0.0;
     int64_t e_next = nit > 0 ? elem_at(0) : 0;
     for (int64_t it = 0; it < nit; ++it) {
         const int64_t e = e_next;                // element list read one iteration ahead
@@ -442,13 +446,13 @@ __global__ void __launch_bounds__(128, MINB)
                 if (wd & 2u) v1 = 0.0;
             }
             tma::st2(w + l, make_double2(v0, v1), polv);
-            dot = fma(uk[kk].x, v0, dot);
-            dot = fma(uk[kk].y, v1, dot);
+            dd_add_prod(dhi, dlo, uk[kk].x, v0);
+            dd_add_prod(dhi, dlo, uk[kk].y, v1);
         }
     }
     if (part) {
-        const double sum = block_sum(dot, S.sred);
-        if (t == 0) part[part_off + blockIdx.x] = sum;
+        block_sum_dd(dhi, dlo, S.sred);
+        if (t == 0) { part[2 * (part_off + blockIdx.x)] = dhi; part[2 * (part_off + blockIdx.x) + 1] = dlo; }
         if (fin_total > 0)
             last_block_finish(part, fin_total, dst, counter, S.sred, &S.last, mail.nranks > 1 ? &mail : nullptr,
                               ctas_total);
@@ -579,6 +583,7 @@ int ax_gstride_f(int N) { return ((6 * (N + 1) * (N + 1) * (N + 1) + 3) / 4) * 4
 int ax_partials_needed(int variant, int N, int64_t E)
 {
     return (int)std::max<int64_t>(std::max<int64_t>(2 * ax_grid(variant, N, E), E), 2 * 4 * (int64_t)device_sms());
+    // (partial slots; each slot holds a (hi, lo) pair of doubles)
 }
 
 template <int NQ>
@@ -629,7 +634,7 @@ cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, co
         }
         return cudaErrorInvalidValue;
     }
-    double *part = L.part ? L.part + L.part_off : nullptr;   // v0: one partial per CTA
+    double *part = L.part ? L.part + 2 * L.part_off : nullptr;   // v0: one (hi, lo) partial per CTA
     switch (N) {
 #define NEK_CASE(NN) \
     case NN: ax_v0_launch<NN + 1>(L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w, part, L.done, s); break;

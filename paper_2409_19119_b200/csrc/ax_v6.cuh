@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(V6<NQ, T>::NT, V6<NQ, T>::MINB)
     T *UR = UP + EPB * WB;                                // [EPB][WB]  u_r, then g_r, then D_r^T g_r
     T *US = UR + EPB * WB;                                // [EPB][WB]  u_s, then g_s, then D_s^T g_s
     __shared__ uint64_t full[ST];
-    __shared__ double sred[32];
+    __shared__ double sred[64];
     __shared__ int s_last;
     const int t = threadIdx.x;
     const int b = t / P2, ij = t % P2, a = ij % NQ, c = ij / NQ;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(V6<NQ, T>::NT, V6<NQ, T>::MINB)
     };
     if (nit > 0) prefetch(0);
 
-    double dot = 0.0;
+    double dhi = 0.0, dlo = 0.0;
     for (int64_t it = 0; it < nit; ++it) {
         const int st = (int)(it % ST);
         // ---- prologue: this batch's column into registers and into UP (padded)
@@ -248,13 +248,13 @@ __global__ void __launch_bounds__(V6<NQ, T>::NT, V6<NQ, T>::MINB)
                 const int64_t l = l0 + k * P2;
                 if ((cmask >> k) & 1u) v = T(0);
                 w[l] = v;
-                dot = fma((double)uc[k], (double)v, dot);
+                dd_add_prod(dhi, dlo, (double)uc[k], (double)v);
             }
         }
     }
     if (part) {
-        const double sum = block_sum(dot, sred);
-        if (t == 0) part[part_off + blockIdx.x] = sum;
+        block_sum_dd(dhi, dlo, sred);
+        if (t == 0) { part[2 * (part_off + blockIdx.x)] = dhi; part[2 * (part_off + blockIdx.x) + 1] = dlo; }
         if (fin_total > 0)
             last_block_finish(part, fin_total, dst, counter, sred, &s_last, mail.nranks > 1 ? &mail : nullptr,
                               ctas_total);

@@ -59,6 +59,57 @@ __device__ __forceinline__ double block_sum_any(double v, double *sred)
     return r;
 }
 
+// ------------------------------------------------------- accurate dot products
+// Inner products are accumulated as unevaluated double-double sums (hi, lo): every product is split
+// exactly (TwoProduct via fma) and every addition carries its exact rounding error (TwoSum) -- the
+// Dot2 scheme of Ogita, Rump and Oishi that the oracle uses (oracle/nek_oracle.c), so the GPU's
+// reductions, in whatever tree order, agree with the oracle's to about an ulp (reading 17).
+// The cost is a few extra FP64 operations per point in bandwidth-bound kernels.
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e)
+{
+    const double x = __dadd_rn(a, b), z = __dsub_rn(x, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(x, z)), __dsub_rn(b, z));
+    s = x;
+}
+// (hi, lo) += x y
+__device__ __forceinline__ void dd_add_prod(double &hi, double &lo, double x, double y)
+{
+    const double h = __dmul_rn(x, y), r = fma(x, y, -h);
+    double e;
+    two_sum(hi, h, hi, e);
+    lo = __dadd_rn(lo, __dadd_rn(e, r));
+}
+// (hi, lo) += (bhi, blo)
+__device__ __forceinline__ void dd_add(double &hi, double &lo, double bhi, double blo)
+{
+    double e;
+    two_sum(hi, bhi, hi, e);
+    lo = __dadd_rn(__dadd_rn(lo, blo), e);
+}
+__device__ __forceinline__ void warp_sum_dd(double &hi, double &lo)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double bh = __shfl_xor_sync(0xffffffffu, hi, o), bl = __shfl_xor_sync(0xffffffffu, lo, o);
+        dd_add(hi, lo, bh, bl);
+    }
+}
+// fixed-order block sum of (hi, lo) pairs (blockDim.x a multiple of 32, <= 1024); result valid in
+// thread 0; sred needs 64 entries
+__device__ __forceinline__ void block_sum_dd(double &hi, double &lo, double *sred)
+{
+    const int t = threadIdx.x, nw = (int)(blockDim.x >> 5);
+    warp_sum_dd(hi, lo);
+    if ((t & 31) == 0) { sred[2 * (t >> 5)] = hi; sred[2 * (t >> 5) + 1] = lo; }
+    __syncthreads();
+    if (t < 32) {
+        hi = t < nw ? sred[2 * t] : 0.0;
+        lo = t < nw ? sred[2 * t + 1] : 0.0;
+        warp_sum_dd(hi, lo);
+    }
+    __syncthreads();
+}
+
 // ------------------------------------------------------------ peer memory
 // One process per GPU (or one context per virtual rank in the loopback group); every rank maps its
 // peers' mailbox / halo buffers and writes into them directly (NVLink, or the same device).  A value
@@ -164,8 +215,9 @@ __device__ __forceinline__ void mail_pull_warp(const P2PMail &M, int channel, do
     if (lane == 0) { sum3[0] = a0; sum3[1] = a1; sum3[2] = a2; }
 }
 
-// Last CTA to finish sums part[0..count) (fixed order) into dst[0] and resets the counter.
-// ctas_total: CTAs (over one or several concurrent launches) that share `counter`.
+// Last CTA to finish folds the (hi, lo) partials part[2c], part[2c+1], c < count (fixed order),
+// into dst[0] = hi + lo and resets the counter.  ctas_total: CTAs (over one or several concurrent
+// launches) that share `counter`.  sred: 64 entries.
 __device__ __forceinline__ void last_block_finish(double *part, int64_t count, double *dst, unsigned int *counter,
                                                   double *sred, int *s_last, const P2PMail *mail = nullptr,
                                                   unsigned int ctas_total = 0)
@@ -177,9 +229,11 @@ __device__ __forceinline__ void last_block_finish(double *part, int64_t count, d
     __syncthreads();
     if (*s_last) {
         __threadfence();
-        double a = 0.0;
-        for (int64_t c = threadIdx.x; c < count; c += blockDim.x) a += ((volatile double *)part)[c];
-        a = block_sum(a, sred);
+        double hi = 0.0, lo = 0.0;
+        for (int64_t c = threadIdx.x; c < count; c += blockDim.x)
+            dd_add(hi, lo, ((volatile double *)part)[2 * c], ((volatile double *)part)[2 * c + 1]);
+        block_sum_dd(hi, lo, sred);
+        const double a = __dadd_rn(hi, lo);
         if (threadIdx.x == 0) {
             dst[0] = a;
             *counter = 0u;

@@ -199,21 +199,21 @@ NEK_PMG_INST(float)
 template cudaError_t launch_convert<double, float>(int64_t, const double *, float *, const int *, cudaStream_t);
 template cudaError_t launch_convert<float, double>(int64_t, const float *, double *, const int *, cudaStream_t);
 
-// dst[0] = sum over owner copies of a[l] b[l] (fixed order: per-thread strided sums, block sums,
-// CTA partials folded by the last CTA)
+// dst[0] = sum over owner copies of a[l] b[l] (double-double: per-thread strided sums, block sums,
+// CTA (hi, lo) partials folded by the last CTA)
 __global__ void __launch_bounds__(256)
     dot_owner_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ a,
                      const double *__restrict__ b, double *__restrict__ part, double *dst, unsigned int *counter,
                      const int *__restrict__ done)
 {
-    __shared__ double sred[32];
+    __shared__ double sred[64];
     __shared__ int s_last;
     if (done && *(volatile const int *)done) return;
-    double acc = 0.0;
+    double hi = 0.0, lo = 0.0;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x)
-        if (bit_of(obits, l)) acc = fma(a[l], b[l], acc);
-    acc = block_sum(acc, sred);
-    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+        if (bit_of(obits, l)) dd_add_prod(hi, lo, a[l], b[l]);
+    block_sum_dd(hi, lo, sred);
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = hi; part[2 * blockIdx.x + 1] = lo; }
     last_block_finish(part, gridDim.x, dst, counter, sred, &s_last);
 }
 

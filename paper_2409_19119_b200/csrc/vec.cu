@@ -73,6 +73,29 @@ __device__ __forceinline__ double rank_sum(const double *red_all, int nranks, in
 }
 
 // r = M b, p = Dinv r, x = 0; [<r, Dinv r>_o, <r, r>_o] reduced by the last CTA into dst[0..1].
+// two double-double dots per CTA: part[4c .. 4c+3] = (hi0, lo0, hi1, lo1)
+__device__ __forceinline__ void store_part2(double *part, double h0, double l0, double h1, double l1, double *sred)
+{
+    block_sum_dd(h0, l0, sred);
+    block_sum_dd(h1, l1, sred);
+    if (threadIdx.x == 0) {
+        part[4 * blockIdx.x] = h0; part[4 * blockIdx.x + 1] = l0;
+        part[4 * blockIdx.x + 2] = h1; part[4 * blockIdx.x + 3] = l1;
+    }
+}
+// the fixed-order fold of the nblk CTA pairs (valid in thread 0)
+__device__ __forceinline__ void fold_part2(const double *part, int nblk, double *sred, double &a0, double &a1)
+{
+    double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
+    for (int c = threadIdx.x; c < nblk; c += blockDim.x) {
+        dd_add(h0, l0, ((volatile const double *)part)[4 * c], ((volatile const double *)part)[4 * c + 1]);
+        dd_add(h1, l1, ((volatile const double *)part)[4 * c + 2], ((volatile const double *)part)[4 * c + 3]);
+    }
+    block_sum_dd(h0, l0, sred);
+    block_sum_dd(h1, l1, sred);
+    a0 = __dadd_rn(h0, l0);
+    a1 = __dadd_rn(h1, l1);
+}
 __device__ __forceinline__ void last_block_finish2(double *part, int nblk, double *dst, unsigned int *counter,
                                                    double *sred, int *s_last)
 {
@@ -83,13 +106,8 @@ __device__ __forceinline__ void last_block_finish2(double *part, int nblk, doubl
     __syncthreads();
     if (*s_last) {
         __threadfence();
-        double a0 = 0.0, a1 = 0.0;
-        for (int c = threadIdx.x; c < nblk; c += blockDim.x) {
-            a0 += ((volatile double *)part)[2 * c];
-            a1 += ((volatile double *)part)[2 * c + 1];
-        }
-        a0 = block_sum(a0, sred);
-        a1 = block_sum(a1, sred);
+        double a0, a1;
+        fold_part2(part, nblk, sred, a0, a1);
         if (threadIdx.x == 0) { dst[0] = a0; dst[1] = a1; *counter = 0u; }
     }
 }
@@ -102,18 +120,16 @@ __global__ void __launch_bounds__(VEC_THREADS)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ int s_last;
-    double a0 = 0.0, a1 = 0.0;
+    double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x) {
         const double rv = bit_of(mbits, l) ? 0.0 : b[l];
-        const double z = dinv[l] * rv;
+        const double z = __dmul_rn(dinv[l], rv);
         r[l] = rv;
         p[l] = p_zero ? 0.0 : z;
         x[l] = 0.0;
-        if (bit_of(obits, l)) { a0 = fma(rv, z, a0); a1 = fma(rv, rv, a1); }
+        if (bit_of(obits, l)) { dd_add_prod(h0, l0, rv, z); dd_add_prod(h1, l1, rv, rv); }
     }
-    a0 = block_sum(a0, sred);
-    a1 = block_sum(a1, sred);
-    if (threadIdx.x == 0) { part[2 * blockIdx.x] = a0; part[2 * blockIdx.x + 1] = a1; }
+    store_part2(part, h0, l0, h1, l1, sred);
     last_block_finish2(part, gridDim.x, dst, counter, sred, &s_last);
 }
 
@@ -166,7 +182,7 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
         return;
     }
     const double alpha = sc->rho / sigma;
-    double a0 = 0.0, a1 = 0.0;
+    double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
     const int64_t n2 = n >> 1;
     const double2 *p2 = reinterpret_cast<const double2 *>(p), *w2 = reinterpret_cast<const double2 *>(w);
     const double2 *d2 = reinterpret_cast<const double2 *>(dinv);
@@ -191,8 +207,8 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
                 xv[q].x = fma(alpha, pv[q].x, xv[q].x); xv[q].y = fma(alpha, pv[q].y, xv[q].y);
                 rv[q].x = fma(-alpha, wv[q].x, rv[q].x); rv[q].y = fma(-alpha, wv[q].y, rv[q].y);
                 x2[h] = xv[q]; r2[h] = rv[q];
-                if (ow[q] & 1u) { a0 = fma(rv[q].x, dv[q].x * rv[q].x, a0); a1 = fma(rv[q].x, rv[q].x, a1); }
-                if (ow[q] & 2u) { a0 = fma(rv[q].y, dv[q].y * rv[q].y, a0); a1 = fma(rv[q].y, rv[q].y, a1); }
+                if (ow[q] & 1u) { dd_add_prod(h0, l0, rv[q].x, __dmul_rn(dv[q].x, rv[q].x)); dd_add_prod(h1, l1, rv[q].x, rv[q].x); }
+                if (ow[q] & 2u) { dd_add_prod(h0, l0, rv[q].y, __dmul_rn(dv[q].y, rv[q].y)); dd_add_prod(h1, l1, rv[q].y, rv[q].y); }
             }
         }
     }
@@ -201,11 +217,9 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
         x[l] = fma(alpha, p[l], x[l]);
         const double rv = fma(-alpha, w[l], r[l]);
         r[l] = rv;
-        if (bit_of(obits, l)) { a0 = fma(rv, dinv[l] * rv, a0); a1 = fma(rv, rv, a1); }
+        if (bit_of(obits, l)) { dd_add_prod(h0, l0, rv, __dmul_rn(dinv[l], rv)); dd_add_prod(h1, l1, rv, rv); }
     }
-    a0 = block_sum(a0, sred);
-    a1 = block_sum(a1, sred);
-    if (threadIdx.x == 0) { part[2 * blockIdx.x] = a0; part[2 * blockIdx.x + 1] = a1; }
+    store_part2(part, h0, l0, h1, l1, sred);
     last_block_finish2(part, gridDim.x, dst, counter, sred, &s_last);
 }
 
@@ -346,7 +360,7 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
         return;
     }
     const double alpha = sc->rho / sigma;
-    double a0 = 0.0, a1 = 0.0;
+    double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
     for (bool first = true; base < n2; base += (int64_t)gridDim.x * tile, first = false) {
         if (!first) load(base);
 #pragma unroll
@@ -355,8 +369,8 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
             if (h < n2) {
                 rv[q].x = fma(-alpha, wv[q].x, rv[q].x); rv[q].y = fma(-alpha, wv[q].y, rv[q].y);
                 tma::st2(r + 2 * h, rv[q], pol);
-                if (ow[q] & 1u) { a0 = fma(rv[q].x, dv[q].x * rv[q].x, a0); a1 = fma(rv[q].x, rv[q].x, a1); }
-                if (ow[q] & 2u) { a0 = fma(rv[q].y, dv[q].y * rv[q].y, a0); a1 = fma(rv[q].y, rv[q].y, a1); }
+                if (ow[q] & 1u) { dd_add_prod(h0, l0, rv[q].x, __dmul_rn(dv[q].x, rv[q].x)); dd_add_prod(h1, l1, rv[q].x, rv[q].x); }
+                if (ow[q] & 2u) { dd_add_prod(h0, l0, rv[q].y, __dmul_rn(dv[q].y, rv[q].y)); dd_add_prod(h1, l1, rv[q].y, rv[q].y); }
             }
         }
     }
@@ -364,11 +378,9 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
         const int64_t l = n - 1;
         const double rl = fma(-alpha, w[l], r[l]);
         r[l] = rl;
-        if (bit_of(obits, l)) { a0 = fma(rl, dinv[l] * rl, a0); a1 = fma(rl, rl, a1); }
+        if (bit_of(obits, l)) { dd_add_prod(h0, l0, rl, __dmul_rn(dinv[l], rl)); dd_add_prod(h1, l1, rl, rl); }
     }
-    a0 = block_sum(a0, sred);
-    a1 = block_sum(a1, sred);
-    if (threadIdx.x == 0) { part[2 * blockIdx.x] = a0; part[2 * blockIdx.x + 1] = a1; }
+    store_part2(part, h0, l0, h1, l1, sred);
     if (threadIdx.x == 0) {
         __threadfence();
         s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
@@ -376,13 +388,8 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     __syncthreads();
     if (s_last) {
         __threadfence();
-        double b0 = 0.0, b1 = 0.0;
-        for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
-            b0 += ((volatile double *)part)[2 * c];
-            b1 += ((volatile double *)part)[2 * c + 1];
-        }
-        b0 = block_sum(b0, sred);
-        b1 = block_sum(b1, sred);
+        double b0, b1;
+        fold_part2(part, (int)gridDim.x, sred, b0, b1);
         if (threadIdx.x == 0) {
             *counter = 0u;
             if (nranks == 1) pcg_bookkeep(sc, b0, b1, alpha, hist);

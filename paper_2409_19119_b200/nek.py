@@ -59,7 +59,8 @@ class nek_stats_t(ctypes.Structure):
     _fields_ = [("ax_ms", ctypes.c_double), ("gs_ms", ctypes.c_double), ("halo_ms", ctypes.c_double),
                 ("vec_ms", ctypes.c_double), ("ax_launches", ctypes.c_int64), ("gs_launches", ctypes.c_int64),
                 ("halo_launches", ctypes.c_int64), ("vec_launches", ctypes.c_int64), ("launches", ctypes.c_int64),
-                ("ax_elements", ctypes.c_int64), ("ax_bytes", ctypes.c_double)]
+                ("ax_elements", ctypes.c_int64), ("ax_bytes", ctypes.c_double), ("axu_ms", ctypes.c_double),
+                ("axu_spans", ctypes.c_int64)]
 
 
 PMG_MAX_LEVELS = 8

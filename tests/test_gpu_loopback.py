@@ -8,9 +8,9 @@ and split-wave kernels as one-process-per-GPU ranks (transport 0 = the NVLink pe
   * gs: every rank's result bit-equal to the oracle's multi-rank emulation (reading 7), and the
     copies of a node bit-identical across ranks;
   * Ax (+ gs + halo): relative 1e-12 normwise against the single-rank oracle;
-  * PCG over a fixed window: |d(||r_k||/||b||)| <= 1e-12 at every k against the single-rank oracle
-    (reading 17: the rank-ordered partial sums only re-associate the inner products), every rank
-    holding the same history bits; x within 1e-12 normwise;
+  * PCG over a fixed window: |d ||r_k||| <= 1e-12 max(||b||, ||r_k||) at every k against the
+    single-rank oracle (reading 17: the rank-ordered partial sums only re-associate the inner
+    products), every rank holding the same history bits; x within 1e-12 normwise;
   * both Ax orderings (boundary / interior on concurrent streams with the split wave, and in
     stream order), slab partitions P = 2, 3 and a 2x2x2 block partition (edges and corners).
 """
@@ -137,13 +137,13 @@ def check_multirank(nek, m, parts, transport, env, window=40, h=(1.0, 0.0), pcg_
     order = np.argsort(allg, kind="stable")
     sg, sw = allg[order], allw[order]
     assert np.all((sg[1:] != sg[:-1]) | (sw[1:] == sw[:-1]))
-    # PCG window: flat 1e-12 on the ||b||-normalised history (reading 17), same bits on every rank
+    # PCG window: WINDOW_TOL relative to max(||b||, ||r_k||) (reading 17), same bits on every rank
     xo, ito, _, ho = O.pcg(h[0], h[1], b, 0.0, window)
     h0 = res[0]["hist"]
     assert all(r_["it"] == window and r_["st"] == nek.MAXIT for r_ in res)
     assert all(np.array_equal(r_["hist"], h0) for r_ in res)
-    dmax = float(np.abs(h0 - ho).max())
-    print(f"P={P} transport={transport} env={env} N={m.N}: max |d hist| = {dmax:.2e}, "
+    dmax = oracle.window_error(h0, ho)
+    print(f"P={P} transport={transport} env={env} N={m.N}: max |d h|/max(1,h) = {dmax:.2e}, "
           f"x err {rel(xg, xo):.2e}, halo doubles {[r_['info']['halo_doubles'] for r_ in res]}")
     assert dmax <= WINDOW_TOL
     assert rel(xg, xo) <= 1e-12
