@@ -8,6 +8,7 @@
 #include <cstdlib>
 
 #include "dev_common.cuh"
+#include "gs_body.cuh"
 
 namespace nekb200 {
 
@@ -33,91 +34,14 @@ cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *o
     return cudaGetLastError();
 }
 
-// Runs grouped by length (2: face, 4: edge, 8: vertex nodes of a box; anything
-// else generic), each class kept in canonical first-touch order, copies
-// ascending: the sum order of every run is unchanged (bit-exact with the
-// oracle) but fixed-length runs need no offsets and load their indices as one
-// vector (one dependent load level fewer).
-constexpr int GS_PPT = 8;   // pairs per thread (quads: GS_PPT / 2)
-
-// Each warp takes a contiguous block of runs of one class and lane l handles
-// runs l, l+32, ... of it, so every warp-wide load touches consecutive runs
-// (first-touch order keeps their copies close in memory).
-template <class T, int GS_PAIRS_PER_THREAD, int GS_QUADS_PER_THREAD>
-__device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n2, const int2 *__restrict__ p2,
-                                                int64_t n4, const int4 *__restrict__ p4, int64_t n8,
-                                                const int4 *__restrict__ p8, int64_t ng,
-                                                const int32_t *__restrict__ pg, const int32_t *__restrict__ og,
-                                                T *__restrict__ v, uint64_t pol)
-{
-    const int64_t w2 = (n2 + 32 * GS_PAIRS_PER_THREAD - 1) / (32 * GS_PAIRS_PER_THREAD);
-    const int64_t w4 = (n4 + 32 * GS_QUADS_PER_THREAD - 1) / (32 * GS_QUADS_PER_THREAD);
-    const int64_t w8 = (n8 + 31) / 32;
-    if (wid < w2) {
-        const int64_t r0 = wid * 32 * GS_PAIRS_PER_THREAD + lane;
-        int2 c[GS_PAIRS_PER_THREAD];
-        T a[GS_PAIRS_PER_THREAD], b[GS_PAIRS_PER_THREAD];
-#pragma unroll
-        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (r0 + 32 * q < n2) c[q] = tma::ldi2(p2 + r0 + 32 * q, pol);
-#pragma unroll
-        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
-            if (r0 + 32 * q < n2) { a[q] = tma::ld1(v + c[q].x, pol); b[q] = tma::ld1(v + c[q].y, pol); }
-#pragma unroll
-        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
-            if (r0 + 32 * q < n2) { const T s = a[q] + b[q]; tma::st1(v + c[q].x, s, pol); tma::st1(v + c[q].y, s, pol); }
-        return;
-    }
-    wid -= w2;
-    if (wid < w4) {
-        const int64_t r0 = wid * 32 * GS_QUADS_PER_THREAD + lane;
-        int4 c[GS_QUADS_PER_THREAD];
-        T a[GS_QUADS_PER_THREAD][4];
-#pragma unroll
-        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (r0 + 32 * q < n4) c[q] = tma::ldi4(p4 + r0 + 32 * q, pol);
-#pragma unroll
-        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
-            if (r0 + 32 * q < n4) {
-                a[q][0] = tma::ld1(v + c[q].x, pol); a[q][1] = tma::ld1(v + c[q].y, pol);
-                a[q][2] = tma::ld1(v + c[q].z, pol); a[q][3] = tma::ld1(v + c[q].w, pol);
-            }
-#pragma unroll
-        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
-            if (r0 + 32 * q < n4) {
-                const T s = ((a[q][0] + a[q][1]) + a[q][2]) + a[q][3];
-                tma::st1(v + c[q].x, s, pol); tma::st1(v + c[q].y, s, pol);
-                tma::st1(v + c[q].z, s, pol); tma::st1(v + c[q].w, s, pol);
-            }
-        return;
-    }
-    wid -= w4;
-    if (wid < w8) {
-        const int64_t r = wid * 32 + lane;
-        if (r >= n8) return;
-        const int4 a = p8[2 * r], b = p8[2 * r + 1];
-        const T s = ((((((v[a.x] + v[a.y]) + v[a.z]) + v[a.w]) + v[b.x]) + v[b.y]) + v[b.z]) + v[b.w];
-        v[a.x] = s; v[a.y] = s; v[a.z] = s; v[a.w] = s;
-        v[b.x] = s; v[b.y] = s; v[b.z] = s; v[b.w] = s;
-        return;
-    }
-    wid -= w8;
-    const int64_t r = wid * 32 + lane;
-    if (r < ng) {
-        const int o0 = og[r], o1 = og[r + 1];
-        T s = v[pg[o0]];
-        for (int c = o0 + 1; c < o1; ++c) s += v[pg[c]];
-        for (int c = o0; c < o1; ++c) v[pg[c]] = s;
-    }
-}
-
 template <class T, int PPT>
 __global__ void __launch_bounds__(256)
     gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
                       const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
                       const int32_t *__restrict__ og, T *__restrict__ v, const int *done, int keep)
 {
-    if (done && *(volatile const int *)done) return;
     gs_classes_body<T, PPT, PPT / 2>((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, n2, p2,
-                                     n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(keep));
+                                     n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(keep), done);
 }
 
 static int64_t gs_class_warps(const GsClasses &C, int ppt)
@@ -139,9 +63,8 @@ __global__ void __launch_bounds__(256)
 {
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    const bool skip = done && *(volatile const int *)done;
     if (wid < cw) {
-        if (!skip) gs_classes_body<T, PPT, PPT / 2>(wid, lane, n2, p2, n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(C_keep));
+        gs_classes_body<T, PPT, PPT / 2>(wid, lane, n2, p2, n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(C_keep), done);
         return;
     }
     const uint64_t e = *(volatile const uint64_t *)(U.epochs + 2);
@@ -149,7 +72,7 @@ __global__ void __launch_bounds__(256)
     if (lane == 0)
         for (int k = 0; k < U.nnbr; ++k) ok &= wait_epoch(U.hflags + U.nbr[k], e, U.err, U.timeout_ns);
     ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (skip) return;
+    if (done && *(volatile const int *)done) return;
     const int64_t r = (wid - cw) * 32 + lane;
     if (r >= U.nifc) return;
     const T *recv = reinterpret_cast<const T *>(U.recv) + (int64_t)(e & 1) * U.half;

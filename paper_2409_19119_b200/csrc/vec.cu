@@ -62,7 +62,18 @@ int device_sms()
 }
 
 int vec_blocks() { return 4 * device_sms(); }
-int upd_blocks() { return 2 * device_sms(); }   // residual update: 2 CTAs per SM, 4 double2 per thread per tile
+// residual update: 2 CTAs per SM with 4 double2 per thread per tile (NEK_UPD_CTAS = 4 or 8: that many CTAs
+// per SM with 2 double2 per thread per tile; measurement switch)
+int upd_blocks()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NEK_UPD_CTAS");
+        v = e ? atoi(e) : 2;
+        if (v != 2 && v != 4 && v != 8) v = 2;
+    }
+    return v * device_sms();
+}
 
 // red_all holds [nranks][RED_N]; sums are taken in rank order.
 __device__ __forceinline__ double rank_sum(const double *red_all, int nranks, int slot)
@@ -406,8 +417,16 @@ cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const doub
 {
     P2PMail m;
     if (mail) m = *mail;
-    pcg_update_fused_kernel<4, 2><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist, part,
-                                                               dst, counter, m, keep);
+    const int per_sm = nblk / device_sms();
+    if (per_sm >= 8)
+        pcg_update_fused_kernel<2, 8><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
+                                                                   part, dst, counter, m, keep);
+    else if (per_sm >= 4)
+        pcg_update_fused_kernel<2, 4><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
+                                                                   part, dst, counter, m, keep);
+    else
+        pcg_update_fused_kernel<4, 2><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
+                                                                   part, dst, counter, m, keep);
     return cudaGetLastError();
 }
 

@@ -504,3 +504,4 @@ def test_pcg_l2_resident_bitwise(nek, keep):
     x0, it0, h0 = res["0"]
     x1, it1, h1 = res[keep]
     assert it1 == it0 and np.array_equal(x1, x0) and np.array_equal(h1, h0)
+
