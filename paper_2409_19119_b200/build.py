@@ -32,10 +32,10 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
-def _stale():
-    if not os.path.exists(LIB):
+def _stale(lib=LIB):
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.inc")) + \
         [os.path.join(ROOT, "include", "nek.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
@@ -47,10 +47,15 @@ def _compile(args):
     return src, r.returncode, r.stdout + r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every source to an object in parallel (one nvcc per translation unit), then link."""
-    if not force and not _stale():
-        return LIB
+LIB_CHECKED = os.path.join(PKG, "libnek_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Compile every source to an object in parallel (one nvcc per translation unit), then link.
+    checked=True builds libnek_checked.so with the device invariant checks on (-DNEK_CHECKED)."""
+    lib_out = LIB_CHECKED if checked else LIB
+    if not force and not _stale(lib_out):
+        return lib_out
     from concurrent.futures import ThreadPoolExecutor
     inc, lib = nccl_paths()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -60,9 +65,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
               "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
     if verbose:
         common += ["-Xptxas", "-v"]
+    if checked:
+        common += ["-DNEK_CHECKED"]
     jobs, objs = [], []
     for src in sources():
-        obj = os.path.join(objdir, os.path.basename(src) + f".{os.getpid()}.o")
+        obj = os.path.join(objdir, os.path.basename(src) + f".{'chk.' if checked else ''}{os.getpid()}.o")
         objs.append(obj)
         jobs.append(([*common, "-c", src, "-o", obj], src))
     with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
@@ -75,7 +82,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         for src, _, out in results:
             sys.stderr.write(f"--- {src}\n{out}")
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib_out + f".tmp{os.getpid()}"
     link = [nvcc, *ARCH, "-shared", *objs, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}", "-o", tmp]
     r = subprocess.run(link, capture_output=True, text=True)
     for o in objs:
@@ -84,10 +91,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link of libnek.so failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

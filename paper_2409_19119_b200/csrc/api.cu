@@ -344,7 +344,7 @@ static int gs_local_and_unpack_p2p(nek_ctx *ctx, T *v, const int *done, bool ski
     U.nifc = ctx->nifc; U.perm = ctx->ifc_perm; U.offs = ctx->ifc_offs; U.coffs = ctx->coffs;
     U.contrib = ctx->contrib; U.nbr = ctx->d_nbr; U.partial = ctx->ifc_partial; U.recv = ctx->recv2;
     U.half = std::max<int64_t>(ctx->nslots, 1); U.hflags = ctx->hflags; U.epochs = ctx->epochs; U.nnbr = (int)ctx->neighbors.size();
-    U.err = ctx->p2p_err; U.timeout_ns = ctx->p2p_timeout_ns;
+    U.err = ctx->p2p_err; U.timeout_ns = ctx->p2p_timeout_ns; U.nv = ctx->n;
     CK(launch_gs_classes_unpack<T>(skip_local ? GsClasses() : ctx->gsc, U, v, done, ctx->s_main));
     ctx->stats.gs_launches += 1;
     ctx->stats.launches += 1;
@@ -782,6 +782,7 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         CK(upload(ctx, &ctx->gs_pg, cg)); CK(upload(ctx, &ctx->gs_og, og));
         ctx->gsc.n2 = (int64_t)c2.size() / 2; ctx->gsc.n4 = (int64_t)c4.size() / 4; ctx->gsc.n8 = (int64_t)c8.size() / 8;
         ctx->gsc.ng = (int64_t)og.size() - 1;
+        ctx->gsc.nv = ctx->n;
         ctx->gsc.p2 = ctx->gs_p2; ctx->gsc.p4 = ctx->gs_p4; ctx->gsc.p8 = ctx->gs_p8;
         ctx->gsc.pg = ctx->gs_pg; ctx->gsc.og = ctx->gs_og;
         // boundary Ax + halo send beside the interior Ax (concurrent streams) pays off for small

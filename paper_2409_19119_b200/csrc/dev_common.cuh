@@ -8,12 +8,23 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cassert>
 #include <cstdint>
 
 #include "ax_tma.cuh"
 #include "nek_ctx.h"
 
 namespace nekb200 {
+
+// Device-side invariant checks of the index-driven kernels (gather-scatter maps, halo slots): active in
+// the checked build (build.py --checked -> libnek_checked.so, -DNEK_CHECKED), a failed check is a device
+// assert (cudaErrorAssert, the call returns NEK_ECUDA).  compute-sanitizer is not available on the
+// GPU pool, so this build plus the parity suite is the memory-safety evidence.
+#ifdef NEK_CHECKED
+#define NEK_CHECK(c) assert(c)
+#else
+#define NEK_CHECK(c) ((void)0)
+#endif
 
 __device__ __forceinline__ bool bit_of(const uint32_t *__restrict__ bits, int64_t l)
 {

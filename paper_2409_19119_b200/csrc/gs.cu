@@ -38,10 +38,10 @@ template <class T, int PPT>
 __global__ void __launch_bounds__(256)
     gs_classes_kernel(int64_t n2, const int2 *__restrict__ p2, int64_t n4, const int4 *__restrict__ p4, int64_t n8,
                       const int4 *__restrict__ p8, int64_t ng, const int32_t *__restrict__ pg,
-                      const int32_t *__restrict__ og, T *__restrict__ v, const int *done, int keep)
+                      const int32_t *__restrict__ og, T *__restrict__ v, const int *done, int keep, int64_t nv)
 {
     gs_classes_body<T, PPT, PPT / 2>((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, n2, p2,
-                                     n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(keep), done);
+                                     n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(keep), done, nv);
 }
 
 static int64_t gs_class_warps(const GsClasses &C, int ppt)
@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(256)
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid < cw) {
-        gs_classes_body<T, PPT, PPT / 2>(wid, lane, n2, p2, n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(C_keep), done);
+        gs_classes_body<T, PPT, PPT / 2>(wid, lane, n2, p2, n4, p4, n8, p8, ng, pg, og, v, tma::policy_keep(C_keep), done,
+                                         U.nv);
         return;
     }
     const uint64_t e = *(volatile const uint64_t *)(U.epochs + 2);
@@ -78,12 +79,16 @@ __global__ void __launch_bounds__(256)
     const T *recv = reinterpret_cast<const T *>(U.recv) + (int64_t)(e & 1) * U.half;
     const T *partial = reinterpret_cast<const T *>(U.partial);
     const int c0 = U.coffs[r], c1 = U.coffs[r + 1];
+    NEK_CHECK(c0 < c1);
     int src = U.contrib[c0];
+    NEK_CHECK(src < U.half);
     T s = src < 0 ? partial[r] : ((volatile const T *)recv)[src];
     for (int c = c0 + 1; c < c1; ++c) {
         src = U.contrib[c];
+        NEK_CHECK(src < U.half);
         s += src < 0 ? partial[r] : ((volatile const T *)recv)[src];
     }
+    for (int c = U.offs[r]; c < U.offs[r + 1]; ++c) NEK_CHECK(U.perm[c] >= 0 && U.perm[c] < U.nv);
     if (!ok) s = T(__longlong_as_double(0x7ff8000000000000ll));   // a neighbour timed out: NaN, not stale data
     for (int c = U.offs[r]; c < U.offs[r + 1]; ++c) v[U.perm[c]] = s;
 }
@@ -107,7 +112,7 @@ cudaError_t launch_gs_classes(const GsClasses &C, T *v, const int *done, cudaStr
     if (warps <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
     gs_classes_kernel<T, GS_PPT><<<grid, 256, 0, s>>>(C.n2, (const int2 *)C.p2, C.n4, (const int4 *)C.p4, C.n8,
-                                                      (const int4 *)C.p8, C.ng, C.pg, C.og, v, done, C.keep);
+                                                      (const int4 *)C.p8, C.ng, C.pg, C.og, v, done, C.keep, C.nv);
     return cudaGetLastError();
 }
 
@@ -209,6 +214,8 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
             }
             partial[run] = s;
             const int k = slot_nbr[sidx];
+            NEK_CHECK(k >= 0 && k < nnbr && sidx >= send_offs[k] && sidx < send_offs[k + 1] && remote_off[k] >= 0 &&
+                      remote_off[k] + (sidx - send_offs[k]) < remote_half[k]);
             reinterpret_cast<T *>(peer_recv[k])[par * remote_half[k] + remote_off[k] + (sidx - send_offs[k])] = s;
         }
     }

@@ -19,7 +19,8 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
                                                 int64_t n4, const int4 *__restrict__ p4, int64_t n8,
                                                 const int4 *__restrict__ p8, int64_t ng,
                                                 const int32_t *__restrict__ pg, const int32_t *__restrict__ og,
-                                                T *__restrict__ v, uint64_t pol, const int *done = nullptr)
+                                                T *__restrict__ v, uint64_t pol, const int *done = nullptr,
+                                                int64_t nv = 0)
 {
     // the index and value loads are issued before the (dependent) read of the convergence flag, so
     // the two latencies overlap; nothing is stored once `done` is set
@@ -32,6 +33,9 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
         T a[GS_PAIRS_PER_THREAD], b[GS_PAIRS_PER_THREAD];
 #pragma unroll
         for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q) if (r0 + 32 * q < n2) c[q] = tma::ldi2(p2 + r0 + 32 * q, pol);
+#pragma unroll
+        for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)   // canonical: copies ascending, inside the vector
+            if (r0 + 32 * q < n2) NEK_CHECK(c[q].x >= 0 && c[q].x < c[q].y && c[q].y < nv);
 #pragma unroll
         for (int q = 0; q < GS_PAIRS_PER_THREAD; ++q)
             if (r0 + 32 * q < n2) { a[q] = tma::ld1(v + c[q].x, pol); b[q] = tma::ld1(v + c[q].y, pol); }
@@ -48,6 +52,10 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
         T a[GS_QUADS_PER_THREAD][4];
 #pragma unroll
         for (int q = 0; q < GS_QUADS_PER_THREAD; ++q) if (r0 + 32 * q < n4) c[q] = tma::ldi4(p4 + r0 + 32 * q, pol);
+#pragma unroll
+        for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
+            if (r0 + 32 * q < n4)
+                NEK_CHECK(c[q].x >= 0 && c[q].x < c[q].y && c[q].y < c[q].z && c[q].z < c[q].w && c[q].w < nv);
 #pragma unroll
         for (int q = 0; q < GS_QUADS_PER_THREAD; ++q)
             if (r0 + 32 * q < n4) {
@@ -70,6 +78,8 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
         const int64_t r = wid * 32 + lane;
         if (r >= n8) return;
         const int4 a = p8[2 * r], b = p8[2 * r + 1];
+        NEK_CHECK(a.x >= 0 && a.x < a.y && a.y < a.z && a.z < a.w && a.w < b.x && b.x < b.y && b.y < b.z &&
+                  b.z < b.w && b.w < nv);
         const T s = ((((((tma::ld1(v + a.x, pol) + tma::ld1(v + a.y, pol)) + tma::ld1(v + a.z, pol)) +
                         tma::ld1(v + a.w, pol)) + tma::ld1(v + b.x, pol)) + tma::ld1(v + b.y, pol)) +
                      tma::ld1(v + b.z, pol)) + tma::ld1(v + b.w, pol);
@@ -81,6 +91,8 @@ __device__ __forceinline__ void gs_classes_body(int64_t wid, int lane, int64_t n
     const int64_t r = wid * 32 + lane;
     if (r < ng) {
         const int o0 = og[r], o1 = og[r + 1];
+        NEK_CHECK(o0 < o1 && pg[o0] >= 0 && pg[o1 - 1] < nv);
+        for (int c = o0 + 1; c < o1; ++c) NEK_CHECK(pg[c - 1] < pg[c]);
         T s = tma::ld1(v + pg[o0], pol);
         for (int c = o0 + 1; c < o1; ++c) s += tma::ld1(v + pg[c], pol);
         for (int c = o0; c < o1; ++c) v[pg[c]] = s;

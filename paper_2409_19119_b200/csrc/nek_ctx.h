@@ -103,6 +103,7 @@ int ax_gstride_f(int N);
 // gather-scatter runs grouped by length (see kernels.cu)
 struct GsClasses {
     int64_t n2 = 0, n4 = 0, n8 = 0, ng = 0;
+    int64_t nv = 0;                      // length of the vector the runs index (checked build)
     const int32_t *p2 = nullptr, *p4 = nullptr, *p8 = nullptr, *pg = nullptr, *og = nullptr;
     int keep = 0;                        // L2 evict_last on the index lists and values (L2-resident mode)
 };
@@ -155,6 +156,7 @@ struct HaloUnpack {
     int nnbr = 0;
     int *err = nullptr;
     uint64_t timeout_ns = 0;
+    int64_t nv = 0;                      // vector length (checked build)
 };
 template <class T>
 cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, T *v, const int *done,

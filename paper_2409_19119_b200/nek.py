@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnek.so")
+# NEK_LIB_VARIANT=checked loads the build with the device invariant checks (build.py --checked)
+LIB_PATH = os.path.join(_PKG, "libnek_checked.so" if os.environ.get("NEK_LIB_VARIANT") == "checked" else "libnek.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
