@@ -84,8 +84,10 @@ def make_mesh(rank, world, ez, N, args=None):
         lz = 64 // world
         return mg.box_mesh(32, 64, 64, N, deform="bubble", eps=0.05, dirichlet="all",
                            zlayers=(rank * lz, (rank + 1) * lz))
+    # every rank owns a unit cube of 16 x 16 x ez elements (cubic elements at any rank count: the per-GPU
+    # problem of weak scaling does not change shape with N; at N = 1, ez = 16 this is config 2)
     return mg.box_mesh(EX, EY, ez * world, N, deform="bubble", eps=0.05, dirichlet="all",
-                       zlayers=(rank * ez, (rank + 1) * ez))
+                       extent=(1.0, 1.0, ez * world / float(EX)), zlayers=(rank * ez, (rank + 1) * ez))
 
 
 def workload_name(args, world):
@@ -98,7 +100,8 @@ def workload_name(args, world):
                 f"layer, {args.rod_layers} layers per GPU ({args.rod_layers * world} total, z-slabs), N={args.order}, "
                 + ("Dirichlet on pins, walls, inlet" if args.h2 != 0.0 else "Dirichlet on the outlet plane"))
     return (f"SEM {kind} Jacobi-PCG, {args.iters} iters/step; {EX}x{EY}x{args.ez} elements per GPU "
-            f"(box {EX}x{EY}x{args.ez * world}, z-slabs), N={args.order}, bubble-deformed, Dirichlet all faces")
+            f"(box {EX}x{EY}x{args.ez * world} elements on [0,1]x[0,1]x[0,{args.ez * world / EX:g}], cubic elements, "
+            f"z-slabs), N={args.order}, bubble-deformed, Dirichlet all faces")
 
 
 class ClockSampler:

@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     }
     const double alpha = sc->rho / sigma;
     double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
+    double g0 = 0.0, k0 = 0.0, g1 = 0.0, k1 = 0.0;   // the .y points: two independent Dot2 chains per dot
     for (bool first = true; base < n2; base += (int64_t)gridDim.x * tile, first = false) {
         if (!first) load(base);
 #pragma unroll
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
                 rv[q].x = fma(-alpha, wv[q].x, rv[q].x); rv[q].y = fma(-alpha, wv[q].y, rv[q].y);
                 tma::st2(r + 2 * h, rv[q], pol);
                 if (ow[q] & 1u) { dd_add_prod(h0, l0, rv[q].x, __dmul_rn(dv[q].x, rv[q].x)); dd_add_prod(h1, l1, rv[q].x, rv[q].x); }
-                if (ow[q] & 2u) { dd_add_prod(h0, l0, rv[q].y, __dmul_rn(dv[q].y, rv[q].y)); dd_add_prod(h1, l1, rv[q].y, rv[q].y); }
+                if (ow[q] & 2u) { dd_add_prod(g0, k0, rv[q].y, __dmul_rn(dv[q].y, rv[q].y)); dd_add_prod(g1, k1, rv[q].y, rv[q].y); }
             }
         }
     }
@@ -391,6 +392,8 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
         r[l] = rl;
         if (bit_of(obits, l)) { dd_add_prod(h0, l0, rl, __dmul_rn(dinv[l], rl)); dd_add_prod(h1, l1, rl, rl); }
     }
+    dd_add(h0, l0, g0, k0);
+    dd_add(h1, l1, g1, k1);
     store_part2(part, h0, l0, h1, l1, sred);
     if (threadIdx.x == 0) {
         __threadfence();

@@ -200,3 +200,51 @@ def test_pmg_errors(nek):
         assert ei.value.code == -1
     finally:
         nek.free(ctx)
+
+
+def test_pmg_long_domain_parity(nek):
+    """A long domain with cubic elements (4 x 4 x 64 elements on [0,1] x [0,1] x [0,16], N = 3, Dirichlet
+    on all faces): pMG-PCG takes the oracle's iteration count (+-1), x within 1e-8."""
+    m = mg.box_mesh(4, 4, 64, 3, deform="bubble", dirichlet="all", extent=(1.0, 1.0, 16.0))
+    O = oracle.Oracle.from_mesh(m)
+    b = mg.smooth_field(m, seed=1)
+    Po = opmg.PMG(O, m.xyz, 1.0, 0.0)
+    xo, ito, sto, _ = opmg.pcg(O, 1.0, 0.0, b, 1e-8, 300, Po.apply)
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        P = nek.PMG(ctx, m.xyz, 1.0, 0.0)
+        x = np.zeros(m.n_local)
+        st, it, rr, _ = P.solve(b, x, 1e-8, 300)
+        P.free()
+        assert st == nek.OK and abs(it - ito) <= 1, (it, ito)
+        assert rel(x, xo) <= 1e-8
+    finally:
+        nek.free(ctx)
+
+
+@pytest.mark.parametrize("aspect", [1, 32])
+def test_pmg_long_domain_iterations(nek, aspect):
+    """8 x 8 x 256 elements, N = 7, Dirichlet on all faces: with cubic elements (domain [0,1]^2 x [0,32])
+    pMG-PCG reaches 1e-8 in <= 30 iterations; squeezed into the unit cube (element aspect ratio 32) the
+    Jacobi-Chebyshev smoother cannot damp the modes that are smooth along the strong direction and the
+    count grows several-fold -- a property of the point smoother, not of the coarse solve (DESIGN.md 3b,
+    reading P7)."""
+    lz = 32.0 if aspect == 1 else 1.0
+    m = mg.box_mesh(8, 8, 256, 7, deform="bubble", dirichlet="all", extent=(1.0, 1.0, lz))
+    ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+    try:
+        b = torch.from_numpy(mg.smooth_field(m, seed=1)).cuda()
+        P = nek.PMG(ctx, m.xyz, 1.0, 0.0)
+        x = torch.zeros_like(b)
+        st, it, rr, _ = P.solve(b, x, 1e-8, 1000)
+        P.free()
+        xj = torch.zeros_like(b)
+        stj, itj, _, _ = nek.pcg_solve(ctx, 1.0, 0.0, b, xj, 1e-8, 20000)
+        print(f"[pmg long domain] aspect {aspect}: pMG {it} iterations, Jacobi {itj}")
+        assert st == nek.OK and stj == nek.OK
+        if aspect == 1:
+            assert it <= 30
+        else:
+            assert it > 2 * 30
+    finally:
+        nek.free(ctx)
