@@ -356,21 +356,22 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     // the first tile's streams are issued before the dependent scalar reads (done, sigma, rho), so
     // their latencies overlap; w, r, Dinv are complete (stream order) whatever the scalars say
     load(base);
+    // the scalars are final when the kernel starts (stream order): their loads are issued together
+    // with the convergence flag's instead of after it
+    const double rho0 = sc->rho;
+    double sigma = (mail.nranks > 1) ? 0.0 : rank_sum(red_all, nranks, RED_SIGMA);
     if (*(volatile int *)&sc->done) return;
-    double sigma;
     if (mail.nranks > 1) {                       // sigma of every rank from the mailbox (channel 0)
         if (threadIdx.x < 32) mail_pull_warp(mail, 0, s_sig);
         __syncthreads();
         sigma = s_sig[0];
         if (blockIdx.x == 0 && threadIdx.x == 0) sc->sigma = sigma;
-    } else {
-        sigma = rank_sum(red_all, nranks, RED_SIGMA);
     }
     if (!(sigma > 0.0)) {                       // breakdown: <p, A p> <= 0, or a peer timed out (NaN)
         if (blockIdx.x == 0 && threadIdx.x == 0) { sc->status = NEK_ENOTSPD; sc->alpha = 0.0; sc->done = 1; }
         return;
     }
-    const double alpha = sc->rho / sigma;
+    const double alpha = rho0 / sigma;
     double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
     double g0 = 0.0, k0 = 0.0, g1 = 0.0, k1 = 0.0;   // the .y points: two independent Dot2 chains per dot
     for (bool first = true; base < n2; base += (int64_t)gridDim.x * tile, first = false) {
