@@ -350,7 +350,9 @@ def main():
 
     mesh = make_mesh(rank, world, args.ez, args.order, args)
     log("setup")
+    t_setup = time.perf_counter()
     ctx = nek.setup(mesh.E, mesh.N, mesh.xyz, mesh.gid, mesh.mask, comm=comm, device=local)
+    t_setup = time.perf_counter() - t_setup
     info = nek.get_info(ctx)
     if args.variant:
         nek.set_variant(ctx, args.variant)
@@ -697,7 +699,8 @@ def main():
                        "parallelism": f"dp{world} (element z-slabs, NCCL halo + allgather reductions)",
                        "timing": "CUDA graph of 10 PCG iterations per replay, device time by CUDA events",
                        "l2_resident": {"keep": info["l2_keep"], "setaside_bytes": info["l2_setaside"],
-                                       "setaside_max": info["l2_setaside_max"]}},
+                                       "setaside_max": info["l2_setaside_max"]},
+                       "setup_s": t_setup},
             "pcg_iter_per_s": args.iters * args.steps / (t_ms * 1e-3),
             "ax_gs": ax_gs,
             "beyond_l2": beyond,

@@ -52,6 +52,19 @@ struct MK {
 template <int NQ> __device__ __forceinline__ double Jm(int I, int i) { return c_Jq[NQ - 1][I * NQ + i]; }
 template <int NQ> __device__ __forceinline__ double Dm(int I, int i) { return c_Dq[NQ - 1][I * NQ + i]; }
 
+// Work items of a contraction stage: `lines` lines of `outs` outputs each, split into `ch` chunks of
+// `w` outputs so that lines * ch covers the CTA (a stage with fewer lines than threads would leave most
+// threads waiting at the next barrier).  Each output is the same fixed-order FMA chain whatever the
+// split, so the results do not depend on it.
+__host__ __device__ constexpr int mk_chunks(int lines, int outs, int nt)
+{
+    return (nt + lines - 1) / lines < outs ? (nt + lines - 1) / lines : outs;
+}
+__host__ __device__ constexpr int mk_width(int lines, int outs, int nt)
+{
+    return (outs + mk_chunks(lines, outs, nt) - 1) / mk_chunks(lines, outs, nt);
+}
+
 template <int NQ>
 __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
     makef_kernel(int64_t E, const double *__restrict__ G9, const double *__restrict__ u0,
@@ -59,7 +72,7 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
                  double *__restrict__ f1, double *__restrict__ f2)
 {
     using C = MK<NQ>;
-    constexpr int MQ = C::MQ, P3 = C::P3, M3 = C::M3, PN = C::PN, PM = C::PM;
+    constexpr int MQ = C::MQ, P3 = C::P3, M3 = C::M3, PN = C::PN, PM = C::PM, NT = C::NT;
     constexpr int SZ_U = C::SZ_U, SZ_A = C::SZ_A, SZ_AA = C::SZ_AA;
     extern __shared__ __align__(16) double sm[];
     double *U3 = sm;                       // [3][NQ][NQ][PN]
@@ -71,6 +84,16 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
     double *BA = AD + SZ_AA;
     double *F = BA + SZ_AA;                // [M3]
     const int t = threadIdx.x, nt = blockDim.x;
+    // stage shapes (lines, outputs per line) and their splits
+    constexpr int L_UI = 3 * NQ * NQ, CH_UI = mk_chunks(L_UI, MQ, NT), W_UI = mk_width(L_UI, MQ, NT);
+    constexpr int L_UJ = 3 * NQ * MQ, CH_UJ = mk_chunks(L_UJ, MQ, NT), W_UJ = mk_width(L_UJ, MQ, NT);
+    constexpr int L_UK = 3 * MQ * MQ, CH_UK = mk_chunks(L_UK, MQ, NT), W_UK = mk_width(L_UK, MQ, NT);
+    constexpr int L_I = NQ * NQ, CH_I = mk_chunks(L_I, MQ, NT), W_I = mk_width(L_I, MQ, NT);
+    constexpr int L_J = 2 * NQ * MQ, CH_J = mk_chunks(L_J, MQ, NT), W_J = mk_width(L_J, MQ, NT);
+    constexpr int L_K = MQ * MQ, CH_K = mk_chunks(L_K, MQ, NT), W_K = mk_width(L_K, MQ, NT);
+    constexpr int L_KT = MQ * MQ, CH_KT = mk_chunks(L_KT, NQ, NT), W_KT = mk_width(L_KT, NQ, NT);
+    constexpr int L_JT = NQ * MQ, CH_JT = mk_chunks(L_JT, NQ, NT), W_JT = mk_width(L_JT, NQ, NT);
+    constexpr int L_IT = NQ * NQ, CH_IT = mk_chunks(L_IT, NQ, NT), W_IT = mk_width(L_IT, NQ, NT);
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
         // the next element's lattice factors into L2 while this one computes (read in the Ut stage)
         if (MK_PF_G && t == 0 && e + gridDim.x < E && (9 * M3 * 8) % 16 == 0)
@@ -83,14 +106,17 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
         }
         __syncthreads();
         // ---- U at the fine points, 3 components together: i-lines, j-lines, k-columns
-        for (int L = t; L < 3 * NQ * NQ; L += nt) {                  // i: [c][k][j] lines
+        for (int it = t; it < L_UI * CH_UI; it += nt) {              // i: [c][k][j] lines
+            const int L = it % L_UI, ch = it / L_UI;
             const int c = L / (NQ * NQ), kj = L % (NQ * NQ);
             double x[NQ];
 #pragma unroll
             for (int m = 0; m < NQ; ++m) x[m] = U3[c * SZ_U + kj * PN + m];
             double *o = (c == 0 ? SA : c == 1 ? SB : AA) + kj * PM;  // scratch per component
-#pragma unroll 2
-            for (int I = 0; I < MQ; ++I) {
+#pragma unroll
+            for (int ii = 0; ii < W_UI; ++ii) {
+                const int I = ch * W_UI + ii;
+                if (I >= MQ) break;
                 double s = 0.0;
 #pragma unroll
                 for (int m = 0; m < NQ; ++m) s = fma(Jm<NQ>(I, m), x[m], s);
@@ -98,15 +124,18 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
             }
         }
         __syncthreads();
-        for (int L = t; L < 3 * NQ * MQ; L += nt) {                  // j: [c][k][I] lines
+        for (int it = t; it < L_UJ * CH_UJ; it += nt) {              // j: [c][k][I] lines
+            const int L = it % L_UJ, ch = it / L_UJ;
             const int c = L / (NQ * MQ), r = L % (NQ * MQ), k = r / MQ, I = r % MQ;
             const double *in = (c == 0 ? SA : c == 1 ? SB : AA);
             double x[NQ];
 #pragma unroll
             for (int m = 0; m < NQ; ++m) x[m] = in[(k * NQ + m) * PM + I];
             double *o = (c == 0 ? AD : c == 1 ? BA : F);              // [k][J][I] stride PM (F: own layout)
-#pragma unroll 2
-            for (int J = 0; J < MQ; ++J) {
+#pragma unroll
+            for (int jj = 0; jj < W_UJ; ++jj) {
+                const int J = ch * W_UJ + jj;
+                if (J >= MQ) break;
                 double s = 0.0;
 #pragma unroll
                 for (int m = 0; m < NQ; ++m) s = fma(Jm<NQ>(J, m), x[m], s);
@@ -115,7 +144,8 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
             }
         }
         __syncthreads();
-        for (int L = t; L < 3 * MQ * MQ; L += nt) {                  // k: [c][J][I] columns -> U
+        for (int it = t; it < L_UK * CH_UK; it += nt) {              // k: [c][J][I] columns -> U
+            const int L = it % L_UK, ch = it / L_UK;
             const int c = L / (MQ * MQ), JI = L % (MQ * MQ);
             double x[NQ];
             if (c < 2) {
@@ -127,8 +157,10 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
 #pragma unroll
                 for (int m = 0; m < NQ; ++m) x[m] = F[m * MQ * MQ + JI];
             }
-#pragma unroll 2
-            for (int K = 0; K < MQ; ++K) {
+#pragma unroll
+            for (int kk = 0; kk < W_UK; ++kk) {
+                const int K = ch * W_UK + kk;
+                if (K >= MQ) break;
                 double s = 0.0;
 #pragma unroll
                 for (int m = 0; m < NQ; ++m) s = fma(Jm<NQ>(K, m), x[m], s);
@@ -151,12 +183,15 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
         // ---- per component: gradient at the fine points, F = Ut . grad u_c, project back
         for (int c = 0; c < 3; ++c) {
             const double *uc = U3 + c * SZ_U;
-            for (int L = t; L < NQ * NQ; L += nt) {                  // i: A = J u, B = Dq u
+            for (int it = t; it < L_I * CH_I; it += nt) {            // i: A = J u, B = Dq u
+                const int L = it % L_I, ch = it / L_I;
                 double x[NQ];
 #pragma unroll
                 for (int m = 0; m < NQ; ++m) x[m] = uc[L * PN + m];
-#pragma unroll 2
-                for (int I = 0; I < MQ; ++I) {
+#pragma unroll
+                for (int ii = 0; ii < W_I; ++ii) {
+                    const int I = ch * W_I + ii;
+                    if (I >= MQ) break;
                     double a = 0.0, b = 0.0;
 #pragma unroll
                     for (int m = 0; m < NQ; ++m) { a = fma(Jm<NQ>(I, m), x[m], a); b = fma(Dm<NQ>(I, m), x[m], b); }
@@ -165,14 +200,17 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
                 }
             }
             __syncthreads();
-            for (int L = t; L < 2 * NQ * MQ; L += nt) {              // j: AA, AD from A; BA from B
+            for (int it = t; it < L_J * CH_J; it += nt) {            // j: AA, AD from A; BA from B
+                const int L = it % L_J, ch = it / L_J;
                 const int which = L / (NQ * MQ), r = L % (NQ * MQ), k = r / MQ, I = r % MQ;
                 const double *in = which == 0 ? SA : SB;
                 double x[NQ];
 #pragma unroll
                 for (int m = 0; m < NQ; ++m) x[m] = in[(k * NQ + m) * PM + I];
-#pragma unroll 2
-                for (int J = 0; J < MQ; ++J) {
+#pragma unroll
+                for (int jj = 0; jj < W_J; ++jj) {
+                    const int J = ch * W_J + jj;
+                    if (J >= MQ) break;
                     if (which == 0) {
                         double a = 0.0, d = 0.0;
 #pragma unroll
@@ -188,7 +226,8 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
                 }
             }
             __syncthreads();
-            for (int L = t; L < MQ * MQ; L += nt) {                  // k: d_r, d_s, d_t and F
+            for (int it = t; it < L_K * CH_K; it += nt) {            // k: d_r, d_s, d_t and F
+                const int L = it % L_K, ch = it / L_K;
                 const int J = L / MQ, I = L % MQ;
                 double xa[NQ], xd[NQ], xb[NQ];
 #pragma unroll
@@ -197,8 +236,10 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
                     xd[m] = AD[(m * MQ + J) * PM + I];
                     xb[m] = BA[(m * MQ + J) * PM + I];
                 }
-#pragma unroll 2
-                for (int K = 0; K < MQ; ++K) {
+#pragma unroll
+                for (int kk = 0; kk < W_K; ++kk) {
+                    const int K = ch * W_K + kk;
+                    if (K >= MQ) break;
                     double dr = 0.0, ds = 0.0, dt = 0.0;
 #pragma unroll
                     for (int m = 0; m < NQ; ++m) {
@@ -211,13 +252,16 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
                 }
             }
             __syncthreads();
-            for (int L = t; L < MQ * MQ; L += nt) {                  // k^T: P1[k][J][I] into AA
+            for (int it = t; it < L_KT * CH_KT; it += nt) {          // k^T: P1[k][J][I] into AA
+                const int L = it % L_KT, ch = it / L_KT;
                 double x[MQ];
 #pragma unroll
                 for (int K = 0; K < MQ; ++K) x[K] = F[K * MQ * MQ + L];
                 const int J = L / MQ, I = L % MQ;
-#pragma unroll 2
-                for (int k = 0; k < NQ; ++k) {
+#pragma unroll
+                for (int kk = 0; kk < W_KT; ++kk) {
+                    const int k = ch * W_KT + kk;
+                    if (k >= NQ) break;
                     double s = 0.0;
 #pragma unroll
                     for (int K = 0; K < MQ; ++K) s = fma(Jm<NQ>(K, k), x[K], s);
@@ -225,13 +269,16 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
                 }
             }
             __syncthreads();
-            for (int L = t; L < NQ * MQ; L += nt) {                  // j^T: P2[k][j][I] into SA
+            for (int it = t; it < L_JT * CH_JT; it += nt) {          // j^T: P2[k][j][I] into SA
+                const int L = it % L_JT, ch = it / L_JT;
                 const int k = L / MQ, I = L % MQ;
                 double x[MQ];
 #pragma unroll
                 for (int J = 0; J < MQ; ++J) x[J] = AA[(k * MQ + J) * PM + I];
-#pragma unroll 2
-                for (int j = 0; j < NQ; ++j) {
+#pragma unroll
+                for (int jj = 0; jj < W_JT; ++jj) {
+                    const int j = ch * W_JT + jj;
+                    if (j >= NQ) break;
                     double s = 0.0;
 #pragma unroll
                     for (int J = 0; J < MQ; ++J) s = fma(Jm<NQ>(J, j), x[J], s);
@@ -240,12 +287,15 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
             }
             __syncthreads();
             double *fo = (c == 0 ? f0 : c == 1 ? f1 : f2) + e * P3;
-            for (int L = t; L < NQ * NQ; L += nt) {                  // i^T: out[k][j][i] = -sum_I J[I][i] P2
+            for (int it = t; it < L_IT * CH_IT; it += nt) {          // i^T: out[k][j][i] = -sum_I J[I][i] P2
+                const int L = it % L_IT, ch = it / L_IT;
                 double x[MQ];
 #pragma unroll
                 for (int I = 0; I < MQ; ++I) x[I] = SA[L * PM + I];
-#pragma unroll 2
-                for (int i = 0; i < NQ; ++i) {
+#pragma unroll
+                for (int ii = 0; ii < W_IT; ++ii) {
+                    const int i = ch * W_IT + ii;
+                    if (i >= NQ) break;
                     double s = 0.0;
 #pragma unroll
                     for (int I = 0; I < MQ; ++I) s = fma(Jm<NQ>(I, i), x[I], s);
