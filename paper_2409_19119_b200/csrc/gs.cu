@@ -9,6 +9,7 @@
 
 #include "dev_common.cuh"
 #include "gs_body.cuh"
+#include "pack_body.cuh"
 
 namespace nekb200 {
 
@@ -198,26 +199,9 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
     const int64_t par = (int64_t)(e & 1);   // receive half by epoch parity, in units of the NEIGHBOUR's half size
     if (!(done && *(volatile const int *)done)) {
         for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < nslots;
-             sidx += (int64_t)gridDim.x * blockDim.x) {
-            const int run = send_run[sidx];
-            T s;
-            const int4 c4 = pack4 ? pack4[sidx] : make_int4(-2, -1, -1, -1);
-            if (c4.x >= 0) {                     // <= 4 local copies, listed per slot (one dependent level)
-                s = v[c4.x];
-                if (c4.y >= 0) s += v[c4.y];
-                if (c4.z >= 0) s += v[c4.z];
-                if (c4.w >= 0) s += v[c4.w];
-            } else {
-                const int o0 = offs[run], o1 = offs[run + 1];
-                s = v[perm[o0]];
-                for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
-            }
-            partial[run] = s;
-            const int k = slot_nbr[sidx];
-            NEK_CHECK(k >= 0 && k < nnbr && sidx >= send_offs[k] && sidx < send_offs[k + 1] && remote_off[k] >= 0 &&
-                      remote_off[k] + (sidx - send_offs[k]) < remote_half[k]);
-            reinterpret_cast<T *>(peer_recv[k])[par * remote_half[k] + remote_off[k] + (sidx - send_offs[k])] = s;
-        }
+             sidx += (int64_t)gridDim.x * blockDim.x)
+            pack_slot<T>(sidx, perm, offs, v, partial, send_run, slot_nbr, peer_recv, remote_off, send_offs,
+                         remote_half, nnbr, par, pack4);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
