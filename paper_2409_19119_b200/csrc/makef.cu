@@ -307,6 +307,218 @@ __global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
     }
 }
 
+// ------------------------------------------------------------ FP64 tensor cores (N = 7)
+// The same stages as makef_kernel with every 1-D contraction done as 8x8x4 FP64 tensor-core products
+// (mma.sync.m8n8k4.f64, DMMA): a stage is a small GEMM, rows = the lines of the stage, columns = the
+// outputs of a line (12 fine points padded to 16, or 8 GLL nodes), K = the points contracted (8 or 12);
+// the 1-D matrices J and Dq = J D sit in registers as B fragments, A fragments come from the shared
+// line buffers, and each warp takes 8-row x 8-column tiles.  One DMMA does 256 FMAs for one
+// instruction, so the stages are no longer bound by instruction issue and FMA latency.
+__device__ __forceinline__ void mk_dmma(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(MK<NQ>::NT, MK<NQ>::MINB)
+    makef_mma_kernel(int64_t E, const double *__restrict__ G9, const double *__restrict__ u0,
+                     const double *__restrict__ u1, const double *__restrict__ u2, double *__restrict__ f0,
+                     double *__restrict__ f1, double *__restrict__ f2)
+{
+    static_assert(NQ == 8, "the DMMA tiling is written for N = 7 (8 GLL nodes, 12 fine points)");
+    using C = MK<NQ>;
+    constexpr int MQ = C::MQ, P3 = C::P3, M3 = C::M3, PN = C::PN, PM = C::PM, NW = C::NT / 32;
+    constexpr int SZ_U = C::SZ_U, SZ_A = C::SZ_A, SZ_AA = C::SZ_AA;
+    extern __shared__ __align__(16) double sm[];
+    double *U3 = sm;
+    double *UT = U3 + 3 * SZ_U;
+    double *SA = UT + 3 * M3;
+    double *SB = SA + SZ_A;
+    double *AA = SB + SZ_A;
+    double *AD = AA + SZ_AA;
+    double *BA = AD + SZ_AA;
+    double *F = BA + SZ_AA;
+    const int t = threadIdx.x, nt = blockDim.x, warp = t >> 5, lane = t & 31;
+    const int ar = lane >> 2, ac = lane & 3;     // A (row ar, col ac), B (row ac, col ar), D (row ar, cols 2ac, 2ac+1)
+    // forward B fragments: B(k = m, n = I) = J[I][m] (K = 8 GLL nodes, 2 k-steps; N = 12 -> 2 tiles of 8)
+    double BJ[2][2], BDq[2][2];
+#pragma unroll
+    for (int n2 = 0; n2 < 2; ++n2)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            const int I = n2 * 8 + ar, m = ks * 4 + ac;
+            BJ[n2][ks] = I < MQ ? Jm<NQ>(I, m) : 0.0;
+            BDq[n2][ks] = I < MQ ? Dm<NQ>(I, m) : 0.0;
+        }
+    // transposed B fragments: B(k = K, n = i) = J[K][i] (K = 12 fine points, 3 k-steps; N = 8)
+    double BT[3];
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks) BT[ks] = Jm<NQ>(ks * 4 + ac, ar);
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        if (MK_PF_G && t == 0 && e + gridDim.x < E && (9 * M3 * 8) % 16 == 0)
+            tma::prefetch_l2(G9 + (e + gridDim.x) * 9 * (int64_t)M3, 9 * M3 * 8);
+        for (int q = t; q < 3 * P3; q += nt) {
+            const int c = q / P3, p = q - c * P3, i = p % NQ, kj = p / NQ;
+            const double *src = c == 0 ? u0 : c == 1 ? u1 : u2;
+            U3[c * SZ_U + kj * PN + i] = src[e * P3 + p];
+        }
+        __syncthreads();
+        // ---- U at the fine points, 3 components: i (rows c,k,j; 192), j (rows c,k,I; 288), k (rows c,J,I; 432)
+        for (int tile = warp; tile < 24 * 2; tile += NW) {
+            const int mt = tile >> 1, n2 = tile & 1;
+            const int row = mt * 8 + ar, c = row / 64, kj = row % 64;
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) mk_dmma(d0, d1, U3[c * SZ_U + kj * PN + ks * 4 + ac], (n2 ? BJ[1][ks] : BJ[0][ks]));
+            const int orow = mt * 8 + ar, oc = orow / 64, okj = orow % 64, I0 = n2 * 8 + 2 * ac;
+            double *o = (oc == 0 ? SA : oc == 1 ? SB : AA) + okj * PM;
+            if (I0 < MQ) o[I0] = d0;
+            if (I0 + 1 < MQ) o[I0 + 1] = d1;
+        }
+        __syncthreads();
+        for (int tile = warp; tile < 36 * 2; tile += NW) {
+            const int mt = tile >> 1, n2 = tile & 1;
+            const int row = mt * 8 + ar, c = row / (NQ * MQ), r = row % (NQ * MQ), k = r / MQ, I = r % MQ;
+            const double *in = (c == 0 ? SA : c == 1 ? SB : AA);
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) mk_dmma(d0, d1, in[(k * NQ + ks * 4 + ac) * PM + I], (n2 ? BJ[1][ks] : BJ[0][ks]));
+            const int J0 = n2 * 8 + 2 * ac;
+            if (c < 2) {
+                double *o = c == 0 ? AD : BA;
+                if (J0 < MQ) o[(k * MQ + J0) * PM + I] = d0;
+                if (J0 + 1 < MQ) o[(k * MQ + J0 + 1) * PM + I] = d1;
+            } else {
+                if (J0 < MQ) F[(k * MQ + J0) * MQ + I] = d0;
+                if (J0 + 1 < MQ) F[(k * MQ + J0 + 1) * MQ + I] = d1;
+            }
+        }
+        __syncthreads();
+        for (int tile = warp; tile < 54 * 2; tile += NW) {
+            const int mt = tile >> 1, n2 = tile & 1;
+            const int row = mt * 8 + ar, c = row / (MQ * MQ), JI = row % (MQ * MQ), J = JI / MQ, I = JI % MQ;
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int m = ks * 4 + ac;
+                const double a = c == 0 ? AD[(m * MQ + J) * PM + I] : c == 1 ? BA[(m * MQ + J) * PM + I]
+                                                                            : F[m * MQ * MQ + JI];
+                mk_dmma(d0, d1, a, (n2 ? BJ[1][ks] : BJ[0][ks]));
+            }
+            const int K0 = n2 * 8 + 2 * ac;
+            if (K0 < MQ) UT[c * M3 + K0 * MQ * MQ + JI] = d0;
+            if (K0 + 1 < MQ) UT[c * M3 + (K0 + 1) * MQ * MQ + JI] = d1;
+        }
+        __syncthreads();
+        // ---- contravariant velocity Ut_a = sum_b G_ab U_b (G streamed from HBM), in place
+        const double *Ge = G9 + e * 9 * (int64_t)M3;
+        for (int q = t; q < M3; q += nt) {
+            const double ux = UT[q], uy = UT[M3 + q], uz = UT[2 * M3 + q];
+            double g[9];
+#pragma unroll
+            for (int a = 0; a < 9; ++a) g[a] = __ldcs(Ge + a * M3 + q);
+            UT[q] = g[0] * ux + g[1] * uy + g[2] * uz;
+            UT[M3 + q] = g[3] * ux + g[4] * uy + g[5] * uz;
+            UT[2 * M3 + q] = g[6] * ux + g[7] * uy + g[8] * uz;
+        }
+        __syncthreads();
+        for (int c = 0; c < 3; ++c) {
+            const double *uc = U3 + c * SZ_U;
+            for (int tile = warp; tile < 8 * 2; tile += NW) {           // i: A = J u, B = Dq u (rows k,j)
+                const int mt = tile >> 1, n2 = tile & 1, L = mt * 8 + ar;
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const double x = uc[L * PN + ks * 4 + ac];
+                    mk_dmma(a0, a1, x, (n2 ? BJ[1][ks] : BJ[0][ks]));
+                    mk_dmma(b0, b1, x, (n2 ? BDq[1][ks] : BDq[0][ks]));
+                }
+                const int I0 = n2 * 8 + 2 * ac;
+                if (I0 < MQ) { SA[L * PM + I0] = a0; SB[L * PM + I0] = b0; }
+                if (I0 + 1 < MQ) { SA[L * PM + I0 + 1] = a1; SB[L * PM + I0 + 1] = b1; }
+            }
+            __syncthreads();
+            for (int tile = warp; tile < 24 * 2; tile += NW) {          // j: AA, AD from A; BA from B
+                const int mt = tile >> 1, n2 = tile & 1;
+                const int row = mt * 8 + ar, which = row / (NQ * MQ), r = row % (NQ * MQ), k = r / MQ, I = r % MQ;
+                const double *in = which == 0 ? SA : SB;
+                double a0 = 0.0, a1 = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const double x = in[(k * NQ + ks * 4 + ac) * PM + I];
+                    mk_dmma(a0, a1, x, (n2 ? BJ[1][ks] : BJ[0][ks]));
+                    if (which == 0) mk_dmma(d0, d1, x, (n2 ? BDq[1][ks] : BDq[0][ks]));
+                }
+                const int J0 = n2 * 8 + 2 * ac;
+                double *oa = which == 0 ? AA : BA;
+                if (J0 < MQ) {
+                    oa[(k * MQ + J0) * PM + I] = a0;
+                    if (which == 0) AD[(k * MQ + J0) * PM + I] = d0;
+                }
+                if (J0 + 1 < MQ) {
+                    oa[(k * MQ + J0 + 1) * PM + I] = a1;
+                    if (which == 0) AD[(k * MQ + J0 + 1) * PM + I] = d1;
+                }
+            }
+            __syncthreads();
+            for (int tile = warp; tile < 18 * 2; tile += NW) {          // k: d_r, d_s, d_t and F (rows J,I)
+                const int mt = tile >> 1, n2 = tile & 1, L = mt * 8 + ar, J = L / MQ, I = L % MQ;
+                double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int m = ks * 4 + ac, ix = (m * MQ + J) * PM + I;
+                    mk_dmma(r0, r1, BA[ix], (n2 ? BJ[1][ks] : BJ[0][ks]));
+                    mk_dmma(s0, s1, AD[ix], (n2 ? BJ[1][ks] : BJ[0][ks]));
+                    mk_dmma(q0, q1, AA[ix], (n2 ? BDq[1][ks] : BDq[0][ks]));
+                }
+                const int K0 = n2 * 8 + 2 * ac;
+                if (K0 < MQ) {
+                    const int qq = K0 * MQ * MQ + L;
+                    F[qq] = UT[qq] * r0 + UT[M3 + qq] * s0 + UT[2 * M3 + qq] * q0;
+                }
+                if (K0 + 1 < MQ) {
+                    const int qq = (K0 + 1) * MQ * MQ + L;
+                    F[qq] = UT[qq] * r1 + UT[M3 + qq] * s1 + UT[2 * M3 + qq] * q1;
+                }
+            }
+            __syncthreads();
+            for (int tile = warp; tile < 18; tile += NW) {              // k^T: P1[k][J][I] into AA (rows J,I)
+                const int L = tile * 8 + ar, J = L / MQ, I = L % MQ;
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 3; ++ks) mk_dmma(d0, d1, F[(ks * 4 + ac) * MQ * MQ + L], BT[ks]);
+                const int k0 = 2 * ac;
+                AA[(k0 * MQ + J) * PM + I] = d0;
+                AA[((k0 + 1) * MQ + J) * PM + I] = d1;
+            }
+            __syncthreads();
+            for (int tile = warp; tile < 12; tile += NW) {              // j^T: P2[k][j][I] into SA (rows k,I)
+                const int row = tile * 8 + ar, k = row / MQ, I = row % MQ;
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 3; ++ks) mk_dmma(d0, d1, AA[(k * MQ + ks * 4 + ac) * PM + I], BT[ks]);
+                const int j0 = 2 * ac;
+                SA[(k * NQ + j0) * PM + I] = d0;
+                SA[(k * NQ + j0 + 1) * PM + I] = d1;
+            }
+            __syncthreads();
+            double *fo = (c == 0 ? f0 : c == 1 ? f1 : f2) + e * P3;
+            for (int tile = warp; tile < 8; tile += NW) {               // i^T: out[k][j][i] = -sum_I J[I][i] P2
+                const int L = tile * 8 + ar;
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 3; ++ks) mk_dmma(d0, d1, SA[L * PM + ks * 4 + ac], BT[ks]);
+                const int i0 = 2 * ac;
+                fo[L * NQ + i0] = -d0;
+                fo[L * NQ + i0 + 1] = -d1;
+            }
+            __syncthreads();
+        }
+    }
+}
+
 // Variant with the three velocity components merged in every stage (9 barriers per element instead
 // of 26, 192..576 lines per stage): one CTA per SM, the whole 12^3 working set of an element (values,
 // contravariant velocity and the three integrands) resident in shared memory (226 KB at N = 7).
@@ -694,8 +906,9 @@ static int makef_variant()
 {
     static int v = -1;
     if (v < 0) {
-        // 0: per-component stages, two CTAs per SM (default, measured fastest); 1 / 2: components merged
-        // in every stage, one CTA per SM with 256 / 384 threads
+        // 0: per-component stages, two CTAs per SM (default; N = 7 on the FP64 tensor cores); 1 / 2:
+        // components merged in every stage, one CTA per SM with 256 / 384 threads; 3: the FMA stages at
+        // N = 7 too
         const char *env = getenv("NEK_MAKEF_VARIANT");
         v = env ? atoi(env) : 0;
     }
@@ -713,15 +926,28 @@ static cudaError_t apply_launch(int64_t E, const double *G9, const double *u0, c
     }
     using C = MK<NQ>;
     const size_t smem = sizeof(double) * C::SMEM_D;
+    int per_sm = (int)((227 * 1024) / (smem + 1024));
+    per_sm = std::max(1, std::min(per_sm, 2048 / C::NT));
+    const int grid = (int)std::min<int64_t>(E, (int64_t)device_sms() * per_sm);
+    if constexpr (NQ == 8) {
+        if (makef_variant() != 3) {   // N = 7: FP64 tensor cores (NEK_MAKEF_VARIANT = 3: the FMA kernel)
+            static bool attr_m = false;
+            if (!attr_m) {
+                cudaError_t e = cudaFuncSetAttribute(makef_mma_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)smem);
+                if (e != cudaSuccess) return e;
+                attr_m = true;
+            }
+            makef_mma_kernel<NQ><<<grid, C::NT, smem, s>>>(E, G9, u0, u1, u2, f0, f1, f2);
+            return cudaGetLastError();
+        }
+    }
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(makef_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    int per_sm = (int)((227 * 1024) / (smem + 1024));
-    per_sm = std::max(1, std::min(per_sm, 2048 / C::NT));
-    const int grid = (int)std::min<int64_t>(E, (int64_t)device_sms() * per_sm);
     makef_kernel<NQ><<<grid, C::NT, smem, s>>>(E, G9, u0, u1, u2, f0, f1, f2);
     return cudaGetLastError();
 }

@@ -1,6 +1,8 @@
 mkdir -p gpurun_out
-R="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
-timeout 900 python -m pytest tests/test_gpu_loopback.py -q -x > gpurun_out/g4_loop.log 2>&1; echo "loop $?" >> gpurun_out/g4_summary.txt
-timeout 600 $R --nproc-per-node 4 --master-port 29662 bench.py --gpus 4 --no-pmg --no-peaks > gpurun_out/g4_bench4.json 2> gpurun_out/g4_bench4.err; echo "bench4 $?" >> gpurun_out/g4_summary.txt
-timeout 600 $R --nproc-per-node 2 --master-port 29664 bench.py --gpus 2 --no-pmg --no-peaks > gpurun_out/g4_bench2.json 2> gpurun_out/g4_bench2.err; echo "bench2 $?" >> gpurun_out/g4_summary.txt
-timeout 600 $R --nproc-per-node 4 --master-port 29665 tools/mgpu_timeline.py --graph --iters 20 > gpurun_out/g4_timeline.log 2>&1; echo "timeline $?" >> gpurun_out/g4_summary.txt
+timeout 600 python -m pytest tests/test_gpu_makef.py -q > gpurun_out/i1_makef.log 2>&1; echo "makef $?" >> gpurun_out/i1_summary.txt
+timeout 300 python tools/makef_bench.py > gpurun_out/i1_makef_bench.log 2>&1; echo "mkbench $?" >> gpurun_out/i1_summary.txt
+NEK_MAKEF_VARIANT=3 timeout 300 python tools/makef_bench.py > gpurun_out/i1_makef_bench3.log 2>&1; echo "mkbench3 $?" >> gpurun_out/i1_summary.txt
+timeout 600 python bench.py --mesh rod --no-pmg --no-beyond --no-cpu-baseline --steps 5 > gpurun_out/h1_rod.json 2> gpurun_out/h1_rod.err; echo "rod $?" >> gpurun_out/i1_summary.txt
+timeout 600 python bench.py --mesh rod --h2 100 --no-pmg --no-beyond --no-cpu-baseline --steps 5 > gpurun_out/h1_rod_h.json 2> gpurun_out/h1_rod_h.err; echo "rodh $?" >> gpurun_out/i1_summary.txt
+timeout 900 python bench.py --mesh cfg3 --no-pmg --no-beyond --no-cpu-baseline --steps 3 > gpurun_out/h1_cfg3.json 2> gpurun_out/h1_cfg3.err; echo "cfg3 $?" >> gpurun_out/i1_summary.txt
+timeout 900 python tools/nsweep.py > gpurun_out/h1_nsweep.log 2>&1; echo "nsweep $?" >> gpurun_out/i1_summary.txt
