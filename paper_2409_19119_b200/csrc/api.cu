@@ -366,6 +366,16 @@ static int gs_full(nek_ctx *ctx, T *v, const int *done)
 // w = M QQ^T (h1 K_L + h2 B_L) M u.  With dot: this rank's <M u, A_L M u> into
 // red_loc[RED_SIGMA] (then allgathered across ranks into red_all).  fused: the
 // PCG direction / deferred x update is applied in the Ax prologue (u == vp).
+static bool use_fused(const nek_ctx *ctx) { return ax_has_fused(ctx->variant, ctx->N); }
+
+// deferred reductions: one rank, the fused v5 kernel.  The Ax leaves its sigma partials for the update
+// (no last-CTA fold) and folds the update's (rho', rr) partials at entry (no last-CTA bookkeeping).
+static bool use_defer(const nek_ctx *ctx)
+{
+    return ctx->defer && ctx->nranks == 1 && ctx->E > 0 && use_fused(ctx) &&
+           ax_is_v5(ax_effective_variant(ctx->variant, ctx->N, true, ctx->l2keep), ctx->N);
+}
+
 static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, bool dot, const int *done,
                     bool fused = false)
 {
@@ -383,6 +393,9 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     if (ctx->nranks == 1) {
         L.nelem = ctx->E;
         if (dot) { L.part = ctx->part; L.fin_total = ax_grid(var, ctx->N, ctx->E); }
+        if (dot && fused && use_defer(ctx)) {
+            L.fin_total = 0; L.upart = ctx->upart; L.nupd = upd_blocks(); L.hist = ctx->hist;
+        }
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         return do_gs_local(ctx, w, done);
     }
@@ -885,6 +898,11 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         }
     }
     CK(dalloc(ctx, &ctx->part, ctx->npart));
+    CK(dalloc(ctx, &ctx->upart, 4 * (int64_t)upd_blocks()));
+    {
+        const char *denv = getenv("NEK_DEFER");
+        ctx->defer = !(denv && std::strcmp(denv, "0") == 0);
+    }
     CK(dalloc(ctx, &ctx->red_loc, RED_N));
     if (ctx->nranks > 1) CK(dalloc(ctx, &ctx->red_all, RED_N * ctx->nranks));
     else ctx->red_all = ctx->red_loc;
@@ -1021,8 +1039,6 @@ int nek_gs(nek_ctx *ctx, double *v, void *stream)
     return NEK_OK;
 }
 
-static bool use_fused(const nek_ctx *ctx) { return ax_has_fused(ctx->variant, ctx->N); }
-
 // one PCG iteration (device-resident, skipped once sc->done is set)
 static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
 {
@@ -1048,6 +1064,18 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
             CK(launch_pcg_fin_p2p(ctx->sc, m, ctx->hist, ctx->s_main));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
+        return NEK_OK;
+    }
+    if (use_defer(ctx)) {
+        // Ax: fold the last update's (rho', rr), bookkeeping, p and deferred x, w = A p, sigma partials;
+        // update: fold sigma, r -= alpha w, (rho', rr) partials -- no last-CTA work in either
+        if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
+        const int var = ax_effective_variant(ctx->variant, ctx->N, true, ctx->l2keep);
+        Scope sc(ctx, CLS_VEC);
+        CK(launch_pcg_update_deferred(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->part,
+                                      (int)ax_grid(var, ctx->N, ctx->E), ctx->sc, ctx->upart, upd_blocks(),
+                                      ctx->l2keep, ctx->s_main));
+        ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         return NEK_OK;
     }
     if (use_fused(ctx)) {
@@ -1191,6 +1219,10 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
             CK(cudaStreamSynchronize(ctx->s_main));
             if (H->done) break;
         }
+    }
+    if (use_defer(ctx)) {   // the last update's (rho', rr) when no Ax followed it
+        CK(launch_pcg_defer_finish(ctx->sc, ctx->upart, upd_blocks(), ctx->hist, ctx->s_main));
+        ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
     if (use_fused(ctx)) {   // the deferred x += alpha p of the last iteration
         CK(launch_pcg_xfinal(ctx->n, ctx->sc, ctx->vp, ctx->vx, ctx->s_main));

@@ -26,6 +26,10 @@ struct PcgScalars {
     double sigma;      // global <p, A p> of the current iteration (P2P path)
     double alpha;      // alpha of the last update whose x += alpha p is still pending (fused path)
     double beta;       // beta for the next direction update (fused path)
+    // deferred reductions (single rank, N = 7): the update leaves its dot partials, the next Ax folds them
+    double rho_next;   // rho for the next update's alpha (written by the Ax that folded the partials)
+    int fold_ready;    // 1 once an update has left partials (the next Ax folds them)
+    int booked;        // iterations whose (rho', rr) the bookkeeping has recorded
 };
 
 // NVLink peer mailbox of a rank: [channel][epoch parity][rank][4] doubles, slot 3 = epoch.
@@ -86,6 +90,12 @@ struct AxLaunch {
     const PcgScalars *sc = nullptr;
     int keep = 0;                        // L2-resident mode: bit 0 p, r, Dinv, w; bit 1 also x
     int64_t grid = 0;                    // > 0: CTAs of this launch (v5), else ax_grid
+    // deferred reductions (single rank, fused v5): fold the previous update's nupd dot partials at entry
+    // (upart: [nupd][4] = (hi, lo) of <r, Dinv r> and <r, r>) and leave this launch's sigma partials
+    // unfolded for the update
+    const double *upart = nullptr;
+    int nupd = 0;
+    double *hist = nullptr;
     int variant = -1;                    // >= 0: the Ax variant of this launch (overrides the context's)
 };
 cudaError_t launch_ax(int variant, int N, const AxLaunch &L, const double *u, const double *G, const double *wJ,
@@ -133,6 +143,13 @@ cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const doub
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
                                     const P2PMail *mail = nullptr, int keep = 0);
+// deferred reductions (single rank, N = 7): sigma folded from the Ax's nax partials at entry, (rho', rr)
+// partials left in upart ([nblk][4]) for the next Ax or for pcg_defer_finish
+cudaError_t launch_pcg_update_deferred(int64_t n, const uint32_t *obits, const double *dinv, const double *w,
+                                       double *r, const double *axpart, int nax, PcgScalars *sc, double *upart,
+                                       int nblk, int keep, cudaStream_t s);
+// the bookkeeping of the last update of a solve when no Ax followed it
+cudaError_t launch_pcg_defer_finish(PcgScalars *sc, const double *upart, int nupd, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
 // device ranges whose L2 lines are demoted from evict_last after an L2-resident solve
 struct L2Ranges {
@@ -164,6 +181,7 @@ cudaError_t launch_gs_classes_unpack(const GsClasses &C, const HaloUnpack &U, T 
 cudaError_t launch_pcg_iter_fin(PcgScalars *sc, const double *red_all, int nranks, double *hist, cudaStream_t s);
 cudaError_t launch_pcg_xfinal(int64_t n, const PcgScalars *sc, const double *p, double *x, cudaStream_t s);
 bool ax_has_fused(int variant, int N);
+bool ax_is_v5(int variant, int N);   // the N = 7 v5 kernel (the only one with the deferred-reduction entry)
 // projection space (NEXT #2)
 constexpr int PROJ_MAX_VECTORS = 32;
 cudaError_t launch_multidot(int64_t n, int l, const double *V, const double *y, const uint32_t *obits,
@@ -245,6 +263,8 @@ struct nek_ctx {
     int32_t *gs_p2 = nullptr, *gs_p4 = nullptr, *gs_p8 = nullptr, *gs_pg = nullptr, *gs_og = nullptr;
     int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
     bool bnd_split = true;                          // concurrent boundary/interior Ax share one wave of CTAs
+    bool defer = true;                              // deferred reductions on the single-rank v5 path (NEK_DEFER)
+    double *upart = nullptr;                        // [upd_blocks][4] update partials the next Ax folds
     int64_t l2_setaside = 0, l2_setaside_max = 0;   // persisting L2 bytes granted / allowed
     bool concurrent_bnd = false;
     bool owns_streams = true, owns_nccl = true;   // false for the internal pMG level contexts

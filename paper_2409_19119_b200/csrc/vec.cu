@@ -164,6 +164,9 @@ __global__ void pcg_init_fin_kernel(PcgScalars *sc, const double *red_all, int n
     sc->done = 0;
     sc->alpha = 0.0;
     sc->beta = 0.0;
+    sc->rho_next = rho;
+    sc->fold_ready = 0;
+    sc->booked = 0;
     if (hist) hist[0] = rr > 0.0 ? 1.0 : 0.0;
     if (!(rr > 0.0)) { sc->done = 1; sc->status = NEK_OK; }              // b = 0 -> x = 0, 0 iterations
     else if (sc->tol >= 1.0) { sc->done = 1; sc->status = NEK_OK; }      // ||r0|| <= tol ||b||
@@ -431,6 +434,125 @@ cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const doub
     else
         pcg_update_fused_kernel<4, 2><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
                                                                    part, dst, counter, m, keep);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------ deferred reductions (single rank)
+// The residual update of the single-rank N = 7 path without last-CTA work: every CTA folds the Ax
+// launch's sigma partials itself (the same fixed order in every CTA, while its first tile of w, r, Dinv
+// is in flight), and leaves its own (rho', rr) partials; the next Ax launch folds those at entry and does
+// the bookkeeping (ax.cu), or pcg_defer_finish does after the last update of a solve.  Every value is
+// computed as on the last-CTA path; only the grouping of the double-double folds differs (within an ulp).
+// No kernel writes a scalar that another CTA of the same launch reads at entry: the update counts the
+// iteration (sc->iter), the Ax that folds its partials records them (sc->booked, history, convergence).
+__device__ __forceinline__ double fold_pairs(const double *part, int count, double *sred)
+{
+    double hi = 0.0, lo = 0.0;
+    for (int c = threadIdx.x; c < count; c += blockDim.x) dd_add(hi, lo, part[2 * c], part[2 * c + 1]);
+    block_sum_dd(hi, lo, sred);
+    return __dadd_rn(hi, lo);
+}
+
+__global__ void __launch_bounds__(VEC_THREADS, 2)
+    pcg_update_deferred_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
+                               const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ axpart,
+                               int nax, PcgScalars *sc, double *__restrict__ upart, int keep)
+{
+    __shared__ double sred[VEC_THREADS];
+    __shared__ double s_sig;
+    constexpr int UNR = 4;
+    const uint64_t pol = tma::policy_keep(keep & 1);
+    const int64_t n2 = n >> 1;
+    const int64_t tile = (int64_t)UNR * blockDim.x;
+    int64_t base = blockIdx.x * tile + threadIdx.x;
+    double2 wv[UNR], dv[UNR], rv[UNR];
+    uint32_t ow[UNR];
+    auto load = [&](int64_t b0) {
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+            const int64_t h = b0 + (int64_t)q * blockDim.x;
+            if (h < n2) {
+                wv[q] = tma::ld2(w + 2 * h, pol); dv[q] = tma::ld2(dinv + 2 * h, pol); rv[q] = tma::ld2(r + 2 * h, pol);
+                ow[q] = tma::ldu(obits + ((2 * h) >> 5), pol) >> ((2 * h) & 31);
+            }
+        }
+    };
+    load(base);
+    const double rho = sc->rho_next;
+    if (*(volatile int *)&sc->done) return;
+    const double sg = fold_pairs(axpart, nax, sred);   // sigma of the Ax launch, folded in every CTA
+    if (threadIdx.x == 0) s_sig = sg;
+    __syncthreads();
+    const double sigma = s_sig;
+    if (!(sigma > 0.0)) {                       // breakdown: <p, A p> <= 0
+        if (blockIdx.x == 0 && threadIdx.x == 0) { sc->status = NEK_ENOTSPD; sc->alpha = 0.0; sc->done = 1; }
+        return;
+    }
+    const double alpha = rho / sigma;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {   // the Ax launch is complete: rho moves on, alpha is pending
+        sc->iter = sc->iter + 1;
+        sc->rho = rho;
+        sc->alpha = alpha;
+        sc->sigma = sigma;
+        sc->fold_ready = 1;
+    }
+    double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0, g0 = 0.0, k0 = 0.0, g1 = 0.0, k1 = 0.0;
+    for (bool first = true; base < n2; base += (int64_t)gridDim.x * tile, first = false) {
+        if (!first) load(base);
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+            const int64_t h = base + (int64_t)q * blockDim.x;
+            if (h < n2) {
+                rv[q].x = fma(-alpha, wv[q].x, rv[q].x); rv[q].y = fma(-alpha, wv[q].y, rv[q].y);
+                tma::st2(r + 2 * h, rv[q], pol);
+                if (ow[q] & 1u) { dd_add_prod(h0, l0, rv[q].x, __dmul_rn(dv[q].x, rv[q].x)); dd_add_prod(h1, l1, rv[q].x, rv[q].x); }
+                if (ow[q] & 2u) { dd_add_prod(g0, k0, rv[q].y, __dmul_rn(dv[q].y, rv[q].y)); dd_add_prod(g1, k1, rv[q].y, rv[q].y); }
+            }
+        }
+    }
+    if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        const int64_t l = n - 1;
+        const double rl = fma(-alpha, w[l], r[l]);
+        r[l] = rl;
+        if (bit_of(obits, l)) { dd_add_prod(h0, l0, rl, __dmul_rn(dinv[l], rl)); dd_add_prod(h1, l1, rl, rl); }
+    }
+    dd_add(h0, l0, g0, k0);
+    dd_add(h1, l1, g1, k1);
+    store_part2(upart, h0, l0, h1, l1, sred);
+}
+
+cudaError_t launch_pcg_update_deferred(int64_t n, const uint32_t *obits, const double *dinv, const double *w,
+                                       double *r, const double *axpart, int nax, PcgScalars *sc, double *upart,
+                                       int nblk, int keep, cudaStream_t s)
+{
+    pcg_update_deferred_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, axpart, nax, sc, upart, keep);
+    return cudaGetLastError();
+}
+
+// after the last update of a solve when no Ax followed it: fold its partials and book the iteration
+__global__ void __launch_bounds__(VEC_THREADS) pcg_defer_finish_kernel(PcgScalars *sc, const double *upart,
+                                                                      int nupd, double *hist)
+{
+    __shared__ double sred[VEC_THREADS];
+    if (*(volatile int *)&sc->done || !*(volatile int *)&sc->fold_ready || sc->booked >= sc->iter) return;
+    double a0, a1;
+    fold_part2(upart, nupd, sred, a0, a1);
+    if (threadIdx.x == 0) {
+        const int it = sc->iter;
+        sc->booked = it;
+        sc->rr = a1;
+        if (hist) hist[it] = sqrt(a1) / sc->bb;
+        sc->beta = a0 / sc->rho;
+        sc->rho_next = a0;
+        if (sqrt(a1) <= sc->tol * sc->bb) { sc->done = 1; sc->status = NEK_OK; }
+        else if (it >= sc->maxit) { sc->done = 1; sc->status = NEK_MAXIT; }
+        __threadfence();
+    }
+}
+
+cudaError_t launch_pcg_defer_finish(PcgScalars *sc, const double *upart, int nupd, double *hist, cudaStream_t s)
+{
+    pcg_defer_finish_kernel<<<1, VEC_THREADS, 0, s>>>(sc, upart, nupd, hist);
     return cudaGetLastError();
 }
 

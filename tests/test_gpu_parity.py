@@ -505,3 +505,43 @@ def test_pcg_l2_resident_bitwise(nek, keep):
     x1, it1, h1 = res[keep]
     assert it1 == it0 and np.array_equal(x1, x0) and np.array_equal(h1, h0)
 
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_pcg_deferred_reductions_match(nek, graph):
+    """Deferred reductions (single rank, N = 7 v5: the next Ax folds the update's dot partials, no
+    last-CTA work) against the last-CTA path (NEK_DEFER=0): the same iteration counts and statuses for
+    fixed windows that end on an update (maxit a multiple of the graph length: the finish kernel books
+    it) or mid-graph, for converged solves and for the breakdown; histories and x agree to the
+    double-double fold regrouping (<= 1e-13)."""
+    m = mg.box_mesh(5, 4, 3, 7, deform="bubble")
+    b = mg.smooth_field(m, seed=12)
+    runs = {}
+    for d in ("0", "1"):
+        os.environ["NEK_DEFER"] = d
+        try:
+            ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+        finally:
+            os.environ.pop("NEK_DEFER", None)
+        if graph == "0":
+            os.environ["NEK_NO_GRAPH"] = "1"
+        try:
+            out = []
+            for tol, maxit in ((0.0, 20), (0.0, 7), (0.0, 1), (1e-9, 400), (1e-9, 30), (0.0, 0)):
+                x = np.zeros(m.n_local)
+                st, it, rr, hg = nek.pcg_solve(ctx, 1.0, 0.0, b, x, tol, maxit, want_hist=True)
+                out.append((st, it, rr, hg, x))
+            with pytest.raises(nek.NekError) as ei:
+                nek.pcg_solve(ctx, -1.0, 0.0, b, np.zeros(m.n_local), 1e-10, 10)
+            out.append(ei.value.code)
+            runs[d] = out
+        finally:
+            os.environ.pop("NEK_NO_GRAPH", None)
+            nek.free(ctx)
+    assert runs["0"][-1] == runs["1"][-1] == nek.ENOTSPD
+    for (s0, i0, r0, h0, x0), (s1, i1, r1, h1, x1) in zip(runs["0"][:-1], runs["1"][:-1]):
+        assert (s1, i1) == (s0, i0)
+        assert len(h1) == len(h0) == i0 + 1
+        assert np.all(np.abs(h1 - h0) <= 1e-13 * np.maximum(1.0, h0))
+        assert abs(r1 - r0) <= 1e-13 * max(1.0, r0)
+        assert rel(x1, x0) <= 1e-13
