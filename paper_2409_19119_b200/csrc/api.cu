@@ -376,6 +376,14 @@ static bool use_defer(const nek_ctx *ctx)
            ax_is_v5(ax_effective_variant(ctx->variant, ctx->N, true, ctx->l2keep), ctx->N);
 }
 
+// the same at P > 1 over peer memory: the update pushes this rank's (rho', rr) as before, and the next
+// Ax pulls every rank's from the mailbox at entry instead of a separate bookkeeping kernel
+static bool use_defer_p2p(const nek_ctx *ctx)
+{
+    return ctx->defer && ctx->nranks > 1 && ctx->p2p && use_fused(ctx) && ctx->N == 7 &&
+           ax_is_v5(ax_effective_variant(ctx->variant, ctx->N, true, ctx->l2keep), ctx->N);
+}
+
 static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double *w, bool dot, const int *done,
                     bool fused = false)
 {
@@ -395,6 +403,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         if (dot) { L.part = ctx->part; L.fin_total = ax_grid(var, ctx->N, ctx->E); }
         if (dot && fused && use_defer(ctx)) {
             L.fin_total = 0; L.upart = ctx->upart; L.nupd = upd_blocks(); L.hist = ctx->hist;
+            L.defer = DEFER_FOLD | DEFER_BOOK;
         }
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         return do_gs_local(ctx, w, done);
@@ -418,6 +427,12 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     }
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
     L.elist = ctx->elist;
+    // deferred bookkeeping (P2P): every CTA of both launches pulls (rho', rr); the first launch that has
+    // elements records the iteration
+    const int dbase = (fused && dot && use_defer_p2p(ctx)) ? DEFER_MAIL : 0;
+    if (dbase) { L.mail = mail_of(ctx); L.hist = ctx->hist; }
+    auto set_defer = [&](bool first) { L.defer = dbase ? (dbase | (first ? DEFER_BOOK : 0)) : 0; };
+    const bool book_bnd = nb > 0;
     {
     Scope span(ctx, CLS_AXU);   // the whole Ax phase (both launches and the send), for the union time
     ctx->stats.axu_spans += 1;
@@ -428,9 +443,11 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         if (dot) { L.part = ctx->part; L.fin_total = g1 + g2; L.ctas_total = (unsigned)(g1 + g2); }
         if (push) L.mail = mail_of(ctx);
         L.nelem = nb; L.eoff = 0; L.part_off = 0;
+        set_defer(book_bnd);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
         L.nelem = ni; L.eoff = nb; L.part_off = g1;
+        set_defer(!book_bnd);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
     } else if (ax_has_fused(ctx->variant, ctx->N)) {
         // Boundary elements and the halo send on the high-priority stream, interior elements on
@@ -441,17 +458,20 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         if (push) L.mail = mail_of(ctx);
         L.nelem = nb; L.eoff = 0; L.part_off = 0;
         if (split) L.grid = g1;
+        set_defer(book_bnd);
         if ((st = do_ax(ctx, h1, h2, u, w, L, ctx->s_hi)) != NEK_OK) return st;
         if ((st = halo_start(ctx, w, done, ctx->s_hi)) != NEK_OK) return st;
         CK(cudaEventRecord(ctx->ev_bnd, ctx->s_hi));
         L.nelem = ni; L.eoff = nb; L.part_off = g1;
         if (split) L.grid = g2;
+        set_defer(!book_bnd);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         CK(cudaStreamWaitEvent(ctx->s_main, ctx->ev_bnd, 0));
     } else {
         L.nelem = nb;
         if (dot) { L.part = ctx->part; L.part_off = 0; L.fin_total = ni > 0 ? 0 : g1; }
         if (push && ni == 0) L.mail = mail_of(ctx);
+        set_defer(book_bnd);
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         if ((st = halo_start(ctx, w, done)) != NEK_OK) return st;
         if (ni > 0) {
@@ -459,6 +479,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
             L.eoff = nb;
             if (dot) { L.part_off = g1; L.fin_total = g1 + g2; }
             if (push) L.mail = mail_of(ctx);
+            set_defer(!book_bnd);
             if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
         }
     }
@@ -1047,7 +1068,10 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
     const int nb = vec_blocks();
     if (use_fused(ctx) && ctx->p2p) {
         // sigma pushed by the Ax kernel, pulled by the update kernel; (rho', rr) pushed by the
-        // update kernel, pulled by the bookkeeping kernel: no separate exchange launches
+        // update kernel, pulled by the bookkeeping kernel (or, deferred, by the next Ax): no
+        // separate exchange launches
+        const bool dp = use_defer_p2p(ctx);
+        if (dp && (st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;   // loopback: (rho', rr) pushed
         if ((st = apply_op(ctx, h1, h2, ctx->vp, ctx->vw, true, done, true)) != NEK_OK) return st;
         const P2PMail m = mail_of(ctx);
         if ((st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;   // loopback: every rank pushed sigma
@@ -1055,9 +1079,10 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, &m, ctx->l2keep));
+                                       ctx->counter + 2, ctx->s_main, &m, ctx->l2keep, dp ? 1 : 0));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
+        if (dp) return NEK_OK;
         if ((st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;   // loopback: every rank pushed (rho', rr)
         {
             Scope sc(ctx, CLS_VEC);
@@ -1222,6 +1247,11 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     }
     if (use_defer(ctx)) {   // the last update's (rho', rr) when no Ax followed it
         CK(launch_pcg_defer_finish(ctx->sc, ctx->upart, upd_blocks(), ctx->hist, ctx->s_main));
+        ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
+    } else if (use_defer_p2p(ctx)) {
+        if ((st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;   // loopback: (rho', rr) pushed
+        const P2PMail m = mail_of(ctx);
+        CK(launch_pcg_defer_finish(ctx->sc, nullptr, 0, ctx->hist, ctx->s_main, &m));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     }
     if (use_fused(ctx)) {   // the deferred x += alpha p of the last iteration

@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(128, MINB)
                  int64_t fin_total, double *__restrict__ dst, unsigned int *counter, const int *__restrict__ done,
                  double *pvec, double *__restrict__ xvec, const double *__restrict__ rvec,
                  const double *__restrict__ dvec, PcgScalars *sc, P2PMail mail, unsigned int ctas_total,
-                 int keep, const double *__restrict__ upart, int nupd, double *hist)
+                 int keep, const double *__restrict__ upart, int nupd, double *hist, int defer)
 {
     constexpr int P3 = 512, N = 7;
     __shared__ AxV5Smem S;
@@ -278,25 +278,30 @@ __global__ void __launch_bounds__(128, MINB)
     }
     if (FUSED) { beta = sc->beta; alpha = sc->alpha; }   // issued beside the done load, not after it
     bool stop = done && *(volatile const int *)done;
-    if (FUSED && upart && !stop && *(volatile const int *)&sc->fold_ready) {
-        // deferred reductions (single rank): fold the previous update's (rho', rr) partials -- the same
-        // fixed order in every CTA -- and take beta and the convergence decision from them; CTA 0 records
-        // the iteration (vec.cu, pcg_update_deferred_kernel)
+    if (FUSED && defer && !stop && *(volatile const int *)&sc->fold_ready) {
+        // deferred reductions: the previous update's (rho', rr) -- folded from its CTA partials in the
+        // same fixed order in every CTA (single rank, DEFER_FOLD), or every rank's pushed totals pulled
+        // from the mailbox in rank order (P2P, DEFER_MAIL) -- give beta and the convergence decision
+        // here; CTA 0 of the booking launch records the iteration (vec.cu, the deferred updates)
         const double rho_old = sc->rho, bb = sc->bb, tol = sc->tol;
         const int it = sc->iter, maxit = sc->maxit;
-        double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
-        for (int c = t; c < nupd; c += blockDim.x) {
-            dd_add(h0, l0, upart[4 * c], upart[4 * c + 1]);
-            dd_add(h1, l1, upart[4 * c + 2], upart[4 * c + 3]);
+        if (defer & DEFER_MAIL) {
+            if (t < 32) mail_pull_warp(mail, 1, &S.sred[64]);
+        } else {
+            double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
+            for (int c = t; c < nupd; c += blockDim.x) {
+                dd_add(h0, l0, upart[4 * c], upart[4 * c + 1]);
+                dd_add(h1, l1, upart[4 * c + 2], upart[4 * c + 3]);
+            }
+            block_sum_dd(h0, l0, S.sred);
+            block_sum_dd(h1, l1, S.sred);
+            if (t == 0) { S.sred[64] = __dadd_rn(h0, l0); S.sred[65] = __dadd_rn(h1, l1); }
         }
-        block_sum_dd(h0, l0, S.sred);
-        block_sum_dd(h1, l1, S.sred);
-        if (t == 0) { S.sred[64] = __dadd_rn(h0, l0); S.sred[65] = __dadd_rn(h1, l1); }
         __syncthreads();
         const double rho1 = S.sred[64], rr = S.sred[65];
         const bool conv = sqrt(rr) <= tol * bb;
         stop = conv || it >= maxit;
-        if (blockIdx.x == 0 && t == 0) {
+        if ((defer & DEFER_BOOK) && blockIdx.x == 0 && t == 0) {
             sc->booked = it;
             sc->rr = rr;
             if (hist) hist[it] = sqrt(rr) / bb;
@@ -510,11 +515,11 @@ static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double
         ax_v5_kernel<HELM, true, MINB, TMAG><<<(unsigned)grid, 128, dsm, s>>>(
             L.nelem, L.eoff, L.elist, (const double *)L.p, G, wJ, mbits, h1, h2, w, L.part, L.part_off, L.fin_total,
             L.dst, L.counter, L.done, L.p, L.x, L.r, L.dinv, const_cast<PcgScalars *>(L.sc), L.mail, ctas, L.keep,
-            L.upart, L.nupd, L.hist);
+            L.upart, L.nupd, L.hist, L.defer);
     else
         ax_v5_kernel<HELM, false, MINB, TMAG><<<(unsigned)grid, 128, dsm, s>>>(
             L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w, L.part, L.part_off, L.fin_total, L.dst, L.counter,
-            L.done, nullptr, nullptr, nullptr, nullptr, nullptr, L.mail, ctas, L.keep, nullptr, 0, nullptr);
+            L.done, nullptr, nullptr, nullptr, nullptr, nullptr, L.mail, ctas, L.keep, nullptr, 0, nullptr, 0);
     return cudaGetLastError();
 }
 

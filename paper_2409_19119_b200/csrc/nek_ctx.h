@@ -72,6 +72,10 @@ cudaError_t launch_geom(int N, int64_t E, const double *xyz, double *G, double *
 // One Ax launch over elements [eoff, eoff + nelem) of `elist` (or of 0..E-1 when
 // elist is NULL).  part/part_off: where its per-CTA <u, w> partials go; when
 // fin_total > 0 the launch also reduces part[0..fin_total) into dst[0].
+// deferred-reduction modes of the fused v5 Ax (AxLaunch::defer): where the previous update's (rho', rr)
+// come from, and whether this launch's CTA 0 records the iteration (one launch per operator application)
+enum { DEFER_FOLD = 1, DEFER_MAIL = 2, DEFER_BOOK = 4 };
+
 struct AxLaunch {
     int64_t nelem = 0, eoff = 0;
     const int32_t *elist = nullptr;
@@ -95,6 +99,7 @@ struct AxLaunch {
     // unfolded for the update
     const double *upart = nullptr;
     int nupd = 0;
+    int defer = 0;   // DEFER_* bits
     double *hist = nullptr;
     int variant = -1;                    // >= 0: the Ax variant of this launch (overrides the context's)
 };
@@ -142,14 +147,15 @@ cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *ob
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail = nullptr, int keep = 0);
+                                    const P2PMail *mail = nullptr, int keep = 0, int defer = 0);
 // deferred reductions (single rank, N = 7): sigma folded from the Ax's nax partials at entry, (rho', rr)
 // partials left in upart ([nblk][4]) for the next Ax or for pcg_defer_finish
 cudaError_t launch_pcg_update_deferred(int64_t n, const uint32_t *obits, const double *dinv, const double *w,
                                        double *r, const double *axpart, int nax, PcgScalars *sc, double *upart,
                                        int nblk, int keep, cudaStream_t s);
 // the bookkeeping of the last update of a solve when no Ax followed it
-cudaError_t launch_pcg_defer_finish(PcgScalars *sc, const double *upart, int nupd, double *hist, cudaStream_t s);
+cudaError_t launch_pcg_defer_finish(PcgScalars *sc, const double *upart, int nupd, double *hist, cudaStream_t s,
+                                    const P2PMail *mail = nullptr);
 cudaError_t launch_pcg_fin_p2p(PcgScalars *sc, const P2PMail &mail, double *hist, cudaStream_t s);
 // device ranges whose L2 lines are demoted from evict_last after an L2-resident solve
 struct L2Ranges {

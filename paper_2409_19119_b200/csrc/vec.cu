@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     pcg_update_fused_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                             const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ red_all,
                             int nranks, PcgScalars *sc, double *hist, double *__restrict__ part, double *dst,
-                            unsigned int *counter, P2PMail mail, int keep)
+                            unsigned int *counter, P2PMail mail, int keep, int defer)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ int s_last;
@@ -361,7 +361,9 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     load(base);
     // the scalars are final when the kernel starts (stream order): their loads are issued together
     // with the convergence flag's instead of after it
-    const double rho0 = sc->rho;
+    // defer (P2P): rho of this iteration is rho_next (the Ax that pulled (rho', rr) set it); CTA 0
+    // counts the iteration and the next Ax records it (ax.cu, DEFER_MAIL)
+    const double rho0 = defer ? sc->rho_next : sc->rho;
     double sigma = (mail.nranks > 1) ? 0.0 : rank_sum(red_all, nranks, RED_SIGMA);
     if (*(volatile int *)&sc->done) return;
     if (mail.nranks > 1) {                       // sigma of every rank from the mailbox (channel 0)
@@ -375,6 +377,12 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
         return;
     }
     const double alpha = rho0 / sigma;
+    if (defer && blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->iter = sc->iter + 1;
+        sc->rho = rho0;
+        sc->alpha = alpha;
+        sc->fold_ready = 1;
+    }
     double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
     double g0 = 0.0, k0 = 0.0, g1 = 0.0, k1 = 0.0;   // the .y points: two independent Dot2 chains per dot
     for (bool first = true; base < n2; base += (int64_t)gridDim.x * tile, first = false) {
@@ -420,20 +428,20 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail, int keep)
+                                    const P2PMail *mail, int keep, int defer)
 {
     P2PMail m;
     if (mail) m = *mail;
     const int per_sm = nblk / device_sms();
     if (per_sm >= 8)
         pcg_update_fused_kernel<2, 8><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
-                                                                   part, dst, counter, m, keep);
+                                                                   part, dst, counter, m, keep, defer);
     else if (per_sm >= 4)
         pcg_update_fused_kernel<2, 4><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
-                                                                   part, dst, counter, m, keep);
+                                                                   part, dst, counter, m, keep, defer);
     else
         pcg_update_fused_kernel<4, 2><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
-                                                                   part, dst, counter, m, keep);
+                                                                   part, dst, counter, m, keep, defer);
     return cudaGetLastError();
 }
 
@@ -531,12 +539,18 @@ cudaError_t launch_pcg_update_deferred(int64_t n, const uint32_t *obits, const d
 
 // after the last update of a solve when no Ax followed it: fold its partials and book the iteration
 __global__ void __launch_bounds__(VEC_THREADS) pcg_defer_finish_kernel(PcgScalars *sc, const double *upart,
-                                                                      int nupd, double *hist)
+                                                                      int nupd, double *hist, P2PMail mail)
 {
     __shared__ double sred[VEC_THREADS];
     if (*(volatile int *)&sc->done || !*(volatile int *)&sc->fold_ready || sc->booked >= sc->iter) return;
     double a0, a1;
-    fold_part2(upart, nupd, sred, a0, a1);
+    if (mail.nranks > 1) {   // P2P: every rank's (rho', rr) from the mailbox (channel 1)
+        if (threadIdx.x < 32) mail_pull_warp(mail, 1, sred);
+        __syncthreads();
+        a0 = sred[0]; a1 = sred[1];
+    } else {
+        fold_part2(upart, nupd, sred, a0, a1);
+    }
     if (threadIdx.x == 0) {
         const int it = sc->iter;
         sc->booked = it;
@@ -550,9 +564,12 @@ __global__ void __launch_bounds__(VEC_THREADS) pcg_defer_finish_kernel(PcgScalar
     }
 }
 
-cudaError_t launch_pcg_defer_finish(PcgScalars *sc, const double *upart, int nupd, double *hist, cudaStream_t s)
+cudaError_t launch_pcg_defer_finish(PcgScalars *sc, const double *upart, int nupd, double *hist, cudaStream_t s,
+                                    const P2PMail *mail)
 {
-    pcg_defer_finish_kernel<<<1, VEC_THREADS, 0, s>>>(sc, upart, nupd, hist);
+    P2PMail m;
+    if (mail) m = *mail;
+    pcg_defer_finish_kernel<<<1, VEC_THREADS, 0, s>>>(sc, upart, nupd, hist, m);
     return cudaGetLastError();
 }
 

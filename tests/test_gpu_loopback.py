@@ -272,3 +272,37 @@ def test_loopback_abort_is_an_error_not_a_hang(nek):
     assert not t.is_alive()
     lb.free()
     assert got.get("code") == nek.ENCCL
+
+
+@pytest.mark.parametrize("mode", ["concurrent", "stream_order", "concurrent_nosplit"])
+def test_loopback_deferred_bookkeeping_bitwise(nek, mode):
+    """P2P deferred bookkeeping (N = 7: the next Ax pulls every rank's (rho', rr) from the mailbox, no
+    separate bookkeeping kernel) against NEK_DEFER=0: the pulled sums are the same values in the same
+    rank order, so statuses, iteration counts, histories and x are bit-identical -- for windows ending
+    on an update (the finish kernel books it), mid-graph, and for a converged solve."""
+    m = mg.box_mesh(4, 3, 6, 7, deform="bubble", dirichlet="all")
+    parts = parts_of(m, "slab", 3)
+    subs = [mg.submesh(m, p) for p in parts]
+    locs = [local_index(m, p) for p in parts]
+    b = mg.smooth_field(m, seed=8)
+
+    def fn(r, comm):
+        s = subs[r]
+        ctx = nek.setup(s.E, s.N, s.xyz, s.gid, s.mask, comm=comm, device=0)
+        try:
+            out = []
+            for tol, maxit in ((0.0, 20), (0.0, 7), (1e-9, 400), (0.0, 0)):
+                x = np.zeros(s.n_local)
+                st, it, rr, hist = nek.pcg_solve(ctx, 1.0, 0.0, b[locs[r]], x, tol, maxit, want_hist=True)
+                out.append((st, it, rr, hist, x))
+            return out
+        finally:
+            nek.free(ctx)
+
+    res = {d: run_ranks(nek, 3, 0, fn, dict(MODES[mode], NEK_DEFER=d)) for d in ("0", "1")}
+    for r in range(3):
+        for (s0, i0, r0, h0, x0), (s1, i1, r1, h1, x1) in zip(res["0"][r], res["1"][r]):
+            assert (s1, i1) == (s0, i0) and r1 == r0
+            assert np.array_equal(h1, h0) and np.array_equal(x1, x0)
+    conv = res["1"][0][2]
+    assert conv[0] == nek.OK and 0 < conv[1] < 400
