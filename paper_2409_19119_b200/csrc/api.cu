@@ -819,6 +819,29 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         ctx->gsc.nv = ctx->n;
         ctx->gsc.p2 = ctx->gs_p2; ctx->gsc.p4 = ctx->gs_p4; ctx->gsc.p8 = ctx->gs_p8;
         ctx->gsc.pg = ctx->gs_pg; ctx->gsc.og = ctx->gs_og;
+        {   // element-chunk offsets of the four classes (runs are in first-copy order within a class)
+            const char *genv = getenv("NEK_GS_CHUNK");
+            if (!(genv && std::strcmp(genv, "0") == 0) && E > 0) {
+                const int64_t K = gs_chunk_elems(), nch = (E + K - 1) / K, S = nch + 1, span = K * ctx->P3;
+                std::vector<int32_t> coff((size_t)(4 * S), 0);
+                auto fill = [&](int k, const std::vector<int32_t> &first) {
+                    int64_t r = 0;
+                    for (int64_t c = 0; c <= nch; ++c) {
+                        while (r < (int64_t)first.size() && first[r] < c * span) ++r;
+                        coff[(size_t)(k * S + c)] = (int32_t)r;
+                    }
+                    coff[(size_t)(k * S + nch)] = (int32_t)first.size();
+                };
+                std::vector<int32_t> f2, f4, f8, fg;
+                for (size_t r = 0; r < c2.size(); r += 2) f2.push_back(c2[r]);
+                for (size_t r = 0; r < c4.size(); r += 4) f4.push_back(c4[r]);
+                for (size_t r = 0; r < c8.size(); r += 8) f8.push_back(c8[r]);
+                for (size_t r = 0; r + 1 < og.size(); ++r) fg.push_back(cg[og[r]]);
+                fill(0, f2); fill(1, f4); fill(2, f8); fill(3, fg);
+                CK(upload(ctx, &ctx->gs_coff, coff));
+                ctx->gsc.coff = ctx->gs_coff; ctx->gsc.nchunk = nch;
+            }
+        }
         // boundary Ax + halo send beside the interior Ax (concurrent streams) pays off for small
         // per-rank problems, where the boundary launch alone would leave most SMs idle; for large
         // ones the send must not queue behind the persistent interior grid (measured)
@@ -980,7 +1003,8 @@ int nek_free(nek_ctx *ctx)
                     (void *)ctx->vx, (void *)ctx->vdinv, (void *)ctx->vtmp, (void *)ctx->stage_in,
                     (void *)ctx->stage_out, (void *)ctx->part, (void *)ctx->red_loc, (void *)ctx->sc,
                     (void *)ctx->counter, (void *)ctx->hist, (void *)ctx->gs_p2, (void *)ctx->gs_p4,
-                    (void *)ctx->gs_p8, (void *)ctx->gs_pg, (void *)ctx->gs_og})
+                    (void *)ctx->gs_p8, (void *)ctx->gs_pg, (void *)ctx->gs_og, (void *)ctx->gs_coff,
+                    (void *)ctx->upart})
         if (p) cudaFree(p);
     if (ctx->red_all && ctx->red_all != ctx->red_loc) cudaFree(ctx->red_all);
     for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);

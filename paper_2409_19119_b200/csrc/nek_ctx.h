@@ -121,8 +121,13 @@ struct GsClasses {
     int64_t nv = 0;                      // length of the vector the runs index (checked build)
     const int32_t *p2 = nullptr, *p4 = nullptr, *p8 = nullptr, *pg = nullptr, *og = nullptr;
     int keep = 0;                        // L2 evict_last on the index lists and values (L2-resident mode)
+    // element-chunk order (gs_chunk_kernel): coff[k * (nchunk + 1) + c] = first run of class k (pairs,
+    // quads, octets, other) whose first copy lies in element chunk c; nullptr: class-major kernel
+    const int32_t *coff = nullptr;
+    int64_t nchunk = 0;
 };
 template <class T> cudaError_t launch_gs_classes(const GsClasses &C, T *v, const int *done, cudaStream_t s);
+int gs_chunk_elems();   // elements per chunk of the element-chunk gs kernel
 cudaError_t launch_reduce(const double *part, int64_t count, int nd, double *dst, const int *done, cudaStream_t s);
 cudaError_t launch_gs_local(int64_t nruns, const int32_t *perm, const int32_t *offs, double *v, const int *done,
                             cudaStream_t s);
@@ -267,6 +272,7 @@ struct nek_ctx {
     int32_t *perm = nullptr, *offs = nullptr;
     int64_t nruns = 0, nperm = 0;
     int32_t *gs_p2 = nullptr, *gs_p4 = nullptr, *gs_p8 = nullptr, *gs_pg = nullptr, *gs_og = nullptr;
+    int32_t *gs_coff = nullptr;   // element-chunk offsets of the classes (GsClasses::coff)
     int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
     bool bnd_split = true;                          // concurrent boundary/interior Ax share one wave of CTAs
     bool defer = true;                              // deferred reductions on the single-rank v5 path (NEK_DEFER)

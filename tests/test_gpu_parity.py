@@ -545,3 +545,27 @@ def test_pcg_deferred_reductions_match(nek, graph):
         assert np.all(np.abs(h1 - h0) <= 1e-13 * np.maximum(1.0, h0))
         assert abs(r1 - r0) <= 1e-13 * max(1.0, r0)
         assert rel(x1, x0) <= 1e-13
+
+
+@pytest.mark.parametrize("mesh", ["box", "rod"])
+def test_gs_chunk_order_matches_class_order(nek, mesh):
+    """The element-chunk gs kernel (default) and the class-major one (NEK_GS_CHUNK=0) run the same
+    runs with the same canonical sums: bit-identical, and equal to the oracle's gs (E not a multiple
+    of the chunk size; the rod bundle has runs of other lengths)."""
+    m = mg.box_mesh(5, 3, 3, 7, deform="bubble") if mesh == "box" else mg.rod_bundle(2, 2, 2, 5)
+    u = mg.random_evector(m, seed=21)
+    out = {}
+    for c in ("1", "0"):
+        os.environ["NEK_GS_CHUNK"] = c
+        try:
+            ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+        finally:
+            os.environ.pop("NEK_GS_CHUNK", None)
+        try:
+            v = u.copy()
+            nek.gs(ctx, v)
+            out[c] = v
+        finally:
+            nek.free(ctx)
+    assert np.array_equal(out["1"], out["0"])
+    assert np.array_equal(out["1"], oracle.Oracle.from_mesh(m).gs_apply(u))
