@@ -696,8 +696,11 @@ def main():
                        "n_dof_per_gpu": mesh.n_dof, "n_local_per_gpu": mesh.n_local,
                        "pcg_iters_per_step": args.iters, "h1": 1.0, "h2": args.h2,
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
-                       "parallelism": f"dp{world} (element z-slabs, NCCL halo + allgather reductions)",
-                       "timing": "CUDA graph of 10 PCG iterations per replay, device time by CUDA events",
+                       "parallelism": f"dp{world} (element z-slabs; " + {
+                           0: "one GPU, no exchange)",
+                           1: "NCCL halo send/recv + allgather reductions)",
+                           2: "halo and reductions through NVLink peer memory)"}[info["transport"]],
+                       "timing": f"CUDA graph of {min(args.iters, 20)} PCG iterations per replay, device time by CUDA events",
                        "l2_resident": {"keep": info["l2_keep"], "setaside_bytes": info["l2_setaside"],
                                        "setaside_max": info["l2_setaside_max"]},
                        "setup_s": t_setup},

@@ -1205,7 +1205,9 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
     CK(launch_pcg_init_fin(ctx->sc, ctx->red_all, ctx->nranks, ctx->hist, ctx->s_main));
     ctx->stats.launches += 1;
 
-    const int C = std::max(1, std::min(maxit, 10));
+    // iterations per graph replay: a replay boundary costs ~6 us on the device; a converged solve
+    // overshoots by < C iterations whose kernels return at entry
+    const int C = std::max(1, std::min(maxit, 20));
     const char *genv = getenv("NEK_NO_GRAPH");
     // loopback: the stage syncs swap events between host threads at every exchange, so the iterations
     // are launched directly (a captured graph would freeze one set of cross-rank waits)
