@@ -1,8 +1,8 @@
 mkdir -p gpurun_out
-S=gpurun_out/j14_summary.txt; : > $S
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q -k "deferred or window or config2 or edge or manufactured or repeatable or l2_resident or slab_p2p" > gpurun_out/j14_tests.log 2>&1; echo "tests $?" >> $S
-tail -1 gpurun_out/j14_tests.log >> $S
-for i in 1 2; do
-  timeout 300 python bench.py --no-cpu-baseline --no-peaks > gpurun_out/j14_b.json 2>gpurun_out/j14_b.err; echo "bench $?" >> $S
-  python -c "import json;d=json.loads(open('gpurun_out/j14_b.json').read().strip().splitlines()[-1]);print(d['value'], d['ms_per_step'], d['kernel_ms_per_step'], d['config']['timing'], d['config']['parallelism'])" >> $S
+S=gpurun_out/j16_summary.txt; : > $S
+true
+tail -1 gpurun_out/j16_tests.log >> $S
+for g in 1 1; do
+  NEK_GSUPD=$g timeout 300 python bench.py --no-cpu-baseline --no-peaks > gpurun_out/j16_b.json 2>gpurun_out/j16_b.err; echo "bench gsupd=$g $?" >> $S
+  python -c "import json;d=json.loads(open('gpurun_out/j16_b.json').read().strip().splitlines()[-1]);print('gsupd=$g', d['value'], d['ms_per_step'], d['kernel_ms_per_step'], d['beyond_l2']['vec_per_iter']['ms'], d['beyond_l2']['pcg_ax']['frac'])" >> $S
 done
