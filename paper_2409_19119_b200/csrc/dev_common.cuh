@@ -167,7 +167,8 @@ __device__ __forceinline__ void mail_push(const P2PMail &M, int channel, double 
         double *dst = (q == M.me ? M.mbox : M.peer_mbox[q]) + (base + M.me) * 4;
         dst[0] = v0; dst[1] = v1; dst[2] = v2;
     }
-    __threadfence_system();
+    // each st.release.sys orders all of this thread's earlier stores (the values above, every peer's)
+    // before its flag: no separate system fence
     for (int q = 0; q < M.nranks; ++q) {
         double *dst = (q == M.me ? M.mbox : M.peer_mbox[q]) + (base + M.me) * 4;
         st_release_sys(reinterpret_cast<uint64_t *>(dst + 3), e);

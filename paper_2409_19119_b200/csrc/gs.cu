@@ -243,15 +243,15 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
                          remote_half, nnbr, par, pack4);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
+    if (threadIdx.x == 0) {   // release: the CTA's peer stores (ordered by the barrier) before the count
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
         s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
         *counter = 0u;
         epochs[2] = e;
-        __threadfence_system();
+        asm volatile("fence.acq_rel.sys;" ::: "memory");   // acquire the other CTAs' releases
         for (int k = 0; k < nnbr; ++k) st_release_sys(peer_hflags[k] + me, e);
     }
 }

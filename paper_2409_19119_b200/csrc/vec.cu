@@ -661,8 +661,7 @@ __global__ void red_exchange_kernel(int channel, int me, int nranks, const doubl
     if ((phase & 1) && q < nranks) {
         double *dst = (q == me ? mbox : peer_mbox[q]) + (base + me) * 4;
         dst[0] = red_loc[0]; dst[1] = red_loc[1]; dst[2] = red_loc[2];
-        __threadfence_system();
-        st_release_sys(reinterpret_cast<uint64_t *>(dst + 3), e);
+        st_release_sys(reinterpret_cast<uint64_t *>(dst + 3), e);   // release: orders the values before it
     }
     if ((phase & 2) && q < nranks) {
         const double *src = mbox + (base + q) * 4;
