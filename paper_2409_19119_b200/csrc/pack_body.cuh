@@ -16,9 +16,11 @@ __device__ __forceinline__ void pack_slot(int64_t sidx, const int32_t *__restric
                                           const int64_t *__restrict__ remote_half, int nnbr, int64_t par,
                                           const int4 *__restrict__ pack4)
 {
-    const int run = send_run[sidx];
+    // the slot lists are read every iteration next to the streamed metric factors: keep them in L2
+    const uint64_t keep = tma::policy_evict_last();
+    const int run = (int)tma::ldu(reinterpret_cast<const uint32_t *>(send_run) + sidx, keep);
     T s;
-    const int4 c4 = pack4 ? pack4[sidx] : make_int4(-2, -1, -1, -1);
+    const int4 c4 = pack4 ? tma::ldi4(pack4 + sidx, keep) : make_int4(-2, -1, -1, -1);
     if (c4.x >= 0) {                     // <= 4 local copies, listed per slot (one dependent level)
         s = v[c4.x];
         if (c4.y >= 0) s += v[c4.y];
@@ -30,7 +32,7 @@ __device__ __forceinline__ void pack_slot(int64_t sidx, const int32_t *__restric
         for (int c = o0 + 1; c < o1; ++c) s += v[perm[c]];
     }
     partial[run] = s;
-    const int k = slot_nbr[sidx];
+    const int k = (int)tma::ldu(reinterpret_cast<const uint32_t *>(slot_nbr) + sidx, keep);
     NEK_CHECK(k >= 0 && k < nnbr && sidx >= send_offs[k] && sidx < send_offs[k + 1] && remote_off[k] >= 0 &&
               remote_off[k] + (sidx - send_offs[k]) < remote_half[k]);
     reinterpret_cast<T *>(peer_recv[k])[par * remote_half[k] + remote_off[k] + (sidx - send_offs[k])] = s;
