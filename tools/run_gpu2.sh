@@ -1,7 +1,6 @@
 mkdir -p gpurun_out
-S=gpurun_out/j21_summary.txt; : > $S
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29631 tools/mgpu_timeline.py --graph --iters 20 --tag _j21p2 > gpurun_out/j21_p2.log 2>&1; echo "p2 $?" >> $S
-for i in 1 2; do
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29632 bench.py --gpus 2 --no-pmg --no-cpu-baseline --no-peaks > gpurun_out/j21_b2.json 2> gpurun_out/j21_b2.err; echo "bench2 $?" >> $S
-python -c "import json;d=json.loads(open('gpurun_out/j21_b2.json').read().strip().splitlines()[-1]);print(d['value'], d['ms_per_step'], d['kernel_ms_per_step'])" >> $S
+S=gpurun_out/j22_summary.txt; : > $S
+for w in 2 0 1 3 4 2 0; do
+  NEK_PF_WAVES=$w timeout 300 python bench.py --no-cpu-baseline --no-peaks --no-beyond --no-pmg > gpurun_out/j22_b.json 2>gpurun_out/j22_b.err; echo "bench w=$w $?" >> $S
+  python -c "import json;d=json.loads(open('gpurun_out/j22_b.json').read().strip().splitlines()[-1]);print('w=$w', d['value'], d['ms_per_step'], d['kernel_ms_per_step'], d['roofline']['frac'])" >> $S
 done
