@@ -391,6 +391,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     AxLaunch L;
     L.done = done;
     L.keep = ctx->l2keep;
+    L.pf_min = ctx->v5_pf_min;
     int var = ax_effective_variant(ctx->variant, ctx->N, fused, ctx->l2keep);   // the kernel do_ax launches
     if (fused) {
         L.fused = true;
@@ -946,6 +947,8 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
     {
         const char *denv = getenv("NEK_DEFER");
         ctx->defer = !(denv && std::strcmp(denv, "0") == 0);
+        const char *penv = getenv("NEK_V5_PF_MIN");
+        if (penv) ctx->v5_pf_min = (int64_t)atoll(penv);
     }
     CK(dalloc(ctx, &ctx->red_loc, RED_N));
     if (ctx->nranks > 1) CK(dalloc(ctx, &ctx->red_all, RED_N * ctx->nranks));

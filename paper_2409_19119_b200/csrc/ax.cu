@@ -226,7 +226,7 @@ struct AxV5Smem {
 
 // TMAG: the 24 KB metric block of the element two ahead is brought into a 2-stage
 // shared-memory ring by one TMA bulk copy while this element computes (dynamic smem).
-template <bool HELM, bool FUSED, int MINB, bool TMAG = false>
+template <bool HELM, bool FUSED, int MINB, bool TMAG = false, bool PF = false>
 __global__ void __launch_bounds__(128, MINB)
     ax_v5_kernel(int64_t nelem, int64_t eoff, const int32_t *__restrict__ elist, const double *u,
                  const double *__restrict__ G, const double *__restrict__ wJ, const uint32_t *__restrict__ mbits,
@@ -326,6 +326,8 @@ __global__ void __launch_bounds__(128, MINB)
     for (int64_t it = 0; it < nit; ++it) {
         const int64_t e = e_next;                // element list read one iteration ahead
         if (it + 1 < nit) e_next = elem_at(it + 1);
+        if (PF && !TMAG && t == 0 && it + 1 < nit)   // the next element's metric block toward L2 (large launches)
+            tma::prefetch_l2(G + e_next * 6 * (int64_t)P3, 6 * P3 * 8);
         const double *ue = u + e * P3;
         const double *Ge = G + e * 6 * (int64_t)P3;
         const int par = (int)(it & 1);
@@ -511,15 +513,21 @@ static cudaError_t ax_v5_launch(const AxLaunch &L, const double *u, const double
         }
     }
     const unsigned ctas = L.ctas_total ? L.ctas_total : (unsigned)grid;
-    if (L.fused)
-        ax_v5_kernel<HELM, true, MINB, TMAG><<<(unsigned)grid, 128, dsm, s>>>(
+    // large launches (vectors beyond L2): a bulk L2 prefetch of the next element's metric block, worth its
+    // register-pressure spills there; small ones keep the spill-free kernel
+    const bool pf = !TMAG && L.nelem >= L.pf_min;
+    if (L.fused) {
+        auto k = pf ? ax_v5_kernel<HELM, true, MINB, TMAG, !TMAG> : ax_v5_kernel<HELM, true, MINB, TMAG, false>;
+        k<<<(unsigned)grid, 128, dsm, s>>>(
             L.nelem, L.eoff, L.elist, (const double *)L.p, G, wJ, mbits, h1, h2, w, L.part, L.part_off, L.fin_total,
             L.dst, L.counter, L.done, L.p, L.x, L.r, L.dinv, const_cast<PcgScalars *>(L.sc), L.mail, ctas, L.keep,
             L.upart, L.nupd, L.hist, L.defer);
-    else
-        ax_v5_kernel<HELM, false, MINB, TMAG><<<(unsigned)grid, 128, dsm, s>>>(
+    } else {
+        auto k = pf ? ax_v5_kernel<HELM, false, MINB, TMAG, !TMAG> : ax_v5_kernel<HELM, false, MINB, TMAG, false>;
+        k<<<(unsigned)grid, 128, dsm, s>>>(
             L.nelem, L.eoff, L.elist, u, G, wJ, mbits, h1, h2, w, L.part, L.part_off, L.fin_total, L.dst, L.counter,
             L.done, nullptr, nullptr, nullptr, nullptr, nullptr, L.mail, ctas, L.keep, nullptr, 0, nullptr, 0);
+    }
     return cudaGetLastError();
 }
 

@@ -100,6 +100,8 @@ struct AxLaunch {
     const double *upart = nullptr;
     int nupd = 0;
     int defer = 0;   // DEFER_* bits
+    // v5 launches of at least pf_min elements bulk-prefetch the next element's metric block to L2
+    int64_t pf_min = 16384;
     double *hist = nullptr;
     int variant = -1;                    // >= 0: the Ax variant of this launch (overrides the context's)
 };
@@ -276,6 +278,7 @@ struct nek_ctx {
     int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
     bool bnd_split = true;                          // concurrent boundary/interior Ax share one wave of CTAs
     bool defer = true;                              // deferred reductions on the single-rank v5 path (NEK_DEFER)
+    int64_t v5_pf_min = 16384;                      // AxLaunch::pf_min (NEK_V5_PF_MIN)
     double *upart = nullptr;                        // [upd_blocks][4] update partials the next Ax folds
     int64_t l2_setaside = 0, l2_setaside_max = 0;   // persisting L2 bytes granted / allowed
     bool concurrent_bnd = false;

@@ -569,3 +569,36 @@ def test_gs_chunk_order_matches_class_order(nek, mesh):
             nek.free(ctx)
     assert np.array_equal(out["1"], out["0"])
     assert np.array_equal(out["1"], oracle.Oracle.from_mesh(m).gs_apply(u))
+
+
+def test_v5_l2_prefetch_path_bitwise(nek):
+    """Large N = 7 launches (>= 16384 elements by default) run the v5 kernels that bulk-prefetch the
+    next element's metric block to L2; a prefetch changes no arithmetic.  Forced on a small mesh
+    (NEK_V5_PF_MIN=1): Ax (Poisson and Helmholtz) and a PCG window bit-identical to the default
+    kernels, and Ax within 1e-12 of the oracle."""
+    m = mg.box_mesh(5, 4, 3, 7, deform="bubble")
+    u = mg.random_evector(m, seed=31)
+    b = mg.smooth_field(m, seed=32)
+    out = {}
+    for pf in ("1", None):
+        if pf:
+            os.environ["NEK_V5_PF_MIN"] = pf
+        try:
+            ctx = nek.setup(m.E, m.N, m.xyz, m.gid, m.mask, device=0)
+        finally:
+            os.environ.pop("NEK_V5_PF_MIN", None)
+        try:
+            ws = []
+            for h in ((1.0, 0.0), (1.0, 0.7)):
+                w = np.empty(m.n_local)
+                nek.ax(ctx, h[0], h[1], u, w)
+                ws.append(w)
+            x = np.zeros(m.n_local)
+            st, it, rr, hg = nek.pcg_solve(ctx, 1.0, 0.0, b, x, 0.0, 30, want_hist=True)
+            out[pf] = (ws, x, hg)
+        finally:
+            nek.free(ctx)
+    (w1, x1, h1), (w0, x0, h0) = out["1"], out[None]
+    assert all(np.array_equal(a, c) for a, c in zip(w1, w0))
+    assert np.array_equal(x1, x0) and np.array_equal(h1, h0)
+    assert rel(w1[1], oracle.Oracle.from_mesh(m).apply(1.0, 0.7, u)) <= 1e-12

@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-S=gpurun_out/j22_summary.txt; : > $S
-for w in 2 0 1 3 4 2 0; do
-  NEK_PF_WAVES=$w timeout 300 python bench.py --no-cpu-baseline --no-peaks --no-beyond --no-pmg > gpurun_out/j22_b.json 2>gpurun_out/j22_b.err; echo "bench w=$w $?" >> $S
-  python -c "import json;d=json.loads(open('gpurun_out/j22_b.json').read().strip().splitlines()[-1]);print('w=$w', d['value'], d['ms_per_step'], d['kernel_ms_per_step'], d['roofline']['frac'])" >> $S
-done
+S=gpurun_out/j26_summary.txt; : > $S
+timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -k "prefetch or variants or window or config2 or rod or config3" > gpurun_out/j26_tests.log 2>&1; echo "tests $?" >> $S
+tail -1 gpurun_out/j26_tests.log >> $S
+NEK_LIB_VARIANT=checked timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "prefetch or variants" > gpurun_out/j26_tests_c.log 2>&1; echo "checked $?" >> $S
+tail -1 gpurun_out/j26_tests_c.log >> $S
