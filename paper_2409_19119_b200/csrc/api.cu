@@ -1106,7 +1106,8 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, &m, ctx->l2keep, dp ? 1 : 0));
+                                       ctx->counter + 2, ctx->s_main, &m, ctx->l2keep, dp ? 1 : 0,
+                                       ctx->E >= ctx->v5_pf_min));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
         if (dp) return NEK_OK;
@@ -1126,7 +1127,7 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
         Scope sc(ctx, CLS_VEC);
         CK(launch_pcg_update_deferred(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->part,
                                       (int)ax_grid(var, ctx->N, ctx->E), ctx->sc, ctx->upart, upd_blocks(),
-                                      ctx->l2keep, ctx->s_main));
+                                      ctx->l2keep, ctx->s_main, ctx->E >= ctx->v5_pf_min));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         return NEK_OK;
     }
@@ -1138,7 +1139,8 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
             Scope sc(ctx, CLS_VEC);
             CK(launch_pcg_update_fused(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->red_all, ctx->nranks,
                                        ctx->sc, ctx->hist, ctx->part, upd_blocks(), ctx->red_loc + RED_RHO,
-                                       ctx->counter + 2, ctx->s_main, nullptr, ctx->l2keep));
+                                       ctx->counter + 2, ctx->s_main, nullptr, ctx->l2keep, 0,
+                                       ctx->E >= ctx->v5_pf_min));
             ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         }
         if (ctx->nranks > 1) {

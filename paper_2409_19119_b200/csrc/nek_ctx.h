@@ -154,12 +154,12 @@ cudaError_t launch_pcg_init(int64_t n, const uint32_t *mbits, const uint32_t *ob
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail = nullptr, int keep = 0, int defer = 0);
+                                    const P2PMail *mail = nullptr, int keep = 0, int defer = 0, bool pf = false);
 // deferred reductions (single rank, N = 7): sigma folded from the Ax's nax partials at entry, (rho', rr)
 // partials left in upart ([nblk][4]) for the next Ax or for pcg_defer_finish
 cudaError_t launch_pcg_update_deferred(int64_t n, const uint32_t *obits, const double *dinv, const double *w,
                                        double *r, const double *axpart, int nax, PcgScalars *sc, double *upart,
-                                       int nblk, int keep, cudaStream_t s);
+                                       int nblk, int keep, cudaStream_t s, bool pf = false);
 // the bookkeeping of the last update of a solve when no Ax followed it
 cudaError_t launch_pcg_defer_finish(PcgScalars *sc, const double *upart, int nupd, double *hist, cudaStream_t s,
                                     const P2PMail *mail = nullptr);

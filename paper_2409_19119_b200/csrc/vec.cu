@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     pcg_update_fused_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                             const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ red_all,
                             int nranks, PcgScalars *sc, double *hist, double *__restrict__ part, double *dst,
-                            unsigned int *counter, P2PMail mail, int keep, int defer)
+                            unsigned int *counter, P2PMail mail, int keep, int defer, int pf)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ int s_last;
@@ -386,6 +386,15 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
     double g0 = 0.0, k0 = 0.0, g1 = 0.0, k1 = 0.0;   // the .y points: two independent Dot2 chains per dot
     for (bool first = true; base < n2; base += (int64_t)gridDim.x * tile, first = false) {
+        if (pf && threadIdx.x == 0) {   // vectors beyond L2: this CTA's next tile of w, r, Dinv toward L2
+            const int64_t nb = base - threadIdx.x + (int64_t)gridDim.x * tile;
+            if (nb < n2) {
+                const uint32_t bytes = (uint32_t)(16 * (nb + tile <= n2 ? tile : n2 - nb));
+                tma::prefetch_l2(w + 2 * nb, bytes);
+                tma::prefetch_l2(r + 2 * nb, bytes);
+                tma::prefetch_l2(dinv + 2 * nb, bytes);
+            }
+        }
         if (!first) load(base);
 #pragma unroll
         for (int q = 0; q < UNR; ++q) {
@@ -428,20 +437,20 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
 cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const double *dinv, const double *w, double *r,
                                     const double *red_all, int nranks, PcgScalars *sc, double *hist, double *part,
                                     int nblk, double *dst, unsigned int *counter, cudaStream_t s,
-                                    const P2PMail *mail, int keep, int defer)
+                                    const P2PMail *mail, int keep, int defer, bool pf)
 {
     P2PMail m;
     if (mail) m = *mail;
     const int per_sm = nblk / device_sms();
     if (per_sm >= 8)
         pcg_update_fused_kernel<2, 8><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
-                                                                   part, dst, counter, m, keep, defer);
+                                                                   part, dst, counter, m, keep, defer, pf ? 1 : 0);
     else if (per_sm >= 4)
         pcg_update_fused_kernel<2, 4><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
-                                                                   part, dst, counter, m, keep, defer);
+                                                                   part, dst, counter, m, keep, defer, pf ? 1 : 0);
     else
         pcg_update_fused_kernel<4, 2><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
-                                                                   part, dst, counter, m, keep, defer);
+                                                                   part, dst, counter, m, keep, defer, pf ? 1 : 0);
     return cudaGetLastError();
 }
 
@@ -464,7 +473,7 @@ __device__ __forceinline__ double fold_pairs(const double *part, int count, doub
 __global__ void __launch_bounds__(VEC_THREADS, 2)
     pcg_update_deferred_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                                const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ axpart,
-                               int nax, PcgScalars *sc, double *__restrict__ upart, int keep)
+                               int nax, PcgScalars *sc, double *__restrict__ upart, int keep, int pf)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ double s_sig;
@@ -506,6 +515,15 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
     }
     double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0, g0 = 0.0, k0 = 0.0, g1 = 0.0, k1 = 0.0;
     for (bool first = true; base < n2; base += (int64_t)gridDim.x * tile, first = false) {
+        if (pf && threadIdx.x == 0) {   // vectors beyond L2: this CTA's next tile of w, r, Dinv toward L2
+            const int64_t nb = base - threadIdx.x + (int64_t)gridDim.x * tile;
+            if (nb < n2) {
+                const uint32_t bytes = (uint32_t)(16 * (nb + tile <= n2 ? tile : n2 - nb));
+                tma::prefetch_l2(w + 2 * nb, bytes);
+                tma::prefetch_l2(r + 2 * nb, bytes);
+                tma::prefetch_l2(dinv + 2 * nb, bytes);
+            }
+        }
         if (!first) load(base);
 #pragma unroll
         for (int q = 0; q < UNR; ++q) {
@@ -531,9 +549,10 @@ __global__ void __launch_bounds__(VEC_THREADS, 2)
 
 cudaError_t launch_pcg_update_deferred(int64_t n, const uint32_t *obits, const double *dinv, const double *w,
                                        double *r, const double *axpart, int nax, PcgScalars *sc, double *upart,
-                                       int nblk, int keep, cudaStream_t s)
+                                       int nblk, int keep, cudaStream_t s, bool pf)
 {
-    pcg_update_deferred_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, axpart, nax, sc, upart, keep);
+    pcg_update_deferred_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, axpart, nax, sc, upart, keep,
+                                                           pf ? 1 : 0);
     return cudaGetLastError();
 }
 
