@@ -138,6 +138,18 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p)
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// relaxed system-scope accesses: no fence of their own (one fence.acq_rel.sys orders a batch)
+__device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v)
+{
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t *p)
+{
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ uint64_t globaltimer_ns()
 {
     uint64_t t;
@@ -148,8 +160,8 @@ __device__ __forceinline__ bool wait_epoch(const uint64_t *flag, uint64_t e, int
 {
     if (ld_acquire_sys(flag) >= e) return true;
     const uint64_t t0 = globaltimer_ns();
-    for (int it = 0;; ++it) {
-        if (ld_acquire_sys(flag) >= e) return true;
+    for (int it = 0;; ++it) {   // poll relaxed (no L1 invalidation per poll), acquire once it is there
+        if (ld_relaxed_sys(flag) >= e) return ld_acquire_sys(flag) >= e;
         if (it > 64) __nanosleep(64);
         if ((it & 255) == 0 && globaltimer_ns() - t0 > timeout_ns) break;
     }
@@ -167,11 +179,11 @@ __device__ __forceinline__ void mail_push(const P2PMail &M, int channel, double 
         double *dst = (q == M.me ? M.mbox : M.peer_mbox[q]) + (base + M.me) * 4;
         dst[0] = v0; dst[1] = v1; dst[2] = v2;
     }
-    // each st.release.sys orders all of this thread's earlier stores (the values above, every peer's)
-    // before its flag: no separate system fence
+    // one system-scope release fence orders the values above (every peer's) before all the flags
+    fence_acq_rel_sys();
     for (int q = 0; q < M.nranks; ++q) {
         double *dst = (q == M.me ? M.mbox : M.peer_mbox[q]) + (base + M.me) * 4;
-        st_release_sys(reinterpret_cast<uint64_t *>(dst + 3), e);
+        st_relaxed_sys(reinterpret_cast<uint64_t *>(dst + 3), e);
     }
 }
 

@@ -251,8 +251,8 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
     if (s_last && threadIdx.x == 0) {
         *counter = 0u;
         epochs[2] = e;
-        asm volatile("fence.acq_rel.sys;" ::: "memory");   // acquire the other CTAs' releases
-        for (int k = 0; k < nnbr; ++k) st_release_sys(peer_hflags[k] + me, e);
+        fence_acq_rel_sys();   // acquire the other CTAs' releases, release everything before the flags
+        for (int k = 0; k < nnbr; ++k) st_relaxed_sys(peer_hflags[k] + me, e);
     }
 }
 
