@@ -150,6 +150,8 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t *p)
     return v;
 }
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// the release / acquire halves of the last-CTA reductions (cheaper than __threadfence's fence.sc.gpu)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ uint64_t globaltimer_ns()
 {
     uint64_t t;
@@ -247,12 +249,12 @@ __device__ __forceinline__ void last_block_finish(double *part, int64_t count, d
                                                   unsigned int ctas_total = 0)
 {
     if (threadIdx.x == 0) {
-        __threadfence();
+        fence_acq_rel_gpu();
         *s_last = atomicAdd(counter, 1u) == (ctas_total ? ctas_total : gridDim.x) - 1;
     }
     __syncthreads();
     if (*s_last) {
-        __threadfence();
+        fence_acq_rel_gpu();
         double hi = 0.0, lo = 0.0;
         for (int64_t c = threadIdx.x; c < count; c += blockDim.x)
             dd_add(hi, lo, ((volatile double *)part)[2 * c], ((volatile double *)part)[2 * c + 1]);

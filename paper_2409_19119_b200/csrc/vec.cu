@@ -111,12 +111,12 @@ __device__ __forceinline__ void last_block_finish2(double *part, int nblk, doubl
                                                    double *sred, int *s_last)
 {
     if (threadIdx.x == 0) {
-        __threadfence();
+        fence_acq_rel_gpu();
         *s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (*s_last) {
-        __threadfence();
+        fence_acq_rel_gpu();
         double a0, a1;
         fold_part2(part, nblk, sred, a0, a1);
         if (threadIdx.x == 0) { dst[0] = a0; dst[1] = a1; *counter = 0u; }
@@ -417,12 +417,12 @@ __global__ void __launch_bounds__(VEC_THREADS, MINB)
     dd_add(h1, l1, g1, k1);
     store_part2(part, h0, l0, h1, l1, sred);
     if (threadIdx.x == 0) {
-        __threadfence();
+        fence_acq_rel_gpu();
         s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (s_last) {
-        __threadfence();
+        fence_acq_rel_gpu();
         double b0, b1;
         fold_part2(part, (int)gridDim.x, sred, b0, b1);
         if (threadIdx.x == 0) {
