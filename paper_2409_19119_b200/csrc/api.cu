@@ -423,7 +423,20 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
     int64_t g1 = ax_grid(var, ctx->N, nb), g2 = ax_grid(var, ctx->N, ni);
     if (split) {
         const int64_t wave = ax_grid(var, ctx->N, ctx->E);
-        g1 = std::min<int64_t>(nb, std::max<int64_t>(1, std::min<int64_t>((nb + 3) / 4, wave / 4)));
+        if (ctx->bnd_epc > 0) {   // NEK_BND_EPC: boundary elements per boundary CTA
+            const int64_t epc = ctx->bnd_epc;
+            g1 = std::min<int64_t>(nb, std::max<int64_t>(1, std::min<int64_t>((nb + epc - 1) / epc, wave / 4)));
+        } else {
+            // the split that finishes first: the interior launch takes ceil(ni / g2) element rounds, the
+            // halo is ready after ceil(nb / g1) rounds plus the pack (~1.7 rounds, measured); the gs waits
+            // for both.  Ties: the larger boundary share (the halo earlier).
+            double best = 1e30;
+            for (int64_t c1 = 1; c1 < wave && c1 <= nb; ++c1) {
+                const int64_t c2 = wave - c1;
+                const double T = std::max<double>((double)((ni + c2 - 1) / c2), (double)((nb + c1 - 1) / c1) + 1.7);
+                if (T <= best) { best = T; g1 = c1; }
+            }
+        }
         g2 = std::min<int64_t>(ni, std::max<int64_t>(1, wave - g1));
     }
     const bool push = fused && dot && ctx->p2p;   // the finalising CTA sends sigma to every rank itself
@@ -850,6 +863,8 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         ctx->concurrent_bnd = cenv ? std::strcmp(cenv, "1") == 0 : E < 16384;
         const char *senv = getenv("NEK_BND_SPLIT");
         ctx->bnd_split = !(senv && std::strcmp(senv, "0") == 0);
+        const char *eenv = getenv("NEK_BND_EPC");
+        ctx->bnd_epc = eenv ? std::max(0, atoi(eenv)) : 0;
     }
     ctx->nifc = (int64_t)p->ifc_offs.size() - 1; ctx->nifc_perm = (int64_t)p->ifc_perm.size();
     CK(upload(ctx, &ctx->ifc_perm, p->ifc_perm));

@@ -243,8 +243,8 @@ __global__ void gs_pack_p2p_fused_kernel(int64_t nslots, const int32_t *__restri
                          remote_half, nnbr, par, pack4);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {   // release: the CTA's peer stores (ordered by the barrier) before the count
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
+    if (threadIdx.x == 0) {   // release (GPU scope): the CTA's peer stores, ordered by the barrier, before
+        fence_acq_rel_gpu();  // the count; the last CTA's system-scope fence below is cumulative over them
         s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();

@@ -277,6 +277,7 @@ struct nek_ctx {
     int32_t *gs_coff = nullptr;   // element-chunk offsets of the classes (GsClasses::coff)
     int l2keep = 0;                                 // L2-resident PCG vectors (AxLaunch::keep bits)
     bool bnd_split = true;                          // concurrent boundary/interior Ax share one wave of CTAs
+    int bnd_epc = 0;                                // boundary elements per boundary CTA (NEK_BND_EPC; 0 = model)
     bool defer = true;                              // deferred reductions on the single-rank v5 path (NEK_DEFER)
     int64_t v5_pf_min = 16384;                      // AxLaunch::pf_min (NEK_V5_PF_MIN)
     double *upart = nullptr;                        // [upd_blocks][4] update partials the next Ax folds
