@@ -165,7 +165,12 @@ int nek_gs(nek_ctx *ctx, double *v, void *stream);
  *   hist      out (host, nullable): maxit+1 entries, hist[k] = ||r_k||/||M b|| for k <= iters.
  * Returns NEK_OK (converged; also b = 0 -> x = 0, iters = 0), NEK_MAXIT,
  * NEK_ENOTSPD (x holds the last iterate), or an error.  The call synchronises
- * `stream` (convergence is polled from the device every few iterations).
+ * `stream` (convergence is polled from the device after every CUDA-graph replay of
+ * 20 iterations; iterations past convergence return at kernel entry).
+ * Schedule (reading 25): the bookkeeping of iteration k (beta, the history
+ * entry, the convergence and maxit tests) runs at the start of the iteration-(k+1)
+ * operator launch, from the residual update's partial sums -- the same values as a
+ * separate bookkeeping step; NEK_DEFER=0 restores the separate step.
  * L2 residency: when the PCG vectors fit in the L2 (nek_info_t.l2_keep), the
  * call raises the DEVICE-WIDE persisting-L2 limit (cudaLimitPersistingL2CacheSize)
  * for its duration and restores the previous value before returning; kernels of
