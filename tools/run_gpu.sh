@@ -16,7 +16,7 @@ if [ "$mode" = tests ]; then
 fi
 if [ "$mode" = ncu ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 2 --warmup 1 --no-pmg --no-peaks --no-cpu-baseline --no-beyond > gpurun_out/${tag}_ncu_launch.log 2>&1; echo "launches $?" >> gpurun_out/${tag}_summary.txt
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gs_classes_kernel|pcg_update_fused|ax_v5" -s 30 -c 3 -o gpurun_out/${tag}_full python tools/prof_step.py --solves 2 --iters 8 --ax 0 > gpurun_out/${tag}_ncu_full.log 2>&1; echo "full $?" >> gpurun_out/${tag}_summary.txt
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gs_chunk|pcg_update|ax_v5" -s 30 -c 3 -o gpurun_out/${tag}_full python tools/prof_step.py --solves 2 --iters 8 --ax 0 > gpurun_out/${tag}_ncu_full.log 2>&1; echo "full $?" >> gpurun_out/${tag}_summary.txt
 fi
 if [ "$mode" = mgpu ]; then
   n=${3:-2}
