@@ -403,7 +403,7 @@ static int apply_op(nek_ctx *ctx, double h1, double h2, const double *u, double 
         L.nelem = ctx->E;
         if (dot) { L.part = ctx->part; L.fin_total = ax_grid(var, ctx->N, ctx->E); }
         if (dot && fused && use_defer(ctx)) {
-            L.fin_total = 0; L.upart = ctx->upart; L.nupd = upd_blocks(); L.hist = ctx->hist;
+            L.fin_total = 0; L.upart = ctx->upart; L.nupd = upd_blocks_deferred(); L.hist = ctx->hist;
             L.defer = DEFER_FOLD | DEFER_BOOK;
         }
         if ((st = do_ax(ctx, h1, h2, u, w, L)) != NEK_OK) return st;
@@ -958,7 +958,7 @@ static int setup_impl(nek_ctx *ctx, int64_t E, int N, const double *xyz, const i
         }
     }
     CK(dalloc(ctx, &ctx->part, ctx->npart));
-    CK(dalloc(ctx, &ctx->upart, 4 * (int64_t)upd_blocks()));
+    CK(dalloc(ctx, &ctx->upart, 4 * (int64_t)std::max(upd_blocks(), upd_blocks_deferred())));
     {
         const char *denv = getenv("NEK_DEFER");
         ctx->defer = !(denv && std::strcmp(denv, "0") == 0);
@@ -1141,7 +1141,7 @@ static int pcg_iteration(nek_ctx *ctx, double h1, double h2)
         const int var = ax_effective_variant(ctx->variant, ctx->N, true, ctx->l2keep);
         Scope sc(ctx, CLS_VEC);
         CK(launch_pcg_update_deferred(ctx->n, ctx->obits, ctx->vdinv, ctx->vw, ctx->vr, ctx->part,
-                                      (int)ax_grid(var, ctx->N, ctx->E), ctx->sc, ctx->upart, upd_blocks(),
+                                      (int)ax_grid(var, ctx->N, ctx->E), ctx->sc, ctx->upart, upd_blocks_deferred(),
                                       ctx->l2keep, ctx->s_main, ctx->E >= ctx->v5_pf_min));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
         return NEK_OK;
@@ -1292,7 +1292,7 @@ int nek_pcg_solve(nek_ctx *ctx, double h1, double h2, const double *b, double *x
         }
     }
     if (use_defer(ctx)) {   // the last update's (rho', rr) when no Ax followed it
-        CK(launch_pcg_defer_finish(ctx->sc, ctx->upart, upd_blocks(), ctx->hist, ctx->s_main));
+        CK(launch_pcg_defer_finish(ctx->sc, ctx->upart, upd_blocks_deferred(), ctx->hist, ctx->s_main));
         ctx->stats.launches += 1; ctx->stats.vec_launches += 1;
     } else if (use_defer_p2p(ctx)) {
         if ((st = lb_stage_sync(ctx, ctx->s_main)) != NEK_OK) return st;   // loopback: (rho', rr) pushed

@@ -224,6 +224,7 @@ cudaError_t launch_pcg_pupdate(int64_t n, const double *dinv, const double *r, d
                                cudaStream_t s);
 int vec_blocks();
 int upd_blocks();
+int upd_blocks_deferred();   // CTAs of the single-rank deferred residual update
 int device_sms();   // multiprocessors of the current device (cached per device)
 
 // makef.cu: dealiased advection (NEXT #4)

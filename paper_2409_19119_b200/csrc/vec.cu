@@ -64,6 +64,19 @@ int device_sms()
 int vec_blocks() { return 4 * device_sms(); }
 // residual update: 2 CTAs per SM with 4 double2 per thread per tile (NEK_UPD_CTAS = 4 or 8: that many CTAs
 // per SM with 2 double2 per thread per tile; measurement switch)
+// the single-rank deferred update (no last CTA, 3 double2 per thread): 3 CTAs per SM (measured: config 2
+// 5.87-5.89 vs 5.92 ms at 2 per SM, 16x16x128 0.82 vs 0.78 of the copy peak); NEK_UPD_CTAS overrides
+int upd_blocks_deferred()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NEK_UPD_CTAS");
+        v = e ? atoi(e) : 3;
+        if (v != 2 && v != 3 && v != 4) v = 3;
+    }
+    return v * device_sms();
+}
+
 int upd_blocks()
 {
     static int v = -1;
@@ -470,14 +483,14 @@ __device__ __forceinline__ double fold_pairs(const double *part, int count, doub
     return __dadd_rn(hi, lo);
 }
 
-__global__ void __launch_bounds__(VEC_THREADS, 2)
+template <int UNR, int MINB>
+__global__ void __launch_bounds__(VEC_THREADS, MINB)
     pcg_update_deferred_kernel(int64_t n, const uint32_t *__restrict__ obits, const double *__restrict__ dinv,
                                const double *__restrict__ w, double *__restrict__ r, const double *__restrict__ axpart,
                                int nax, PcgScalars *sc, double *__restrict__ upart, int keep, int pf)
 {
     __shared__ double sred[VEC_THREADS];
     __shared__ double s_sig;
-    constexpr int UNR = 4;
     const uint64_t pol = tma::policy_keep(keep & 1);
     const int64_t n2 = n >> 1;
     const int64_t tile = (int64_t)UNR * blockDim.x;
@@ -551,8 +564,16 @@ cudaError_t launch_pcg_update_deferred(int64_t n, const uint32_t *obits, const d
                                        double *r, const double *axpart, int nax, PcgScalars *sc, double *upart,
                                        int nblk, int keep, cudaStream_t s, bool pf)
 {
-    pcg_update_deferred_kernel<<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, axpart, nax, sc, upart, keep,
-                                                           pf ? 1 : 0);
+    const int per_sm = nblk / device_sms();
+    if (per_sm >= 4)
+        pcg_update_deferred_kernel<2, 4><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, axpart, nax, sc, upart,
+                                                                     keep, pf ? 1 : 0);
+    else if (per_sm == 3)
+        pcg_update_deferred_kernel<3, 3><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, axpart, nax, sc, upart,
+                                                                     keep, pf ? 1 : 0);
+    else
+        pcg_update_deferred_kernel<4, 2><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, axpart, nax, sc, upart,
+                                                                     keep, pf ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -1,9 +1,8 @@
 mkdir -p gpurun_out
-S=gpurun_out/j38_summary.txt; : > $S
-NEK_BND_ONE=1 NEK_P2P_TIMEOUT_MS=5000 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29631 tools/mgpu_check.py > gpurun_out/j38_mgpu.log 2>&1; echo "mgpu one $?" >> $S
-grep -o '"ok": [a-z]*' gpurun_out/j38_mgpu.log | head -3 >> $S
-for o in 1 0 1 0; do
-NEK_BND_ONE=$o NEK_P2P_TIMEOUT_MS=5000 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29632 bench.py --gpus 2 --no-pmg --no-cpu-baseline --no-peaks --no-beyond > gpurun_out/j38_b2.json 2> gpurun_out/j38_b2.err; echo "bench2 one=$o $?" >> $S
-python -c "import json;d=json.loads(open('gpurun_out/j38_b2.json').read().strip().splitlines()[-1]);print('one=$o', d['value'], d['ms_per_step'])" >> $S
+S=gpurun_out/j40_summary.txt; : > $S
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q -k "deferred or window or config2 or edge or manufactured or prefetch or repeatable or l2_resident or slab_p2p" > gpurun_out/j40_t.log 2>&1; echo "tests $?" >> $S
+tail -1 gpurun_out/j40_t.log >> $S
+for i in 1 2; do
+  timeout 300 python bench.py --no-cpu-baseline --no-peaks --no-pmg > gpurun_out/j40_b.json 2>gpurun_out/j40_b.err; echo "bench $?" >> $S
+  python -c "import json;d=json.loads(open('gpurun_out/j40_b.json').read().strip().splitlines()[-1]);print(d['value'], d['ms_per_step'], d['kernel_ms_per_step']['vec_ms'], 'big', d['beyond_l2']['vec_per_iter']['frac'], d['gpu_launches'])" >> $S
 done
-NEK_BND_ONE=1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29633 tools/mgpu_timeline.py --graph --iters 20 --tag _j38p2 > gpurun_out/j38_p2.log 2>&1; echo "p2 $?" >> $S
