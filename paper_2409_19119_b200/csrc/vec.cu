@@ -83,7 +83,7 @@ int upd_blocks()
     if (v < 0) {
         const char *e = getenv("NEK_UPD_CTAS");
         v = e ? atoi(e) : 2;
-        if (v != 2 && v != 4 && v != 8) v = 2;
+        if (v != 2 && v != 3 && v != 4 && v != 8) v = 2;
     }
     return v * device_sms();
 }
@@ -455,7 +455,10 @@ cudaError_t launch_pcg_update_fused(int64_t n, const uint32_t *obits, const doub
     P2PMail m;
     if (mail) m = *mail;
     const int per_sm = nblk / device_sms();
-    if (per_sm >= 8)
+    if (per_sm == 3)
+        pcg_update_fused_kernel<3, 3><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
+                                                                   part, dst, counter, m, keep, defer, pf ? 1 : 0);
+    else if (per_sm >= 8)
         pcg_update_fused_kernel<2, 8><<<nblk, VEC_THREADS, 0, s>>>(n, obits, dinv, w, r, red_all, nranks, sc, hist,
                                                                    part, dst, counter, m, keep, defer, pf ? 1 : 0);
     else if (per_sm >= 4)
